@@ -328,7 +328,7 @@ static int cmp_key_desc(const void* pa, const void* pb) {
 int orc_apply_compulsory_quota(const double* probs, const double* c_hat_row, int S, int N, int* expert,
                                double* gate, double* score, unsigned char* kept, long long* counts,
                                long long* dropped) {
-  double* share = (double*)malloc(sizeof(double) * (size_t)N);
+  double* share = (double*)calloc((size_t)N + 1, sizeof(double));
   long long* quota = (long long*)malloc(sizeof(long long) * (size_t)N);
   key_t_* order = (key_t_*)malloc(sizeof(key_t_) * (size_t)(S + 1));
   key_t_* er = (key_t_*)malloc(sizeof(key_t_) * (size_t)N);
