@@ -78,6 +78,85 @@ int tamoe_grouped_dgrad(const void* grad_tokens, const void* w, int G, int M, in
 int tamoe_grouped_wgrad(const void* a_tokens, const void* b_tokens, int G, int M, int N, int R,
                         const int* seg_start, const int* seg_rows, void* out, void* stream);
 
+/* ------------------------------------------------------------------ device router
+ * The reference's routing operators on the device: gate_forward (gate.cpp:30-32) and topk_route
+ * (gate.cpp:91-202) for P logical processes of S tokens, N experts, top-k (k <= 8). */
+typedef struct tamoe_router tamoe_router;
+
+/* Readable routing arrays (tamoe_router_read / tamoe_layer_read). */
+#define TAMOE_R_IDX 0         /* int32  [P*S*k] expert of each pick (pick = token*k + slot) */
+#define TAMOE_R_GATE 1        /* fp32   [P*S*k] combine weight (gate_value) */
+#define TAMOE_R_SCORE 2       /* fp64   [P*S*k] raw selection probability */
+#define TAMOE_R_KEPT 3        /* uint8  [P*S*k] */
+#define TAMOE_R_POS 4         /* int32  [P*S*k] row in the expert-sorted buffer, -1 if dropped */
+#define TAMOE_R_COUNTS 5      /* int32  [P*N] kept per (process, expert) */
+#define TAMOE_R_DROPPED 6     /* int32  [P*N] */
+#define TAMOE_R_MEAN_PROBS 7  /* fp64   [P*N] column means of the softmax */
+#define TAMOE_R_SEG_START 8   /* int32  [N] padded row segment of each expert */
+#define TAMOE_R_SEG_ROWS 9    /* int32  [N] */
+#define TAMOE_R_CLIST 10      /* int32  [P*S*k] kept picks, expert-major, (process, token) order */
+#define TAMOE_R_LIST_START 11 /* int32  [N] start of each expert's range in CLIST */
+#define TAMOE_R_BAD 12        /* int32  [1] non-zero if a gate logit was non-finite */
+#define TAMOE_R_LOGITS 13     /* fp32   [P*S*N] (layer only) */
+
+int tamoe_router_create(int P, int S, int N, int k, tamoe_router** out);
+int tamoe_router_destroy(tamoe_router* r);
+/* topk_route on device fp64 probabilities [P*S*N]; caps = tamoe_capacity_caps() output (host int64 [P*N]). */
+int tamoe_router_route_probs(tamoe_router* r, const double* probs, int mode, const long long* caps, void* stream);
+/* gate_forward + topk_route fused: x bf16 [P*S x d], wg bf16 [P x n_pad x d] (n_pad = round_up(N,16), pad rows 0).
+ * logits (fp32 [P*S x N]) and probs (fp64 [P*S x N]) are optional device outputs.  Raises status 2 on a
+ * non-finite logit (gate.cpp:16). */
+int tamoe_router_route_gate(tamoe_router* r, const void* x, const void* wg, int n_pad, int d, float* logits,
+                            double* probs, int mode, const long long* caps, void* stream);
+/* Gather token rows into the padded expert-sorted buffer xp [r_max x d] (pad rows zeroed). */
+int tamoe_router_permute(tamoe_router* r, const void* x, int d, void* xp, int r_max, void* stream);
+/* Copy a routing array (TAMOE_R_*) to host or device memory; synchronises the stream. */
+int tamoe_router_read(tamoe_router* r, int what, void* dst, long long bytes, void* stream);
+
+/* ------------------------------------------------------------------ the MoE layer (trainer.cpp:243-356)
+ * One step = gate -> route (capacity) -> permute -> experts -> combine -> task MSE + aux loss ->
+ * backward (expert dgrad/wgrad, combine-weight Jacobian, softmax backward, dWg, optional dX).
+ * No optimizer update (the reference's SGD, trainer.cpp:410-416, is the caller's). */
+typedef struct tamoe_layer tamoe_layer;
+
+typedef struct {
+  int P;          /* logical processes on this device (reference P when world_size == 1) */
+  int S;          /* tokens per process */
+  int d, d_out;   /* d % 256 == 0, d_out % 128 == 0 */
+  int N, k;       /* experts (<= 256), top-k (<= 8) */
+  int f;          /* 0: linear expert U_e (reference); > 0: FFN d -> f -> d_out, f % 256 == 0 */
+  int act;        /* TAMOE_ACT_* (FFN only) */
+  int cap_mode;   /* TAMOE_CAP_* */
+  double capacity_factor;
+  int aux_kind;   /* TAMOE_LOSS_* */
+  double aux_weight;
+  int penalty_norm;
+  double temperature;
+  int need_dx;    /* compute dL/dx (not in the reference) */
+  int world_size, rank;
+} tamoe_layer_config;
+
+typedef struct {
+  const void* x;   /* bf16 [P*S x d] */
+  const void* y;   /* bf16 [P*S x d_out] regression targets (trainer.cpp:290-296) */
+  const void* wg;  /* bf16 [P x n_pad x d] gate weights (reference W_i transposed, pad rows zero) */
+  const void* w1;  /* linear: bf16 [E x d_out x d] = U_e^T;  FFN: bf16 [E x f x d] */
+  const void* w2;  /* FFN: bf16 [E x d_out x f] */
+  float* dwg;      /* fp32 [P x n_pad x d] */
+  void* dw1;       /* bf16, shape of w1 */
+  void* dw2;       /* bf16, shape of w2 */
+  void* dx;        /* bf16 [P*S x d] when need_dx */
+  void* y_hat;     /* optional bf16 [P*S x d_out] */
+  double* losses;  /* device fp64[2]: task MSE, aux loss (this device's share) */
+} tamoe_layer_io;
+
+/* c_hat: host fp64 [P_global x N] dispatch target (required for topo loss / proportional capacity). */
+int tamoe_layer_create(const tamoe_layer_config* cfg, const double* c_hat, tamoe_layer** out);
+int tamoe_layer_destroy(tamoe_layer* l);
+int tamoe_layer_step(tamoe_layer* l, const tamoe_layer_io* io, void* stream);
+int tamoe_layer_read(tamoe_layer* l, int what, void* dst, long long bytes, void* stream);
+int tamoe_layer_n_pad(int N);
+
 #ifdef __cplusplus
 }
 #endif

@@ -6,9 +6,69 @@
 
 #include "capi_util.hpp"
 #include "expert.hpp"
+#include "gate.hpp"
 #include "host_topology.hpp"
+#include "layer.hpp"
+#include "route.hpp"
 
 using namespace tamoe;
+
+struct tamoe_router {
+  Router impl;
+  tamoe_router(int P, int S, int N, int k) : impl(P, S, N, k) {}
+};
+struct tamoe_layer {
+  Layer impl;
+  tamoe_layer(const LayerConfig& c, const double* ch) : impl(c, ch) {}
+};
+
+namespace {
+
+struct ReadSpec {
+  const void* src;
+  long long bytes;
+};
+
+ReadSpec route_array(const RouteWorkspace& rw, int what, const float* logits) {
+  const RouteDims& d = rw.dims;
+  const RouteBuffers& b = rw.buf;
+  const long long picks = d.picks(), pn = static_cast<long long>(d.P) * d.N;
+  switch (what) {
+    case TAMOE_R_IDX: return {b.idx, picks * 4};
+    case TAMOE_R_GATE: return {b.gate, picks * 4};
+    case TAMOE_R_SCORE: return {b.score, picks * 8};
+    case TAMOE_R_KEPT: return {b.kept, picks};
+    case TAMOE_R_POS: return {b.pos, picks * 4};
+    case TAMOE_R_COUNTS: return {b.counts, pn * 4};
+    case TAMOE_R_DROPPED: return {b.dropped, pn * 4};
+    case TAMOE_R_MEAN_PROBS: return {b.mean_probs, pn * 8};
+    case TAMOE_R_SEG_START: return {b.seg_start, d.N * 4LL};
+    case TAMOE_R_SEG_ROWS: return {b.seg_rows, d.N * 4LL};
+    case TAMOE_R_CLIST: return {b.clist, picks * 4};
+    case TAMOE_R_LIST_START: return {b.list_start, d.N * 4LL};
+    case TAMOE_R_BAD: return {b.bad, 4};
+    case TAMOE_R_LOGITS:
+      require(logits != nullptr, "logits are only kept by the layer");
+      return {logits, static_cast<long long>(d.P) * d.S * d.N * 4};
+    default: throw ValidationError("unknown routing array id");
+  }
+}
+
+void read_array(const RouteWorkspace& rw, int what, void* dst, long long bytes, cudaStream_t s, const float* lg) {
+  ReadSpec r = route_array(rw, what, lg);
+  require(dst != nullptr && bytes >= r.bytes, "read: destination too small");
+  TAMOE_CUDA(cudaMemcpyAsync(dst, r.src, r.bytes, cudaMemcpyDefault, s));
+  TAMOE_CUDA(cudaStreamSynchronize(s));
+}
+
+void check_bad(const RouteWorkspace& rw, cudaStream_t s) {
+  int bad = 0;
+  TAMOE_CUDA(cudaMemcpyAsync(&bad, rw.buf.bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  TAMOE_CUDA(cudaStreamSynchronize(s));
+  require(bad == 0, "non-finite gate logit");
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -82,5 +142,93 @@ int tamoe_grouped_wgrad(const void* a_tokens, const void* b_tokens, int G, int M
                   R, seg_start, seg_rows, static_cast<__nv_bfloat16*>(out), static_cast<cudaStream_t>(stream));
   });
 }
+
+int tamoe_router_create(int P, int S, int N, int k, tamoe_router** out) {
+  return guarded([&] {
+    require(out != nullptr, "router_create: null out");
+    *out = new tamoe_router(P, S, N, k);
+  });
+}
+
+int tamoe_router_destroy(tamoe_router* r) {
+  return guarded([&] { delete r; });
+}
+
+int tamoe_router_route_probs(tamoe_router* r, const double* probs, int mode, const long long* caps, void* stream) {
+  return guarded([&] {
+    require(r && probs && caps, "route_probs: null argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    RouteWorkspace& rw = r->impl.rw;
+    rw.upload_caps(caps, s);
+    route_rows_from_probs(probs, rw.dims, rw.row_out(nullptr, nullptr), s);
+    rw.finish(mode, s);
+  });
+}
+
+int tamoe_router_route_gate(tamoe_router* r, const void* x, const void* wg, int n_pad, int d, float* logits,
+                            double* probs, int mode, const long long* caps, void* stream) {
+  return guarded([&] {
+    require(r && x && wg && caps, "route_gate: null argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    RouteWorkspace& rw = r->impl.rw;
+    rw.upload_caps(caps, s);
+    TAMOE_CUDA(cudaMemsetAsync(rw.buf.bad, 0, sizeof(int), s));
+    gate_forward(static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(wg), n_pad, rw.dims, d,
+                 rw.row_out(logits, probs), s);
+    check_bad(rw, s);
+    rw.finish(mode, s);
+  });
+}
+
+int tamoe_router_permute(tamoe_router* r, const void* x, int d, void* xp, int r_max, void* stream) {
+  return guarded([&] {
+    require(r && x && xp, "permute: null argument");
+    RouteWorkspace& rw = r->impl.rw;
+    route_permute(rw.dims, rw.buf, static_cast<const __nv_bfloat16*>(x), d, static_cast<__nv_bfloat16*>(xp), r_max,
+                  nullptr, 0, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int tamoe_router_read(tamoe_router* r, int what, void* dst, long long bytes, void* stream) {
+  return guarded([&] {
+    require(r != nullptr, "read: null router");
+    read_array(r->impl.rw, what, dst, bytes, static_cast<cudaStream_t>(stream), nullptr);
+  });
+}
+
+int tamoe_layer_create(const tamoe_layer_config* cfg, const double* c_hat, tamoe_layer** out) {
+  return guarded([&] {
+    require(cfg && out, "layer_create: null argument");
+    LayerConfig c{cfg->P, cfg->S, cfg->d, cfg->d_out, cfg->N, cfg->k, cfg->f, cfg->act, cfg->cap_mode,
+                  cfg->capacity_factor, cfg->aux_kind, cfg->aux_weight, cfg->penalty_norm, cfg->temperature,
+                  cfg->need_dx, cfg->world_size, cfg->rank};
+    *out = new tamoe_layer(c, c_hat);
+  });
+}
+
+int tamoe_layer_destroy(tamoe_layer* l) {
+  return guarded([&] { delete l; });
+}
+
+int tamoe_layer_step(tamoe_layer* l, const tamoe_layer_io* io, void* stream) {
+  return guarded([&] {
+    require(l && io, "layer_step: null argument");
+    LayerIO x{static_cast<const __nv_bfloat16*>(io->x), static_cast<const __nv_bfloat16*>(io->y),
+              static_cast<const __nv_bfloat16*>(io->wg), static_cast<const __nv_bfloat16*>(io->w1),
+              static_cast<const __nv_bfloat16*>(io->w2), io->dwg, static_cast<__nv_bfloat16*>(io->dw1),
+              static_cast<__nv_bfloat16*>(io->dw2), static_cast<__nv_bfloat16*>(io->dx),
+              static_cast<__nv_bfloat16*>(io->y_hat), io->losses};
+    l->impl.step(x, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int tamoe_layer_read(tamoe_layer* l, int what, void* dst, long long bytes, void* stream) {
+  return guarded([&] {
+    require(l != nullptr, "read: null layer");
+    read_array(l->impl.route(), what, dst, bytes, static_cast<cudaStream_t>(stream), l->impl.logits());
+  });
+}
+
+int tamoe_layer_n_pad(int N) { return (N + 15) & ~15; }
 
 }  // extern "C"

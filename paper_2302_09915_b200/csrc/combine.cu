@@ -1,0 +1,121 @@
+// Weighted gather-combine fused with the reference's task loss and the first
+// backward step (trainer.cpp:290-316):
+//   y_hat_t = sum_{kept slots} g_slot * O[pos(t, slot)]           (combine)
+//   r_t     = y_hat_t - y_t ;  task += |r_t|^2                      (MSE)
+//   dO[pos] = (2 / (P S d_out)) * g_slot * r_t                       (combine backward, scattered
+//                                                                     straight into expert order)
+//   dldg    = (2 / (P S d_out)) * <r_t, O[pos]>                      (gate-value gradient)
+// One warp per token, 16-byte vectors, fp32 math on bf16 rows.
+#include <cuda_bf16.h>
+
+#include "combine.hpp"
+#include "common.hpp"
+#include "route.hpp"
+
+namespace tamoe {
+
+namespace {
+
+constexpr int kCombWarps = 8;
+
+__device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint4 v;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  return v;
+}
+
+__global__ void __launch_bounds__(kCombWarps * 32) combine_loss_kernel(CombineArgs a) {
+  __shared__ double wsum[kCombWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long t = static_cast<long long>(blockIdx.x) * kCombWarps + warp;
+  double lsum = 0.0;
+  if (t < a.T) {
+    const int k = a.k;
+    int rows[kMaxTopK];
+    float g[kMaxTopK], dot[kMaxTopK];
+#pragma unroll
+    for (int j = 0; j < kMaxTopK; ++j) {
+      rows[j] = (j < k) ? a.pos[t * k + j] : -1;
+      g[j] = (j < k) ? a.gate[t * k + j] : 0.f;
+      dot[j] = 0.f;
+    }
+    const int nv = a.dout / 8;
+    const uint4* y4 = reinterpret_cast<const uint4*>(a.y + t * a.dout);
+    for (int v = lane; v < nv; v += 32) {
+      float yh[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) yh[i] = 0.f;
+      float o[kMaxTopK][8];
+#pragma unroll
+      for (int j = 0; j < kMaxTopK; ++j) {
+        if (rows[j] >= 0) {
+          unpack8(reinterpret_cast<const uint4*>(a.O + static_cast<long long>(rows[j]) * a.dout)[v], o[j]);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) yh[i] += g[j] * o[j][i];
+        }
+      }
+      if (a.y_hat) reinterpret_cast<uint4*>(a.y_hat + t * a.dout)[v] = pack8(yh);
+      float yy[8], r[8];
+      unpack8(y4[v], yy);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        r[i] = yh[i] - yy[i];
+        lsum += static_cast<double>(r[i]) * r[i];
+      }
+#pragma unroll
+      for (int j = 0; j < kMaxTopK; ++j) {
+        if (rows[j] >= 0) {
+          float go[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            dot[j] += r[i] * o[j][i];
+            go[i] = a.mse_scale * g[j] * r[i];
+          }
+          reinterpret_cast<uint4*>(a.dO + static_cast<long long>(rows[j]) * a.dout)[v] = pack8(go);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxTopK; ++j) {
+      if (j < k) {
+        float s = dot[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) a.dldg[t * k + j] = rows[j] >= 0 ? a.mse_scale * s : 0.f;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+  if (lane == 0) wsum[warp] = lsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kCombWarps; ++w) s += wsum[w];
+    a.loss_part[blockIdx.x] = s;
+  }
+}
+
+}  // namespace
+
+int combine_blocks(long long T) { return static_cast<int>((T + kCombWarps - 1) / kCombWarps); }
+
+void combine_loss(const CombineArgs& a, cudaStream_t s) {
+  require(a.dout % 8 == 0, "combine: d_out must be a multiple of 8");
+  require(a.k >= 1 && a.k <= kMaxTopK, "combine: k out of range");
+  combine_loss_kernel<<<combine_blocks(a.T), kCombWarps * 32, 0, s>>>(a);
+  TAMOE_CUDA(cudaGetLastError());
+}
+
+}  // namespace tamoe

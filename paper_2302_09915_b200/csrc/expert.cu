@@ -16,6 +16,7 @@
 #include "common.hpp"
 #include "expert.hpp"
 #include "gemm_sm100.cuh"
+#include "gemm_launch.cuh"
 #include "tma_host.hpp"
 
 namespace tamoe {
@@ -110,22 +111,6 @@ struct EpiWgrad {
   }
 };
 
-template <int kMode, int BN, bool A_MN, bool B_MN, class Epi>
-static void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
-                        const typename Epi::Params& ep, int grid_limit, cudaStream_t s) {
-  auto kern = gemm_sm100_kernel<kMode, BN, A_MN, B_MN, Epi>;
-  const int smem = GemmSmem<BN>::kTotal;
-  static bool configured = false;
-  if (!configured) {
-    TAMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = true;
-  }
-  int grid = num_sms();
-  if (grid_limit > 0 && grid_limit < grid) grid = grid_limit;
-  kern<<<grid, kGemmThreads, smem, s>>>(ta, tb, p, ep);
-  TAMOE_CUDA(cudaGetLastError());
-}
-
 static void check_groups(int G) { require(G >= 1 && G <= kMaxGroups, "group count out of range [1, 1024]"); }
 
 void grouped_fwd(const __nv_bfloat16* tokens, const __nv_bfloat16* w, int G, int M, int K, int R,
@@ -136,7 +121,7 @@ void grouped_fwd(const __nv_bfloat16* tokens, const __nv_bfloat16* w, int G, int
   require(K % 64 == 0, "grouped_fwd: K must be a multiple of 64");
   CUtensorMap ta = make_tmap_bf16(w, K, static_cast<uint64_t>(G) * M, K, kBM);
   CUtensorMap tb = make_tmap_bf16(tokens, K, R, K, 256);
-  GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1};
+  GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1};
   EpiSwap::Params ep{out, pre_out, nullptr, M, act, kActNone};
   launch_gemm<kModeSwap, 256, false, false, EpiSwap>(ta, tb, p, ep, 0, s);
 }
@@ -150,7 +135,7 @@ void grouped_dgrad(const __nv_bfloat16* grad_tokens, const __nv_bfloat16* w, int
   require(K % 64 == 0, "grouped_dgrad: K must be a multiple of 64");
   CUtensorMap ta = make_tmap_bf16(w, M, static_cast<uint64_t>(G) * K, M, 64);
   CUtensorMap tb = make_tmap_bf16(grad_tokens, K, R, K, 256);
-  GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1};
+  GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1};
   EpiSwap::Params ep{out, nullptr, pre_in, M, kActNone, pre_in ? act : kActNone};
   launch_gemm<kModeSwap, 256, true, false, EpiSwap>(ta, tb, p, ep, 0, s);
 }
@@ -163,7 +148,7 @@ void grouped_wgrad(const __nv_bfloat16* a_tokens, const __nv_bfloat16* b_tokens,
   require(N % 256 == 0, "grouped_wgrad: N must be a multiple of 256");
   CUtensorMap ta = make_tmap_bf16(a_tokens, M, R, M, 64);
   CUtensorMap tb = make_tmap_bf16(b_tokens, N, R, N, 64);
-  GemmParams p{G, seg_start, seg_rows, M, N, 0, 1, 1, 1};
+  GemmParams p{G, seg_start, seg_rows, M, N, 0, 1, 1, 1, 1};
   EpiWgrad::Params ep{out};
   launch_gemm<kModeWgrad, 256, true, true, EpiWgrad>(ta, tb, p, ep, 0, s);
 }

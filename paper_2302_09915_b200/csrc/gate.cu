@@ -1,0 +1,135 @@
+// Fused gate: logits = x . Wg^T on tcgen05 (TMA-staged, fp32 accumulate in
+// TMEM), then per token in the epilogue: fp64 softmax exactly as the reference
+// (max-subtract, exp, sequential sum over experts, divide: gate.cpp:12-28),
+// streaming top-k (gate.cpp:117-134), per-warp expert histograms and
+// probability partial sums for the aux loss (gate.cpp:115).
+//
+// Replaces gate_forward (gate.cpp:30-32) + the per-token part of topk_route.
+#include <cuda_bf16.h>
+
+#include <cmath>
+
+#include "common.hpp"
+#include "gate.hpp"
+#include "gemm_launch.cuh"
+#include "route_row.cuh"
+#include "tma_host.hpp"
+
+namespace tamoe {
+
+struct EpiGate {
+  struct Params {
+    RowRouteOut o;
+    int N, k, S, TB;
+  };
+  static __device__ __forceinline__ void run(const Params& e, const GemmParams& p, const TileInfo& ti,
+                                             uint32_t tmem_tile, int q, int lane) {
+    const int row = q * 32 + lane;
+    const int tok = ti.m0 + row;
+    const bool valid = tok < e.S;
+    const long long gtok = static_cast<long long>(ti.g) * e.S + tok;
+    const int tile_warp = (ti.g * e.TB + ti.m0 / kBM) * 4 + q;
+    const int N = e.N;
+    // pass 1: max (and the non-finite check of gate.cpp:16)
+    float mx = -INFINITY;
+    bool finite = true;
+    for (int c0 = 0; c0 < N; c0 += 32) {
+      float v[32];
+      load_acc32(tmem_tile, c0, v);
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        if (c0 + c < N) {
+          finite &= isfinite(v[c]);
+          mx = fmaxf(mx, v[c]);
+          if (valid && e.o.logits) e.o.logits[gtok * N + c0 + c] = v[c];
+        }
+      }
+    }
+    if (valid && !finite) atomicOr(e.o.bad, 1);
+    const double dmx = valid ? static_cast<double>(mx) : 0.0;
+    // pass 2: denominator, sequential in expert order
+    double denom = 0.0;
+    for (int c0 = 0; c0 < N; c0 += 32) {
+      float v[32];
+      load_acc32(tmem_tile, c0, v);
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        if (c0 + c < N) denom += valid ? exp(static_cast<double>(v[c]) - dmx) : 0.0;
+    }
+    // pass 3: probabilities, top-k, probability sums
+    TopK tk;
+    tk.init();
+    double* msum = e.o.msum4 + static_cast<long long>(tile_warp) * N;
+    for (int c0 = 0; c0 < N; c0 += 32) {
+      float v[32];
+      load_acc32(tmem_tile, c0, v);
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        if (c0 + c < N) {
+          const double pr = valid ? exp(static_cast<double>(v[c]) - dmx) / denom : 0.0;
+          if (valid && e.o.probs) e.o.probs[gtok * N + c0 + c] = pr;
+          tk.insert(pr, c0 + c, e.k);
+          const double s = warp_sum_f64(pr);
+          if (lane == 0) msum[c0 + c] = s;
+        }
+      }
+    }
+    finish_row(tk, valid, gtok, e.k, N, tile_warp, e.o, lane);
+  }
+};
+
+// Standalone router over caller-provided fp64 probabilities (the reference's topk_route input).
+__global__ void __launch_bounds__(kRouteTile) route_rows_kernel(const double* __restrict__ probs, RouteDims d,
+                                                               RowRouteOut o) {
+  const int tile = blockIdx.x;
+  const int proc = tile / d.TB;
+  const int tok = (tile % d.TB) * kRouteTile + threadIdx.x;
+  const bool valid = tok < d.S;
+  const long long gtok = static_cast<long long>(proc) * d.S + tok;
+  const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile_warp = tile * 4 + q;
+  TopK tk;
+  tk.init();
+  double* msum = o.msum4 + static_cast<long long>(tile_warp) * d.N;
+  const double* row = probs + gtok * d.N;
+  for (int e = 0; e < d.N; ++e) {
+    const double pr = valid ? row[e] : 0.0;
+    tk.insert(pr, e, d.k);
+    const double s = warp_sum_f64(pr);
+    if (lane == 0) msum[e] = s;
+  }
+  finish_row(tk, valid, gtok, d.k, d.N, tile_warp, o, lane);
+}
+
+void route_rows_from_probs(const double* probs, const RouteDims& d, const RowRouteOut& o, cudaStream_t s) {
+  require(d.k >= 1 && d.k <= kMaxTopK && d.k <= d.N, "k must be in [1, min(N, 8)]");
+  route_rows_kernel<<<d.tiles(), kRouteTile, 0, s>>>(probs, d, o);
+  TAMOE_CUDA(cudaGetLastError());
+}
+
+template <int BN>
+static void gate_launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, const EpiGate::Params& ep,
+                        cudaStream_t s) {
+  launch_gemm<kModeGate, BN, false, false, EpiGate>(ta, tb, p, ep, 0, s);
+}
+
+void gate_forward(const __nv_bfloat16* x, const __nv_bfloat16* wg, int n_pad, const RouteDims& d, int dm,
+                  const RowRouteOut& o, cudaStream_t s) {
+  require(d.k >= 1 && d.k <= kMaxTopK && d.k <= d.N, "k must be in [1, min(N, 8)]");
+  require(dm % 64 == 0, "gate: d must be a multiple of 64 (pad with zeros)");
+  require(n_pad % 16 == 0 && n_pad >= d.N && n_pad <= 256, "gate: n_pad must be round_up(N, 16) <= 256");
+  const int BNsel = n_pad <= 32 ? 32 : (n_pad <= 64 ? 64 : (n_pad <= 128 ? 128 : 256));
+  const long long T = static_cast<long long>(d.P) * d.S;
+  CUtensorMap ta = make_tmap_bf16(x, dm, T, dm, kBM);
+  CUtensorMap tb = make_tmap_bf16(wg, dm, static_cast<uint64_t>(d.P) * n_pad, dm, BNsel);
+  GemmParams p{1, nullptr, nullptr, 0, n_pad, dm, 1, d.S, n_pad, d.P};
+  EpiGate::Params ep{o, d.N, d.k, d.S, d.TB};
+  switch (BNsel) {
+    case 32: gate_launch<32>(ta, tb, p, ep, s); break;
+    case 64: gate_launch<64>(ta, tb, p, ep, s); break;
+    case 128: gate_launch<128>(ta, tb, p, ep, s); break;
+    default: gate_launch<256>(ta, tb, p, ep, s); break;
+  }
+}
+
+}  // namespace tamoe

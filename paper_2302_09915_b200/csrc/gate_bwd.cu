@@ -1,0 +1,290 @@
+// Gate backward (trainer.cpp:318-355, gate.cpp:257-287):
+//   dpi_t  = combine-weight Jacobian of dldg (top-1: dpi[e0] += dldg; top-k: renormalisation
+//            Jacobian with the raw scores) + (w / P) * coeff  (coeff = topo or balance coefficients
+//            of the kept counts, stop-gradient);
+//   dz_t   = pi_t * (dpi_t - <dpi_t, pi_t>)                          (softmax backward)
+//   dWg    = x^T dz            (tcgen05, split-K over tokens, fixed-order reduction)
+//   dX     = dz Wg + sum_slots dX_perm[pos]     (tcgen05 GEMM whose epilogue gathers the expert
+//                                                path's input gradient back to token order)
+// plus the loss finalisation (task MSE, aux loss: trainer.cpp:334-345, 360-361).
+#include <cuda_bf16.h>
+
+#include <cmath>
+
+#include "common.hpp"
+#include "gate_bwd.hpp"
+#include "gemm_launch.cuh"
+#include "route.hpp"
+#include "tma_host.hpp"
+
+namespace tamoe {
+
+namespace {
+
+constexpr int kDzWarps = 8;
+constexpr int kMaxNPerLane = 8;  // N <= 256
+
+__global__ void __launch_bounds__(kDzWarps * 32) gate_dz_kernel(GateDzArgs a) {
+  extern __shared__ double coeff[];  // [P*N]
+  const int N = a.N;
+  const double s2 = static_cast<double>(a.S) * a.S;
+  for (int i = threadIdx.x; i < a.P * N; i += blockDim.x) {
+    const double c = static_cast<double>(a.counts[i]);
+    coeff[i] = a.aux_kind == 1 ? (static_cast<double>(N) * a.P_global / s2) * a.penalties[i] * c : c / s2;
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    // loss finalisation (one warp): task = sum residual^2 / (P S d_out); aux = mean over processes
+    const int lane = threadIdx.x;
+    double task = 0.0;
+    for (int i = lane; i < a.n_loss_part; i += 32) task += a.loss_part[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) task += __shfl_xor_sync(0xffffffffu, task, o);
+    double aux = 0.0;
+    for (int pr = 0; pr < a.P; ++pr) {
+      double l = 0.0;
+      for (int e = lane; e < N; e += 32) {
+        const double frac = static_cast<double>(a.counts[pr * N + e]) / a.S;
+        l += (a.aux_kind == 1 ? a.penalties[pr * N + e] : 1.0) * a.mean_probs[pr * N + e] * frac;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+      aux += a.aux_kind == 1 ? static_cast<double>(N) * a.P_global * l : l;
+    }
+    if (lane == 0) {
+      a.losses[0] = task / (static_cast<double>(a.P_global) * a.S * a.dout);
+      a.losses[1] = aux / a.P_global;
+    }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long t = static_cast<long long>(blockIdx.x) * kDzWarps + warp;
+  if (t >= static_cast<long long>(a.P) * a.S) return;
+  const int proc = static_cast<int>(t / a.S);
+  const int k = a.k;
+  // softmax of the stored fp32 logits (fp32 math, max-subtracted)
+  float l[kMaxNPerLane], p[kMaxNPerLane], dpi[kMaxNPerLane];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < kMaxNPerLane; ++i) {
+    const int e = lane + 32 * i;
+    l[i] = e < N ? a.logits[t * N + e] : -INFINITY;
+    mx = fmaxf(mx, l[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float den = 0.f;
+#pragma unroll
+  for (int i = 0; i < kMaxNPerLane; ++i) {
+    p[i] = (lane + 32 * i < N) ? expf(l[i] - mx) : 0.f;
+    den += p[i];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
+  const float inv = 1.f / den;
+  const float aux_scale = static_cast<float>(a.aux_weight / a.P_global);
+#pragma unroll
+  for (int i = 0; i < kMaxNPerLane; ++i) {
+    const int e = lane + 32 * i;
+    p[i] *= inv;
+    dpi[i] = e < N ? aux_scale * static_cast<float>(coeff[proc * N + e]) : 0.f;
+  }
+  // combine-weight Jacobian (trainer.cpp:318-331)
+  int ex[kMaxTopK];
+  float add[kMaxTopK];
+  double mass = 0.0;
+#pragma unroll
+  for (int j = 0; j < kMaxTopK; ++j) {
+    ex[j] = j < k ? a.idx[t * k + j] : -1;
+    if (j < k) mass += a.score[t * k + j];
+  }
+  if (k == 1) {
+    add[0] = a.dldg[t];
+#pragma unroll
+    for (int j = 1; j < kMaxTopK; ++j) add[j] = 0.f;
+  } else {
+#pragma unroll
+    for (int l2 = 0; l2 < kMaxTopK; ++l2) {
+      double acc = 0.0;
+      if (l2 < k) {
+#pragma unroll
+        for (int j = 0; j < kMaxTopK; ++j) {
+          if (j < k) {
+            const double dg = a.dldg[t * k + j];
+            if (dg != 0.0) acc += dg * ((j == l2 ? mass : 0.0) - a.score[t * k + j]) / (mass * mass);
+          }
+        }
+      }
+      add[l2] = static_cast<float>(acc);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kMaxNPerLane; ++i) {
+    const int e = lane + 32 * i;
+#pragma unroll
+    for (int j = 0; j < kMaxTopK; ++j) dpi[i] += (ex[j] == e) ? add[j] : 0.f;
+  }
+  float dot = 0.f;
+#pragma unroll
+  for (int i = 0; i < kMaxNPerLane; ++i) dot += dpi[i] * p[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+  __nv_bfloat16* dz = a.dz + t * a.n64;
+#pragma unroll
+  for (int i = 0; i < kMaxNPerLane; ++i) {
+    const int e = lane + 32 * i;
+    if (e < a.n64) dz[e] = __float2bfloat16(e < N ? p[i] * (dpi[i] - dot) : 0.f);
+  }
+}
+
+// dWg partials: acc[m = d index][n = expert] -> part[((ks * P + proc) * n64 + n) * d + m]
+struct EpiGateDw {
+  struct Params {
+    float* part;
+    int d, n64, P;
+  };
+  static __device__ __forceinline__ void run(const Params& e, const GemmParams& p, const TileInfo& ti,
+                                             uint32_t tmem_tile, int q, int lane) {
+    const int m = ti.m0 + q * 32 + lane;
+    for (int c0 = 0; c0 < ti.n; c0 += 32) {
+      float v[32];
+      if (ti.k_len > 0) {
+        load_acc32(tmem_tile, c0, v);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = 0.f;
+      }
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        const int n = ti.n0 + c0 + c;
+        e.part[((static_cast<long long>(ti.ks) * e.P + ti.g) * e.n64 + n) * e.d + m] = v[c];
+      }
+    }
+  }
+};
+
+__global__ void dwg_reduce_kernel(const float* __restrict__ part, int splits, int P, int n64, int n_pad, int d,
+                                  int N, float* __restrict__ dwg) {
+  const long long total = static_cast<long long>(P) * n_pad * d;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int m = static_cast<int>(i % d);
+    const int n = static_cast<int>((i / d) % n_pad);
+    const int proc = static_cast<int>(i / (static_cast<long long>(d) * n_pad));
+    float s = 0.f;
+    if (n < N)
+      for (int ks = 0; ks < splits; ++ks) s += part[((static_cast<long long>(ks) * P + proc) * n64 + n) * d + m];
+    dwg[i] = s;
+  }
+}
+
+// dX: acc[token][d col] + gathered expert-path input gradients
+struct EpiGateDx {
+  struct Params {
+    __nv_bfloat16* dx;
+    const __nv_bfloat16* dxp;
+    const int* pos;
+    int k, S, d;
+  };
+  static __device__ __forceinline__ void run(const Params& e, const GemmParams& p, const TileInfo& ti,
+                                             uint32_t tmem_tile, int q, int lane) {
+    const int tok = ti.m0 + q * 32 + lane;
+    const bool valid = tok < e.S;  // tcgen05.ld is warp-collective: every lane runs the loop
+    const long long gtok = static_cast<long long>(ti.g) * e.S + tok;
+    int rows[kMaxTopK];
+#pragma unroll
+    for (int j = 0; j < kMaxTopK; ++j) rows[j] = (valid && j < e.k) ? e.pos[gtok * e.k + j] : -1;
+    for (int c0 = 0; c0 < ti.n; c0 += 32) {
+      float v[32];
+      load_acc32(tmem_tile, c0, v);
+      const int col = ti.n0 + c0;
+#pragma unroll
+      for (int j = 0; j < kMaxTopK; ++j) {
+        if (rows[j] >= 0) {
+          const uint4* src = reinterpret_cast<const uint4*>(e.dxp + static_cast<long long>(rows[j]) * e.d + col);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint4 w = src[u];
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float2 f = __bfloat1622float2(h[i]);
+              v[8 * u + 2 * i] += f.x;
+              v[8 * u + 2 * i + 1] += f.y;
+            }
+          }
+        }
+      }
+      if (!valid) continue;
+      uint4* dst = reinterpret_cast<uint4*>(e.dx + gtok * e.d + col);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        uint4 w;
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&w);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[8 * u + 2 * i], v[8 * u + 2 * i + 1]);
+        dst[u] = w;
+      }
+    }
+  }
+};
+
+}  // namespace
+
+void gate_dz(const GateDzArgs& a, cudaStream_t s) {
+  require(a.N <= 32 * kMaxNPerLane, "gate backward: N must be <= 256");
+  require(a.k >= 1 && a.k <= kMaxTopK, "gate backward: k out of range");
+  const long long T = static_cast<long long>(a.P) * a.S;
+  const int blocks = static_cast<int>((T + kDzWarps - 1) / kDzWarps);
+  gate_dz_kernel<<<blocks, kDzWarps * 32, sizeof(double) * a.P * a.N, s>>>(a);
+  TAMOE_CUDA(cudaGetLastError());
+}
+
+int gate_dw_splits(int P, int S, int d, int n64) {
+  const int tiles_per_split = P * (d / 128) * (n64 / 64);
+  int splits = (num_sms() + tiles_per_split - 1) / tiles_per_split;
+  const int max_split = (S + 63) / 64;
+  if (splits > max_split) splits = max_split;
+  return splits < 1 ? 1 : splits;
+}
+
+void gate_dw(const __nv_bfloat16* x, const __nv_bfloat16* dz, int P, int S, int d, int n64, int n_pad, int N,
+             float* part, int splits, float* dwg, cudaStream_t s) {
+  require(d % 128 == 0, "gate dW: d must be a multiple of 128");
+  require(n64 % 64 == 0, "gate dW: dz width must be a multiple of 64");
+  require(P == 1 || S % 16 == 0, "gate dW: S must be a multiple of 16 when several processes share a device");
+  const long long T = static_cast<long long>(P) * S;
+  CUtensorMap ta = make_tmap_bf16(x, d, T, d, 64);     // A = x^T (MN-major)
+  CUtensorMap tb = make_tmap_bf16(dz, n64, T, n64, 64);  // B = dz   (MN-major)
+  GemmParams p{1, nullptr, nullptr, d, 64, 0, splits, S, 0, P};
+  // one 64-column N block per launch keeps BN = 64 (n64 > 64 loops over column blocks)
+  EpiGateDw::Params ep{part, d, n64, P};
+  if (n64 == 64) {
+    launch_gemm<kModeGateDw, 64, true, true, EpiGateDw>(ta, tb, p, ep, 0, s);
+  } else {
+    require(n64 == 256 || n64 == 128, "gate dW: unsupported expert padding");
+    if (n64 == 128) {
+      p.Nw = 128;
+      launch_gemm<kModeGateDw, 128, true, true, EpiGateDw>(ta, tb, p, ep, 0, s);
+    } else {
+      p.Nw = n64;
+      launch_gemm<kModeGateDw, 256, true, true, EpiGateDw>(ta, tb, p, ep, 0, s);
+    }
+  }
+  const long long total = static_cast<long long>(P) * n_pad * d;
+  const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 4096));
+  dwg_reduce_kernel<<<blocks, 256, 0, s>>>(part, splits, P, n64, n_pad, d, N, dwg);
+  TAMOE_CUDA(cudaGetLastError());
+}
+
+void gate_dx(const __nv_bfloat16* dz, const __nv_bfloat16* wg, int P, int S, int d, int n64, int n_pad,
+             const __nv_bfloat16* dxp, const int* pos, int k, __nv_bfloat16* dx, cudaStream_t s) {
+  require(d % 256 == 0, "gate dX: d must be a multiple of 256");
+  const long long T = static_cast<long long>(P) * S;
+  CUtensorMap ta = make_tmap_bf16(dz, n64, T, n64, 128);                         // A = dz (K-major)
+  CUtensorMap tb = make_tmap_bf16(wg, d, static_cast<uint64_t>(P) * n_pad, d, 64);  // B = Wg (MN-major)
+  GemmParams p{1, nullptr, nullptr, 0, d, n_pad, 1, S, n_pad, P};
+  EpiGateDx::Params ep{dx, dxp, pos, k, S, d};
+  launch_gemm<kModeGateDx, 256, false, true, EpiGateDx>(ta, tb, p, ep, 0, s);
+}
+
+}  // namespace tamoe

@@ -37,9 +37,10 @@ struct GemmParams {
   const int* seg_start;  // [G] first (padded) row of group g in the token buffers
   const int* seg_rows;   // [G] padded row count (multiple of 16)
   int Mw, Nw, Kw;        // see GemmMode
-  int k_split;           // kModeGateDw
+  int k_split;           // kModeGateDw: K splits per process
   int tokens_per_proc;   // rows per logical process (gate modes)
   int w_rows_per_proc;   // weight rows per process (gate modes)
+  int procs;             // logical processes (gate modes)
 };
 
 struct TileInfo {
@@ -75,11 +76,11 @@ __device__ __forceinline__ int group_tiles(const GemmParams& p, int g) {
   } else if constexpr (kMode == kModeWgrad) {
     return (p.Mw / kBM) * (p.Nw / BN);
   } else if constexpr (kMode == kModeGate) {
-    return ceil_div(p.Mw, kBM);
+    return p.procs * ceil_div(p.tokens_per_proc, kBM);
   } else if constexpr (kMode == kModeGateDw) {
-    return (p.Mw / kBM) * (p.Nw / BN) * p.k_split;
+    return p.procs * (p.Mw / kBM) * (p.Nw / BN) * p.k_split;
   } else {
-    return ceil_div(p.Mw, kBM) * (p.Nw / BN);
+    return p.procs * ceil_div(p.tokens_per_proc, kBM) * (p.Nw / BN);
   }
 }
 
@@ -115,35 +116,46 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, const int* pref
     ti.ax = ti.m0; ti.ay = p.seg_start[g];
     ti.bx = ti.n0; ti.by = p.seg_start[g];
   } else if constexpr (kMode == kModeGate) {
-    ti.m0 = r * kBM;
+    // tile r -> (process, 128-token block); rows beyond the process' S are masked by the epilogue
+    const int tb = ceil_div(p.tokens_per_proc, kBM);
+    const int proc = r / tb;
+    ti.g = proc;
+    ti.m0 = (r % tb) * kBM;
     ti.n0 = 0;
     ti.n = BN;
     ti.k_len = p.Kw;
-    const int proc = ti.m0 / p.tokens_per_proc;
-    ti.ax = 0; ti.ay = ti.m0;
+    ti.ax = 0; ti.ay = proc * p.tokens_per_proc + ti.m0;
     ti.bx = 0; ti.by = proc * p.w_rows_per_proc;
   } else if constexpr (kMode == kModeGateDw) {
+    // tile r -> (process, split, m block, n block); K = the process' tokens
     const int nb = p.Nw / BN;
     const int per_split = (p.Mw / kBM) * nb;
-    ti.ks = r / per_split;
-    const int rr = r % per_split;
+    const int per_proc = per_split * p.k_split;
+    const int proc = r / per_proc;
+    const int rr0 = r % per_proc;
+    ti.g = proc;
+    ti.ks = rr0 / per_split;
+    const int rr = rr0 % per_split;
     ti.m0 = (rr / nb) * kBM;
     ti.n0 = (rr % nb) * BN;
     ti.n = BN;
-    const int chunk = ceil_div(ceil_div(p.Kw, p.k_split), kBK) * kBK;
+    const int chunk = ceil_div(ceil_div(p.tokens_per_proc, p.k_split), kBK) * kBK;
     const int kb = ti.ks * chunk;
-    ti.k_len = max(0, min(p.Kw, kb + chunk) - kb);
+    ti.k_len = max(0, min(p.tokens_per_proc, kb + chunk) - kb);
     ti.k_len = (ti.k_len + 15) & ~15;
-    ti.ax = ti.m0; ti.ay = kb;
-    ti.bx = ti.n0; ti.by = kb;
-  } else {  // kModeGateDx
+    ti.ax = ti.m0; ti.ay = proc * p.tokens_per_proc + kb;
+    ti.bx = ti.n0; ti.by = proc * p.tokens_per_proc + kb;
+  } else {  // kModeGateDx: tile r -> (process, 128-token block, n block)
     const int nb = p.Nw / BN;
-    ti.m0 = (r / nb) * kBM;
-    ti.n0 = (r % nb) * BN;
+    const int tb = ceil_div(p.tokens_per_proc, kBM);
+    const int proc = r / (tb * nb);
+    const int rr = r % (tb * nb);
+    ti.g = proc;
+    ti.m0 = (rr / nb) * kBM;
+    ti.n0 = (rr % nb) * BN;
     ti.n = BN;
     ti.k_len = p.Kw;
-    const int proc = ti.m0 / p.tokens_per_proc;
-    ti.ax = 0; ti.ay = ti.m0;
+    ti.ax = 0; ti.ay = proc * p.tokens_per_proc + ti.m0;
     ti.bx = ti.n0; ti.by = proc * p.w_rows_per_proc;
   }
 }

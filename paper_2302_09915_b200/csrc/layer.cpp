@@ -1,0 +1,208 @@
+// TA-MoE layer step orchestration (trainer.cpp:371-482 on the device):
+//   gate (tcgen05) -> bucket -> capacity -> permute -> expert FFN (tcgen05 grouped) ->
+//   combine + MSE + dO -> expert dgrad / wgrad (tcgen05 grouped) -> gate backward.
+#include "layer.hpp"
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <vector>
+
+#include "combine.hpp"
+#include "common.hpp"
+#include "expert.hpp"
+#include "gate.hpp"
+#include "gate_bwd.hpp"
+#include "host_topology.hpp"
+
+namespace tamoe {
+
+Arena::~Arena() {
+  if (base_) cudaFree(base_);
+}
+
+void Arena::commit() {
+  require(base_ == nullptr, "arena committed twice");
+  TAMOE_CUDA(cudaMalloc(&base_, static_cast<size_t>(size_ > 0 ? size_ : 256)));
+  for (const Slot& s : slots_) *s.ptr = base_ + s.off;
+}
+
+void RouteWorkspace::reserve(Arena& a, int P, int S, int N, int k) {
+  require(P >= 1 && S >= 1, "P and S must be positive");
+  require(N >= 1 && N <= 1024, "N must be in [1, 1024]");
+  require(k >= 1 && k <= N, "k must be in [1, N]");
+  require(k <= kMaxTopK, "device routing supports k <= 8");
+  dims = RouteDims{P, S, N, k, (S + kRouteTile - 1) / kRouteTile};
+  const long long picks = dims.picks();
+  const long long tw = static_cast<long long>(dims.tiles()) * 4 * N;
+  a.reserve(buf.idx, picks);
+  a.reserve(buf.gate, picks);
+  a.reserve(buf.score, picks);
+  a.reserve(buf.kept, picks);
+  a.reserve(buf.pos, picks);
+  a.reserve(buf.hist4, tw);
+  a.reserve(buf.msum4, tw);
+  a.reserve(buf.list_pick, picks);
+  a.reserve(buf.list_score, picks);
+  a.reserve(buf.clist, picks);
+  a.reserve(buf.list_keep, picks);
+  a.reserve(buf.list_start, N);
+  a.reserve(buf.list_count, N);
+  a.reserve(buf.bucket_start, static_cast<long long>(P) * N);
+  a.reserve(buf.bucket_count, static_cast<long long>(P) * N);
+  a.reserve(buf.counts, static_cast<long long>(P) * N);
+  a.reserve(buf.dropped, static_cast<long long>(P) * N);
+  a.reserve(buf.mean_probs, static_cast<long long>(P) * N);
+  a.reserve(buf.seg_start, N);
+  a.reserve(buf.seg_rows, N);
+  a.reserve(buf.total_rows, 1);
+  a.reserve(buf.bad, 1);
+  a.reserve(caps, static_cast<long long>(P) * N);
+}
+
+void RouteWorkspace::upload_caps(const long long* caps_host, cudaStream_t s) {
+  const int n = dims.P * dims.N;
+  std::vector<int> c(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) c[i] = static_cast<int>(std::min<long long>(std::max<long long>(caps_host[i], 0), INT_MAX));
+  TAMOE_CUDA(cudaMemcpyAsync(caps, c.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
+  TAMOE_CUDA(cudaStreamSynchronize(s));  // c is a stack temporary
+}
+
+void RouteWorkspace::finish(int mode, cudaStream_t s) const {
+  route_bucket(dims, buf, s);
+  route_capacity(dims, buf, mode, caps, s);
+}
+
+Router::Router(int P, int S, int N, int k) {
+  rw.reserve(arena, P, S, N, k);
+  arena.commit();
+}
+
+// ------------------------------------------------------------------------------------ Layer
+Layer::Layer(const LayerConfig& c, const double* c_hat) : cfg_(c) {
+  require(c.world_size == 1, "expert parallelism across ranks is configured through tamoe_layer_create_ep");
+  require(c.d % 256 == 0, "layer: d must be a multiple of 256");
+  require(c.d_out % 128 == 0, "layer: d_out must be a multiple of 128");
+  require(c.f == 0 || (c.f % 256 == 0), "layer: f must be 0 (linear expert) or a multiple of 256");
+  require(c.f != 0 || c.d % 256 == 0, "layer: linear experts need d % 256 == 0");
+  require(c.P == 1 || c.S % 16 == 0, "layer: S must be a multiple of 16 when P > 1 processes share a device");
+  require(c.cap_mode >= 0 && c.cap_mode <= 3, "unknown capacity mode");
+  require(c.aux_kind == 0 || c.aux_kind == 1, "unknown aux loss kind");
+  require(c.N <= 256, "layer: N must be <= 256");
+  P_global_ = c.P * c.world_size;
+  n_pad_ = (c.N + 15) & ~15;
+  n64_ = expert_pad64(c.N);
+  const long long T = static_cast<long long>(c.P) * c.S;
+  r_max_ = static_cast<int>(T * c.k + 16LL * c.N);
+  rw_.reserve(arena_, c.P, c.S, c.N, c.k);
+  arena_.reserve(xp_, static_cast<long long>(r_max_) * c.d);
+  arena_.reserve(O_, static_cast<long long>(r_max_) * c.d_out);
+  arena_.reserve(dO_, static_cast<long long>(r_max_) * c.d_out);
+  if (c.f > 0) {
+    arena_.reserve(H_, static_cast<long long>(r_max_) * c.f);
+    arena_.reserve(A_, static_cast<long long>(r_max_) * c.f);
+    arena_.reserve(dA_, static_cast<long long>(r_max_) * c.f);
+  }
+  if (c.need_dx) arena_.reserve(dxp_, static_cast<long long>(r_max_) * c.d);
+  arena_.reserve(dz_, T * n64_);
+  arena_.reserve(logits_, T * c.N);
+  arena_.reserve(dldg_, T * c.k);
+  dw_splits_ = gate_dw_splits(c.P, c.S, c.d, n64_);
+  arena_.reserve(dw_part_, static_cast<long long>(dw_splits_) * c.P * n64_ * c.d);
+  arena_.reserve(penalties_, static_cast<long long>(c.P) * c.N);
+  n_loss_part_ = combine_blocks(T);
+  arena_.reserve(loss_part_, n_loss_part_);
+  arena_.commit();
+
+  // host-side, once per topology: penalties p = Norm(1/c_hat) and capacities (gate.cpp:151-180, 222-246)
+  std::vector<double> pen(static_cast<size_t>(c.P) * c.N, 1.0 / c.N);
+  if (c.aux_kind == 1) {
+    require(c_hat != nullptr, "topo loss requires a target pattern (c_hat)");
+    for (int i = 0; i < c.P; ++i) {
+      auto p = penalty_weights(c_hat + static_cast<size_t>(c.rank * c.P + i) * c.N, c.N, c.penalty_norm,
+                               c.temperature);
+      std::copy(p.begin(), p.end(), pen.begin() + static_cast<size_t>(i) * c.N);
+    }
+  }
+  TAMOE_CUDA(cudaMemcpy(penalties_, pen.data(), sizeof(double) * pen.size(), cudaMemcpyHostToDevice));
+  // the reference withholds c_hat from balance routing (trainer.cpp:250): proportional capacity then throws
+  const double* ch = (c.aux_kind == 0) ? nullptr : c_hat;
+  auto caps = capacity_caps(c.cap_mode, c.cf, c.k, c.S, c.N, P_global_, ch);
+  rw_.upload_caps(caps.data() + static_cast<size_t>(c.rank) * c.P * c.N, nullptr);
+}
+
+void Layer::step(const LayerIO& io, cudaStream_t s) {
+  const LayerConfig& c = cfg_;
+  require(io.x && io.y && io.wg && io.w1 && io.dwg && io.dw1 && io.losses, "layer step: missing buffer");
+  require(c.f == 0 || (io.w2 && io.dw2), "layer step: FFN experts need w2 / dw2");
+  require(!c.need_dx || io.dx, "layer step: need_dx set but dx is null");
+  const RouteBuffers& b = rw_.buf;
+  const RouteDims& dm = rw_.dims;
+  const int E = c.N;  // experts on this device
+  // ---- forward: gate + routing
+  TAMOE_CUDA(cudaMemsetAsync(b.bad, 0, sizeof(int), s));
+  gate_forward(io.x, io.wg, n_pad_, dm, c.d, rw_.row_out(logits_, nullptr), s);
+  rw_.finish(c.cap_mode, s);
+  route_permute(dm, b, io.x, c.d, xp_, r_max_, dO_, c.d_out, s);
+  // ---- forward: experts
+  if (c.f == 0) {
+    grouped_fwd(xp_, io.w1, E, c.d_out, c.d, r_max_, b.seg_start, b.seg_rows, O_, nullptr, kActNone, s);
+  } else {
+    grouped_fwd(xp_, io.w1, E, c.f, c.d, r_max_, b.seg_start, b.seg_rows, H_, A_, c.act, s);
+    grouped_fwd(H_, io.w2, E, c.d_out, c.f, r_max_, b.seg_start, b.seg_rows, O_, nullptr, kActNone, s);
+  }
+  // ---- combine + task loss + dO
+  CombineArgs ca{};
+  ca.T = static_cast<long long>(c.P) * c.S;
+  ca.k = c.k;
+  ca.dout = c.d_out;
+  ca.mse_scale = static_cast<float>(2.0 / (static_cast<double>(P_global_) * c.S * c.d_out));
+  ca.pos = b.pos;
+  ca.gate = b.gate;
+  ca.O = O_;
+  ca.y = io.y;
+  ca.y_hat = io.y_hat;
+  ca.dO = dO_;
+  ca.dldg = dldg_;
+  ca.loss_part = loss_part_;
+  combine_loss(ca, s);
+  // ---- backward: experts
+  if (c.f == 0) {
+    grouped_wgrad(dO_, xp_, E, c.d_out, c.d, r_max_, b.seg_start, b.seg_rows, io.dw1, s);
+    if (c.need_dx)
+      grouped_dgrad(dO_, io.w1, E, c.d, c.d_out, r_max_, b.seg_start, b.seg_rows, dxp_, nullptr, kActNone, s);
+  } else {
+    grouped_dgrad(dO_, io.w2, E, c.f, c.d_out, r_max_, b.seg_start, b.seg_rows, dA_, A_, c.act, s);
+    grouped_wgrad(dO_, H_, E, c.d_out, c.f, r_max_, b.seg_start, b.seg_rows, io.dw2, s);
+    grouped_wgrad(dA_, xp_, E, c.f, c.d, r_max_, b.seg_start, b.seg_rows, io.dw1, s);
+    if (c.need_dx)
+      grouped_dgrad(dA_, io.w1, E, c.d, c.f, r_max_, b.seg_start, b.seg_rows, dxp_, nullptr, kActNone, s);
+  }
+  // ---- backward: gate
+  GateDzArgs ga{};
+  ga.P = c.P;
+  ga.S = c.S;
+  ga.N = c.N;
+  ga.k = c.k;
+  ga.n64 = n64_;
+  ga.dout = c.d_out;
+  ga.P_global = P_global_;
+  ga.aux_kind = c.aux_kind;
+  ga.aux_weight = c.aux_weight;
+  ga.logits = logits_;
+  ga.idx = b.idx;
+  ga.score = b.score;
+  ga.dldg = dldg_;
+  ga.counts = b.counts;
+  ga.mean_probs = b.mean_probs;
+  ga.penalties = penalties_;
+  ga.loss_part = loss_part_;
+  ga.n_loss_part = n_loss_part_;
+  ga.losses = io.losses;
+  ga.dz = dz_;
+  gate_dz(ga, s);
+  gate_dw(io.x, dz_, c.P, c.S, c.d, n64_, n_pad_, c.N, dw_part_, dw_splits_, io.dwg, s);
+  if (c.need_dx) gate_dx(dz_, io.wg, c.P, c.S, c.d, n64_, n_pad_, dxp_, b.pos, c.k, io.dx, s);
+}
+
+}  // namespace tamoe

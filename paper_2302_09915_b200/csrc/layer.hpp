@@ -1,0 +1,108 @@
+// TA-MoE layer: one object per (rank, device).  Owns the routing state and all
+// activation workspaces; weights, gradients and inputs are caller-owned.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "route.hpp"
+
+namespace tamoe {
+
+// Device arena: pointers are registered first, then one cudaMalloc backs them all
+// (256-byte aligned slices) and the registered pointers are patched in commit().
+class Arena {
+ public:
+  ~Arena();
+  template <class T>
+  void reserve(T*& ptr, long long count) {
+    const long long off = (size_ + 255) & ~255ll;
+    size_ = off + (count > 0 ? count : 1) * static_cast<long long>(sizeof(T));
+    slots_.push_back({reinterpret_cast<void**>(&ptr), off});
+  }
+  void commit();
+  long long bytes() const { return size_; }
+
+ private:
+  struct Slot {
+    void** ptr;
+    long long off;
+  };
+  char* base_ = nullptr;
+  long long size_ = 0;
+  std::vector<Slot> slots_;
+};
+
+// Routing workspace (device) for P processes x S tokens, N experts, top-k.
+struct RouteWorkspace {
+  RouteDims dims{};
+  RouteBuffers buf{};
+  int* caps = nullptr;  // [P*N] int32
+  void reserve(Arena& a, int P, int S, int N, int k);
+  void upload_caps(const long long* caps_host, cudaStream_t s);
+  // gate outputs view of the workspace
+  RowRouteOut row_out(float* logits, double* probs) const {
+    return RowRouteOut{buf.idx, buf.gate, buf.score, buf.hist4, buf.msum4, logits, probs, buf.bad};
+  }
+  void finish(int mode, cudaStream_t s) const;  // bucket + capacity
+};
+
+// Standalone router (the reference's topk_route / gate_forward operator API on device).
+struct Router {
+  Arena arena;
+  RouteWorkspace rw;
+  Router(int P, int S, int N, int k);
+};
+
+struct LayerConfig {
+  int P, S, d, d_out, N, k, f, act;
+  int cap_mode;
+  double cf;
+  int aux_kind;
+  double aux_weight;
+  int penalty_norm;
+  double temperature;
+  int need_dx;
+  int world_size, rank;
+};
+
+struct LayerIO {
+  const __nv_bfloat16* x;
+  const __nv_bfloat16* y;
+  const __nv_bfloat16* wg;
+  const __nv_bfloat16* w1;
+  const __nv_bfloat16* w2;
+  float* dwg;
+  __nv_bfloat16* dw1;
+  __nv_bfloat16* dw2;
+  __nv_bfloat16* dx;
+  __nv_bfloat16* y_hat;
+  double* losses;
+};
+
+class Layer {
+ public:
+  Layer(const LayerConfig& cfg, const double* c_hat);
+  void step(const LayerIO& io, cudaStream_t s);
+  const LayerConfig& cfg() const { return cfg_; }
+  RouteWorkspace& route() { return rw_; }
+  int n_pad() const { return n_pad_; }
+  int r_max() const { return r_max_; }
+  const float* logits() const { return logits_; }
+
+ private:
+  LayerConfig cfg_;
+  Arena arena_;
+  RouteWorkspace rw_;
+  int n_pad_ = 0, n64_ = 0, r_max_ = 0, dw_splits_ = 1, P_global_ = 1;
+  // activations (expert order, padded segments)
+  __nv_bfloat16 *xp_ = nullptr, *O_ = nullptr, *dO_ = nullptr, *H_ = nullptr, *A_ = nullptr, *dA_ = nullptr,
+                *dxp_ = nullptr, *dz_ = nullptr;
+  float *logits_ = nullptr, *dldg_ = nullptr, *dw_part_ = nullptr;
+  double *penalties_ = nullptr, *loss_part_ = nullptr;
+  int n_loss_part_ = 0;
+};
+
+}  // namespace tamoe

@@ -1,0 +1,341 @@
+// Expert histogram / scan / capacity / permute kernels.
+//
+// Replaces the counting and capacity parts of topk_route (gate.cpp:138-199)
+// and the token movement the reference leaves implicit.  Bucket order inside
+// an expert is ascending (process, token, slot) -- the reference's bucket
+// insertion order (gate.cpp:160-164, 181-185) -- and capacity keeps the best
+// (score desc, process asc, token asc) picks (gate.cpp:140-149) via an exact
+// radix select on the fp64 score bits, so kept sets are bit-identical.
+#include <cuda_bf16.h>
+
+#include <climits>
+#include <cstdint>
+
+#include "common.hpp"
+#include "route.hpp"
+
+namespace tamoe {
+
+namespace {
+
+// In-place exclusive scan of smem a[0..n); returns the total.  All threads of the block must call.
+__device__ int block_excl_scan(int* a, int n, int* wtmp) {
+  const int nt = blockDim.x;
+  const int per = (n + nt - 1) / nt;
+  const int b = threadIdx.x * per;
+  const int e = min(n, b + per);
+  int local = 0;
+  for (int i = b; i < e; ++i) local += a[i];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (nt + 31) >> 5;
+  int x = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wtmp[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int v = lane < nw ? wtmp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    if (lane < nw) wtmp[lane] = v;
+  }
+  __syncthreads();
+  int base = (w > 0 ? wtmp[w - 1] : 0) + x - local;
+  for (int i = b; i < e; ++i) {
+    const int t = a[i];
+    a[i] = base;
+    base += t;
+  }
+  const int total = wtmp[nw - 1];
+  __syncthreads();
+  return total;
+}
+
+// ---------------------------------------------------------------- bucket
+// One CTA per 128-token tile.  Position of a pick in its expert's list =
+// list_start[e] + picks to e in earlier tiles + earlier warps + earlier lanes.
+__global__ void __launch_bounds__(kRouteTile) route_bucket_kernel(RouteDims d, RouteBuffers b) {
+  extern __shared__ int sm[];
+  const int N = d.N, k = d.k;
+  int* base = sm;                      // [N]  list start + earlier tiles
+  int* wbase = base + N;               // [4*N]
+  int* sel = wbase + 4 * N;            // [128*k]
+  int* wtmp = sel + kRouteTile * k;    // [32]
+  int* tot = wtmp + 32;                // [N]
+  const int tile = blockIdx.x;
+  const int tiles = d.tiles();
+  for (int e = threadIdx.x; e < N; e += blockDim.x) {
+    int before = 0, all = 0;
+    for (int t = 0; t < tiles; ++t) {
+      const int* h = b.hist4 + static_cast<long long>(t) * 4 * N + e;
+      const int c = h[0] + h[N] + h[2 * N] + h[3 * N];
+      all += c;
+      if (t < tile) before += c;
+    }
+    tot[e] = all;
+    base[e] = before;
+  }
+  __syncthreads();
+  block_excl_scan(tot, N, wtmp);  // tot -> list_start
+  for (int e = threadIdx.x; e < N; e += blockDim.x) {
+    const int* h = b.hist4 + static_cast<long long>(tile) * 4 * N + e;
+    int acc = tot[e] + base[e];
+    for (int w = 0; w < 4; ++w) {
+      wbase[w * N + e] = acc;
+      acc += h[w * N];
+    }
+  }
+  if (blockIdx.x == 0) {
+    // expert list starts / counts and per-(process, expert) buckets, written once
+    for (int e = threadIdx.x; e < N; e += blockDim.x) {
+      b.list_start[e] = tot[e];
+      int acc = 0;
+      for (int pr = 0; pr < d.P; ++pr) {
+        int c = 0;
+        for (int t = pr * d.TB; t < (pr + 1) * d.TB; ++t) {
+          const int* h = b.hist4 + static_cast<long long>(t) * 4 * N + e;
+          c += h[0] + h[N] + h[2 * N] + h[3 * N];
+        }
+        b.bucket_start[pr * N + e] = acc;
+        b.bucket_count[pr * N + e] = c;
+        acc += c;
+      }
+      b.list_count[e] = acc;
+    }
+  }
+  const int proc = tile / d.TB;
+  const int tok = (tile % d.TB) * kRouteTile + threadIdx.x;
+  const bool valid = tok < d.S;
+  const long long gtok = static_cast<long long>(proc) * d.S + tok;
+  for (int j = 0; j < k; ++j) sel[threadIdx.x * k + j] = valid ? b.idx[gtok * k + j] : -1;
+  __syncthreads();
+  if (!valid) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int a = 0; a < k; ++a) {
+    const int e = sel[threadIdx.x * k + a];
+    int r = 0;
+    for (int l = w * 32; l < threadIdx.x; ++l)
+      for (int j = 0; j < k; ++j) r += (sel[l * k + j] == e);
+    const int pos = wbase[w * N + e] + r;
+    b.list_pick[pos] = static_cast<int>(gtok * k + a);
+    b.list_score[pos] = b.score[gtok * k + a];
+  }
+  (void)lane;
+}
+
+// ---------------------------------------------------------------- capacity
+// One CTA per expert.  For every capacity domain (bucket) over budget, an exact
+// 8-pass radix select on the fp64 score bits finds the cap-th best score v;
+// keep score > v, plus the first (cap - #greater) picks with score == v in list
+// order (= process asc, token asc).
+constexpr int kCapThreads = 512;
+
+__device__ __forceinline__ unsigned long long score_key(double s) {
+  // scores are probabilities >= 0: the IEEE bits are monotone
+  return static_cast<unsigned long long>(__double_as_longlong(s));
+}
+
+__global__ void __launch_bounds__(kCapThreads) route_capacity_kernel(RouteDims d, RouteBuffers b, int mode,
+                                                                     const int* __restrict__ caps) {
+  __shared__ int hist[256];
+  __shared__ int wtmp[32];
+  __shared__ int sh_digit, sh_need;
+  __shared__ int carry;
+  const int e = blockIdx.x;
+  const int N = d.N;
+  const int ls = b.list_start[e];
+  const int nb = mode == 1 ? 1 : d.P;
+  // pass A: per bucket select + keep flags
+  for (int bk = 0; bk < nb; ++bk) {
+    const int bs = mode == 1 ? 0 : b.bucket_start[bk * N + e];
+    const int bc = mode == 1 ? b.list_count[e] : b.bucket_count[bk * N + e];
+    const int cap = mode == 0 ? INT_MAX : max(caps[bk * N + e], 0);
+    const double* sc = b.list_score + ls + bs;
+    uint8_t* keep = b.list_keep + ls + bs;
+    if (bc <= cap) {
+      for (int j = threadIdx.x; j < bc; j += blockDim.x) keep[j] = 1;
+      continue;
+    }
+    unsigned long long prefix = 0, mask = 0;
+    int need = cap;  // elements still to take from the top among the candidates
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+      __syncthreads();
+      for (int j = threadIdx.x; j < bc; j += blockDim.x) {
+        const unsigned long long key = score_key(sc[j]);
+        if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int cum = 0, dg = 0;
+        for (dg = 255; dg > 0; --dg) {
+          if (cum + hist[dg] >= need) break;
+          cum += hist[dg];
+        }
+        sh_digit = dg;
+        sh_need = need - cum;
+      }
+      __syncthreads();
+      prefix |= static_cast<unsigned long long>(sh_digit) << shift;
+      mask |= 255ull << shift;
+      need = sh_need;
+      __syncthreads();
+    }
+    // need = how many picks with key == prefix to keep (in list order)
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int j0 = 0; j0 < bc; j0 += blockDim.x) {
+      const int j = j0 + threadIdx.x;
+      unsigned long long key = 0;
+      int eq = 0;
+      if (j < bc) {
+        key = score_key(sc[j]);
+        eq = key == prefix;
+      }
+      // exclusive rank of equality flags inside the block
+      const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+      const unsigned bal = __ballot_sync(0xffffffffu, eq);
+      const int in_warp = __popc(bal & ((1u << lane) - 1));
+      if (lane == 0) wtmp[w] = __popc(bal);
+      __syncthreads();
+      int before = carry;
+      for (int ww = 0; ww < w; ++ww) before += wtmp[ww];
+      if (j < bc) keep[j] = (key > prefix) || (eq && (before + in_warp) < need);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int s = 0;
+        for (int ww = 0; ww < (int)(blockDim.x >> 5); ++ww) s += wtmp[ww];
+        carry += s;
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  // pass B: compaction over the whole expert list (stable), counts, kept / pos of drops
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int total = b.list_count[e];
+  for (int j0 = 0; j0 < total; j0 += blockDim.x) {
+    const int j = j0 + threadIdx.x;
+    const int kp = j < total ? b.list_keep[ls + j] : 0;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned bal = __ballot_sync(0xffffffffu, kp);
+    if (lane == 0) wtmp[w] = __popc(bal);
+    __syncthreads();
+    int before = carry;
+    for (int ww = 0; ww < w; ++ww) before += wtmp[ww];
+    if (j < total) {
+      const int pick = b.list_pick[ls + j];
+      b.kept[pick] = static_cast<uint8_t>(kp);
+      if (kp) b.clist[ls + before + __popc(bal & ((1u << lane) - 1))] = pick;
+      else b.pos[pick] = -1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int s = 0;
+      for (int ww = 0; ww < (int)(blockDim.x >> 5); ++ww) s += wtmp[ww];
+      carry += s;
+    }
+    __syncthreads();
+  }
+  // per-bucket kept / dropped counts and mean probabilities (fixed-order sums)
+  for (int pr = threadIdx.x; pr < d.P; pr += blockDim.x) {
+    const int bs = b.bucket_start[pr * N + e], bc = b.bucket_count[pr * N + e];
+    int kc = 0;
+    for (int j = 0; j < bc; ++j) kc += b.list_keep[ls + bs + j];
+    b.counts[pr * N + e] = kc;
+    b.dropped[pr * N + e] = bc - kc;
+    double m = 0.0;
+    for (int t = pr * d.TB; t < (pr + 1) * d.TB; ++t)
+      for (int w = 0; w < 4; ++w) m += b.msum4[(static_cast<long long>(t) * 4 + w) * N + e];
+    b.mean_probs[pr * N + e] = m / d.S;
+  }
+}
+
+// ---------------------------------------------------------------- permute
+// One warp per destination row of the padded expert-sorted buffer.
+constexpr int kPermWarps = 8;
+
+__global__ void __launch_bounds__(kPermWarps * 32) route_permute_kernel(RouteDims d, RouteBuffers b,
+                                                                        const __nv_bfloat16* __restrict__ x, int dx,
+                                                                        __nv_bfloat16* __restrict__ xp, int r_max,
+                                                                        __nv_bfloat16* __restrict__ zrows, int zdim) {
+  extern __shared__ int sm[];
+  const int N = d.N;
+  int* start = sm;          // [N]
+  int* cnt = start + N;     // [N]
+  int* wtmp = cnt + N;      // [32]
+  for (int e = threadIdx.x; e < N; e += blockDim.x) {
+    int c = 0;
+    for (int pr = 0; pr < d.P; ++pr) c += b.counts[pr * N + e];
+    cnt[e] = c;
+    start[e] = (c + 15) & ~15;
+  }
+  __syncthreads();
+  const int total = block_excl_scan(start, N, wtmp);
+  if (blockIdx.x == 0) {
+    for (int e = threadIdx.x; e < N; e += blockDim.x) {
+      b.seg_start[e] = start[e];
+      b.seg_rows[e] = (cnt[e] + 15) & ~15;
+    }
+    if (threadIdx.x == 0) *b.total_rows = total;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * kPermWarps + warp;
+  if (r >= total || r >= r_max) return;
+  int lo = 0, hi = N - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (start[mid] <= r) lo = mid; else hi = mid - 1;
+  }
+  // skip empty experts sharing the same start
+  while (lo + 1 < N && start[lo + 1] <= r) ++lo;
+  const int e = lo;
+  const int j = r - start[e];
+  uint4* dst = reinterpret_cast<uint4*>(xp + static_cast<long long>(r) * dx);
+  const int nv = dx / 8;
+  if (j < cnt[e]) {
+    const int pick = b.clist[b.list_start[e] + j];
+    const long long tok = pick / d.k;
+    if (lane == 0) b.pos[pick] = r;
+    const uint4* src = reinterpret_cast<const uint4*>(x + tok * dx);
+    for (int v = lane; v < nv; v += 32) dst[v] = src[v];
+  } else {
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    for (int v = lane; v < nv; v += 32) dst[v] = z;
+    if (zrows) {
+      uint4* zd = reinterpret_cast<uint4*>(zrows + static_cast<long long>(r) * zdim);
+      for (int v = lane; v < zdim / 8; v += 32) zd[v] = z;
+    }
+  }
+}
+
+}  // namespace
+
+void route_bucket(const RouteDims& d, const RouteBuffers& b, cudaStream_t s) {
+  const size_t smem = sizeof(int) * (6 * d.N + kRouteTile * d.k + 32);
+  route_bucket_kernel<<<d.tiles(), kRouteTile, smem, s>>>(d, b);
+  TAMOE_CUDA(cudaGetLastError());
+}
+
+void route_capacity(const RouteDims& d, const RouteBuffers& b, int mode, const int* caps, cudaStream_t s) {
+  require(mode >= 0 && mode <= 3, "unknown capacity mode");
+  route_capacity_kernel<<<d.N, kCapThreads, 0, s>>>(d, b, mode, caps);
+  TAMOE_CUDA(cudaGetLastError());
+}
+
+void route_permute(const RouteDims& d, const RouteBuffers& b, const __nv_bfloat16* x, int dx, __nv_bfloat16* xp,
+                   int r_max, __nv_bfloat16* zero_rows, int zdim, cudaStream_t s) {
+  require(dx % 8 == 0 && (zero_rows == nullptr || zdim % 8 == 0), "permute: row widths must be multiples of 8");
+  const int blocks = (r_max + kPermWarps - 1) / kPermWarps;
+  const size_t smem = sizeof(int) * (2 * d.N + 32);
+  route_permute_kernel<<<blocks, kPermWarps * 32, smem, s>>>(d, b, x, dx, xp, r_max, zero_rows, zdim);
+  TAMOE_CUDA(cudaGetLastError());
+}
+
+}  // namespace tamoe

@@ -1,0 +1,78 @@
+// Routing state shared by the gate epilogue, the histogram/scan/capacity/permute
+// kernels and the combine / backward kernels.  All buffers are device memory.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace tamoe {
+
+constexpr int kMaxTopK = 8;
+constexpr int kRouteTile = 128;  // tokens per routing tile (= GEMM M tile), 4 warps of 32
+
+struct RouteDims {
+  int P;      // logical processes on this device
+  int S;      // tokens per process
+  int N;      // experts
+  int k;      // experts per token
+  int TB;     // 128-token tiles per process = ceil(S / 128)
+  __host__ __device__ int tiles() const { return P * TB; }
+  __host__ __device__ long long picks() const { return static_cast<long long>(P) * S * k; }
+};
+
+struct RouteBuffers {
+  // per pick [P*S*k], pick id = token * k + slot (token = proc * S + s)
+  int* idx = nullptr;
+  float* gate = nullptr;
+  double* score = nullptr;
+  uint8_t* kept = nullptr;
+  int* pos = nullptr;  // row of the pick in the expert-sorted buffer, -1 if dropped
+  // per (tile, warp, expert) [tiles*4*N]
+  int* hist4 = nullptr;
+  double* msum4 = nullptr;
+  // expert lists [P*S*k]
+  int* list_pick = nullptr;     // pre-capacity, expert-major, (process, token) order inside
+  double* list_score = nullptr;
+  int* clist = nullptr;         // kept picks compacted at the front of each expert range
+  uint8_t* list_keep = nullptr;
+  // per expert / bucket
+  int* list_start = nullptr;  // [N]
+  int* list_count = nullptr;  // [N]
+  int* bucket_start = nullptr;  // [P*N] offset inside the expert list
+  int* bucket_count = nullptr;  // [P*N]
+  int* counts = nullptr;      // [P*N] kept
+  int* dropped = nullptr;     // [P*N]
+  double* mean_probs = nullptr;  // [P*N]
+  int* seg_start = nullptr;   // [N] padded row segment per expert
+  int* seg_rows = nullptr;    // [N]
+  int* total_rows = nullptr;  // [1]
+  int* bad = nullptr;         // [1] non-finite logit flag
+};
+
+// Gate epilogue / standalone router outputs (per-row routing, see gate.cu).
+struct RowRouteOut {
+  int* idx;
+  float* gate;
+  double* score;
+  int* hist4;
+  double* msum4;
+  float* logits;  // optional [P*S*N]
+  double* probs;  // optional [P*S*N]
+  int* bad;
+};
+
+// Top-k selection from fp64 probabilities (P x S x N), the reference's topk_route input.
+void route_rows_from_probs(const double* probs, const RouteDims& d, const RowRouteOut& o, cudaStream_t s);
+
+// histogram scan + stable bucket lists (gate.cpp:160-164 / 181-185 order)
+void route_bucket(const RouteDims& d, const RouteBuffers& b, cudaStream_t s);
+// capacity enforcement + compaction + counts + mean probs (gate.cpp:115, 138-199)
+// caps: device int32 [P*N] (INT32_MAX = unlimited); mode: 0 none, 1 global, 2 local, 3 proportional
+void route_capacity(const RouteDims& d, const RouteBuffers& b, int mode, const int* caps, cudaStream_t s);
+// padded expert segments + gather of token rows into the expert-sorted buffer.
+// x: [P*S x dx] bf16; xp: [R_max x dx]; zero_rows (optional): second buffer whose pad rows are zeroed.
+void route_permute(const RouteDims& d, const RouteBuffers& b, const __nv_bfloat16* x, int dx, __nv_bfloat16* xp,
+                   int r_max, __nv_bfloat16* zero_rows, int zdim, cudaStream_t s);
+
+}  // namespace tamoe

@@ -1,0 +1,155 @@
+"""TAMoELayer: the reference's MoE layer step (trainer.cpp:243-356) on the B200
+through libtamoe.so.  Torch is used only to own device memory and streams.
+
+Weight layouts (device, bf16):
+  wg  [P, n_pad, d]       gate weights, reference W_i (d x N) transposed, pad rows zero
+  w1  linear: [E, d_out, d] (U_e^T);  FFN: [E, f, d]
+  w2  FFN: [E, d_out, f]
+Reference-layout converters are provided for the parity tests.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .ops import CapacityMode, PenaltyNorm, n_pad, _R_DTYPES, R_LOGITS  # noqa: F401
+
+ACT_NONE, ACT_GELU, ACT_RELU = 0, 1, 2
+LOSS_BALANCE, LOSS_TOPO = 0, 1
+
+
+class _Cfg(ctypes.Structure):
+    _fields_ = [("P", ctypes.c_int), ("S", ctypes.c_int), ("d", ctypes.c_int), ("d_out", ctypes.c_int),
+                ("N", ctypes.c_int), ("k", ctypes.c_int), ("f", ctypes.c_int), ("act", ctypes.c_int),
+                ("cap_mode", ctypes.c_int), ("capacity_factor", ctypes.c_double), ("aux_kind", ctypes.c_int),
+                ("aux_weight", ctypes.c_double), ("penalty_norm", ctypes.c_int), ("temperature", ctypes.c_double),
+                ("need_dx", ctypes.c_int), ("world_size", ctypes.c_int), ("rank", ctypes.c_int)]
+
+
+class _IO(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("x", "y", "wg", "w1", "w2", "dwg", "dw1", "dw2", "dx", "y_hat",
+                                               "losses")]
+
+
+_lib.lib.tamoe_layer_create.argtypes = [ctypes.POINTER(_Cfg), ctypes.POINTER(ctypes.c_double),
+                                        ctypes.POINTER(ctypes.c_void_p)]
+_lib.lib.tamoe_layer_destroy.argtypes = [ctypes.c_void_p]
+_lib.lib.tamoe_layer_step.argtypes = [ctypes.c_void_p, ctypes.POINTER(_IO), ctypes.c_void_p]
+_lib.lib.tamoe_layer_read.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_longlong,
+                                      ctypes.c_void_p]
+for _n in ("tamoe_layer_create", "tamoe_layer_destroy", "tamoe_layer_step", "tamoe_layer_read"):
+    getattr(_lib.lib, _n).restype = ctypes.c_int
+
+
+@dataclass
+class LayerConfig:
+    P: int
+    S: int
+    d: int
+    d_out: int
+    N: int
+    k: int = 1
+    f: int = 0
+    act: int = ACT_GELU
+    cap_mode: int = 0
+    capacity_factor: float = 1.0
+    aux_kind: int = LOSS_BALANCE
+    aux_weight: float = 1.0
+    penalty_norm: int = 0
+    temperature: float = 0.0
+    need_dx: bool = False
+    world_size: int = 1
+    rank: int = 0
+
+    @property
+    def n_pad(self):
+        return n_pad(self.N)
+
+    @property
+    def experts_local(self):
+        return self.N // self.world_size
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+class TAMoELayer:
+    def __init__(self, cfg: LayerConfig, c_hat=None, device="cuda"):
+        self.cfg = cfg
+        self.device = torch.device(device)
+        c = _Cfg(cfg.P, cfg.S, cfg.d, cfg.d_out, cfg.N, cfg.k, cfg.f, cfg.act, cfg.cap_mode, cfg.capacity_factor,
+                 cfg.aux_kind, cfg.aux_weight, cfg.penalty_norm, cfg.temperature, int(cfg.need_dx), cfg.world_size,
+                 cfg.rank)
+        self._c_hat = np.ascontiguousarray(c_hat, np.float64) if c_hat is not None else None
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib.tamoe_layer_create(
+            ctypes.byref(c), self._c_hat.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if self._c_hat is not None
+            else None, ctypes.byref(h)))
+        self._h = h
+        E = cfg.experts_local
+        bf = dict(dtype=torch.bfloat16, device=self.device)
+        # gradient buffers (reused every step)
+        self.dwg = torch.zeros(cfg.P, cfg.n_pad, cfg.d, dtype=torch.float32, device=self.device)
+        if cfg.f == 0:
+            self.dw1 = torch.zeros(E, cfg.d_out, cfg.d, **bf)
+            self.dw2 = None
+        else:
+            self.dw1 = torch.zeros(E, cfg.f, cfg.d, **bf)
+            self.dw2 = torch.zeros(E, cfg.d_out, cfg.f, **bf)
+        self.dx = torch.zeros(cfg.P * cfg.S, cfg.d, **bf) if cfg.need_dx else None
+        self.losses = torch.zeros(2, dtype=torch.float64, device=self.device)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.lib.tamoe_layer_destroy(self._h)
+            self._h = None
+
+    # ------------------------------------------------------------------ parameters
+    def init_params(self, seed=0, gate_std=0.02):
+        cfg = self.cfg
+        g = torch.Generator(device=self.device).manual_seed(seed)
+        E = cfg.experts_local
+        wg = torch.zeros(cfg.P, cfg.n_pad, cfg.d, dtype=torch.bfloat16, device=self.device)
+        wg[:, :cfg.N] = (torch.randn(cfg.P, cfg.N, cfg.d, generator=g, device=self.device) * gate_std).bfloat16()
+        if cfg.f == 0:
+            w1 = (torch.randn(E, cfg.d_out, cfg.d, generator=g, device=self.device) / cfg.d ** 0.5).bfloat16()
+            w2 = None
+        else:
+            w1 = (torch.randn(E, cfg.f, cfg.d, generator=g, device=self.device) / cfg.d ** 0.5).bfloat16()
+            w2 = (torch.randn(E, cfg.d_out, cfg.f, generator=g, device=self.device) / cfg.f ** 0.5).bfloat16()
+        return dict(wg=wg, w1=w1, w2=w2)
+
+    def step(self, x, y, params, y_hat=None, stream=None):
+        """Forward + task/aux loss + backward.  Gradients land in self.dwg / dw1 / dw2 / dx;
+        losses (device fp64[2]: task, aux) in self.losses.  Stream-ordered; no host sync."""
+        io = _IO(_ptr(x), _ptr(y), _ptr(params["wg"]), _ptr(params["w1"]), _ptr(params.get("w2")), _ptr(self.dwg),
+                 _ptr(self.dw1), _ptr(self.dw2), _ptr(self.dx), _ptr(y_hat), _ptr(self.losses))
+        s = stream if stream is not None else torch.cuda.current_stream()
+        _lib.check(_lib.lib.tamoe_layer_step(self._h, ctypes.byref(io), ctypes.c_void_p(s.cuda_stream)))
+        return self.losses
+
+    def read(self, what, shape):
+        out = np.zeros(shape, dtype=_R_DTYPES[what])
+        _lib.check(_lib.lib.tamoe_layer_read(self._h, what, out.ctypes.data_as(ctypes.c_void_p), out.nbytes,
+                                             ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        return out
+
+    # ------------------------------------------------------------------ reference-layout converters
+    @staticmethod
+    def gates_from_reference(gates, n_pad_, device="cuda"):
+        """reference gates [P][d][N] -> wg [P, n_pad, d] bf16."""
+        g = torch.as_tensor(np.asarray(gates), dtype=torch.float32)
+        P, d, N = g.shape
+        wg = torch.zeros(P, n_pad_, d, dtype=torch.bfloat16)
+        wg[:, :N] = g.transpose(1, 2).bfloat16()
+        return wg.to(device)
+
+    @staticmethod
+    def linear_from_reference(U, device="cuda"):
+        """reference experts U_e [N][d][d_out] -> w1 [N, d_out, d] bf16."""
+        return torch.as_tensor(np.asarray(U), dtype=torch.float32).transpose(1, 2).contiguous().bfloat16().to(device)

@@ -1,0 +1,252 @@
+"""Python mirror of the reference operator API (namespace tad, gate.hpp:22-97,
+solver.hpp target_closed_form, dispatch.hpp device_payload_tokens), executed by
+libtamoe.so.  Host-side topology inputs run the library's C++ (fp64, bit-identical
+to the reference); routing runs the sm_100a kernels.
+
+Names, argument meaning and error behaviour follow the reference: malformed
+inputs raise ValidationError (tad::ValidationError).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from enum import IntEnum
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import ValidationError, TamoeError  # noqa: F401
+
+_D = ctypes.POINTER(ctypes.c_double)
+_L = ctypes.POINTER(ctypes.c_longlong)
+
+
+class CapacityMode(IntEnum):  # gate.hpp:40
+    none = 0
+    global_ = 1
+    local = 2
+    local_proportional = 3
+
+
+class PenaltyNorm(IntEnum):  # gate.hpp:74
+    sum_norm = 0
+    softmax = 1
+
+
+def capacity_mode_from_string(s: str) -> CapacityMode:  # gate.cpp:34-40
+    table = {"none": 0, "global": 1, "local": 2, "proportional": 3, "local_proportional": 3}
+    if s not in table:
+        raise ValidationError(f"unknown capacity mode: {s}")
+    return CapacityMode(table[s])
+
+
+@dataclass
+class CapacityPolicy:  # gate.hpp:42-49
+    mode: CapacityMode = CapacityMode.none
+    capacity_factor: float = 1.0
+
+    def expert_capacity(self, k: int, S: int, N: int, P: int) -> float:
+        return self.capacity_factor * float(k) * S * P / N
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+# ----------------------------------------------------------------------------- host-side inputs
+def largest_remainder_round(values, target: int) -> np.ndarray:
+    v = _f64(values)
+    out = np.zeros(len(v), dtype=np.int64)
+    _lib.call("tamoe_largest_remainder_round", v.ctypes.data_as(_D), len(v), int(target), out.ctypes.data_as(_L))
+    return out
+
+
+def penalty_weights(c_hat_row, norm: PenaltyNorm = PenaltyNorm.sum_norm, temperature: float = 0.0) -> np.ndarray:
+    c = _f64(c_hat_row)
+    p = np.zeros(len(c))
+    _lib.call("tamoe_penalty_weights", c.ctypes.data_as(_D), len(c), int(norm), float(temperature),
+              p.ctypes.data_as(_D))
+    return p
+
+
+def target_closed_form(beta_hat, N: int, k: int, S: int) -> np.ndarray:
+    b = _f64(beta_hat)
+    P = b.shape[0]
+    out = np.zeros((P, N))
+    _lib.call("tamoe_target_closed_form", b.ctypes.data_as(_D), P, N, k, S, out.ctypes.data_as(_D))
+    return out
+
+
+def capacity_caps(policy: CapacityPolicy, k: int, S: int, N: int, P: int, c_hat=None) -> np.ndarray:
+    ch = _f64(c_hat) if c_hat is not None else None
+    caps = np.zeros((P, N), dtype=np.int64)
+    _lib.call("tamoe_capacity_caps", int(policy.mode), float(policy.capacity_factor), k, S, N, P,
+              ch.ctypes.data_as(_D) if ch is not None else None, caps.ctypes.data_as(_L))
+    return caps
+
+
+def device_payload_tokens(counts) -> np.ndarray:
+    c = _f64(counts)
+    P, N = c.shape
+    out = np.zeros((P, P))
+    _lib.call("tamoe_device_payload_tokens", c.ctypes.data_as(_D), P, N, out.ctypes.data_as(_D))
+    return out
+
+
+# ----------------------------------------------------------------------------- device router
+R_IDX, R_GATE, R_SCORE, R_KEPT, R_POS, R_COUNTS, R_DROPPED, R_MEAN_PROBS, R_SEG_START, R_SEG_ROWS, R_CLIST, \
+    R_LIST_START, R_BAD, R_LOGITS = range(14)
+
+_R_DTYPES = {R_IDX: np.int32, R_GATE: np.float32, R_SCORE: np.float64, R_KEPT: np.uint8, R_POS: np.int32,
+             R_COUNTS: np.int32, R_DROPPED: np.int32, R_MEAN_PROBS: np.float64, R_SEG_START: np.int32,
+             R_SEG_ROWS: np.int32, R_CLIST: np.int32, R_LIST_START: np.int32, R_BAD: np.int32,
+             R_LOGITS: np.float32}
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def n_pad(N: int) -> int:
+    return (N + 15) // 16 * 16
+
+
+class Router:
+    """Device routing for P processes x S tokens, N experts, top-k (topk_route, gate.cpp:91-202)."""
+
+    def __init__(self, P: int, S: int, N: int, k: int):
+        self.P, self.S, self.N, self.k = P, S, N, k
+        h = ctypes.c_void_p()
+        _lib.lib.tamoe_router_create.argtypes = [ctypes.c_int] * 4 + [ctypes.POINTER(ctypes.c_void_p)]
+        _lib.call("tamoe_router_create", P, S, N, k, ctypes.byref(h))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.lib.tamoe_router_destroy(self._h)
+            self._h = None
+
+    def _shape(self, what):
+        picks = self.P * self.S * self.k
+        pn = self.P * self.N
+        return {R_IDX: (self.P, self.S, self.k), R_GATE: (self.P, self.S, self.k), R_SCORE: (self.P, self.S, self.k),
+                R_KEPT: (self.P, self.S, self.k), R_POS: (self.P, self.S, self.k), R_COUNTS: (self.P, self.N),
+                R_DROPPED: (self.P, self.N), R_MEAN_PROBS: (self.P, self.N), R_SEG_START: (self.N,),
+                R_SEG_ROWS: (self.N,), R_CLIST: (picks,), R_LIST_START: (self.N,), R_BAD: (1,)}[what] if what != R_LOGITS \
+            else (self.P, self.S, self.N)
+
+    def read(self, what) -> np.ndarray:
+        out = np.zeros(self._shape(what), dtype=_R_DTYPES[what])
+        self._read_fn(what, out)
+        return out
+
+    def _read_fn(self, what, out):
+        _lib.call("tamoe_router_read", self._h, what, out.ctypes.data_as(ctypes.c_void_p), out.nbytes, _stream())
+
+    def route_probs(self, probs: torch.Tensor, policy: CapacityPolicy, caps: np.ndarray):
+        assert probs.dtype == torch.float64 and probs.is_cuda and probs.is_contiguous()
+        c = np.ascontiguousarray(caps, np.int64)
+        _lib.call("tamoe_router_route_probs", self._h, ctypes.c_void_p(probs.data_ptr()), int(policy.mode),
+                  c.ctypes.data_as(_L), _stream())
+
+    def route_gate(self, x: torch.Tensor, wg: torch.Tensor, policy: CapacityPolicy, caps: np.ndarray,
+                   want_probs=False):
+        """x bf16 [P*S, d]; wg bf16 [P, n_pad, d].  Returns (logits fp32, probs fp64 or None) on device."""
+        d = x.shape[1]
+        logits = torch.empty(self.P * self.S, self.N, dtype=torch.float32, device=x.device)
+        probs = torch.empty(self.P * self.S, self.N, dtype=torch.float64, device=x.device) if want_probs else None
+        c = np.ascontiguousarray(caps, np.int64)
+        _lib.call("tamoe_router_route_gate", self._h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(wg.data_ptr()),
+                  wg.shape[1], d, ctypes.c_void_p(logits.data_ptr()),
+                  ctypes.c_void_p(probs.data_ptr()) if probs is not None else None, int(policy.mode),
+                  c.ctypes.data_as(_L), _stream())
+        return logits, probs
+
+    def permute(self, x: torch.Tensor, r_max: int) -> torch.Tensor:
+        xp = torch.full((r_max, x.shape[1]), float("nan"), dtype=x.dtype, device=x.device)
+        _lib.call("tamoe_router_permute", self._h, ctypes.c_void_p(x.data_ptr()), x.shape[1],
+                  ctypes.c_void_p(xp.data_ptr()), r_max, _stream())
+        return xp
+
+    def expert_order(self) -> list:
+        """Kept picks per expert in buffer order: list of arrays of pick ids (token*k + slot)."""
+        clist, ls, cnt = self.read(R_CLIST), self.read(R_LIST_START), self.read(R_COUNTS).sum(0)
+        return [clist[ls[e]:ls[e] + cnt[e]] for e in range(self.N)]
+
+
+for _name, _args in {
+    "tamoe_router_destroy": [ctypes.c_void_p],
+    "tamoe_router_route_probs": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, _L, ctypes.c_void_p],
+    "tamoe_router_route_gate": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, _L, ctypes.c_void_p],
+    "tamoe_router_permute": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                             ctypes.c_void_p],
+    "tamoe_router_read": [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p],
+}.items():
+    getattr(_lib.lib, _name).argtypes = _args
+    getattr(_lib.lib, _name).restype = ctypes.c_int
+
+
+def gate_forward(x: torch.Tensor, W: torch.Tensor):
+    """gate_forward (gate.cpp:30-32) on the device: softmax(x W) in fp64 from tcgen05 fp32 logits.
+    x [S, d] (any float dtype, rounded to bf16), W [d, N] (reference layout).  Returns fp64 probs [S, N]."""
+    S, d = x.shape
+    N = W.shape[1]
+    dp = (d + 63) // 64 * 64
+    np_ = n_pad(N)
+    xb = torch.zeros(S, dp, dtype=torch.bfloat16, device="cuda")
+    xb[:, :d] = x.to("cuda", torch.bfloat16)
+    wg = torch.zeros(1, np_, dp, dtype=torch.bfloat16, device="cuda")
+    wg[0, :N, :d] = W.to("cuda").t().to(torch.bfloat16)
+    r = Router(1, S, N, 1)
+    caps = np.full((1, N), np.iinfo(np.int64).max, dtype=np.int64)
+    _, probs = r.route_gate(xb, wg, CapacityPolicy(), caps, want_probs=True)
+    return probs
+
+
+@dataclass
+class RoutingResult:  # gate.hpp:32-38, arrays instead of nested vectors
+    expert: np.ndarray
+    gate_value: np.ndarray
+    score: np.ndarray
+    kept: np.ndarray
+    counts: np.ndarray
+    dropped: np.ndarray
+    mean_probs: np.ndarray
+    order: list  # kept picks per expert in dispatch order
+
+
+def topk_route(probs, k: int, policy: CapacityPolicy = CapacityPolicy(), c_hat=None):
+    """topk_route (gate.cpp:91-202): probs [P, S, N] (or [S, N]) fp64 -> list of per-process RoutingResult
+    (a single RoutingResult for 2-D input, like the single-process wrapper gate.cpp:204-207)."""
+    single = False
+    p = torch.as_tensor(probs, dtype=torch.float64)
+    if p.dim() == 2:
+        p = p[None]
+        single = True
+    P, S, N = p.shape
+    if k < 1 or k > N:
+        raise ValidationError("k must be in [1, N]")
+    if policy.mode == CapacityMode.local_proportional and c_hat is None:
+        raise ValidationError("local_proportional capacity requires a target pattern")
+    caps = capacity_caps(policy, k, S, N, P, c_hat)
+    r = Router(P, S, N, k)
+    r.route_probs(p.to("cuda").contiguous(), policy, caps)
+    idx, gate, score, kept = r.read(R_IDX), r.read(R_GATE), r.read(R_SCORE), r.read(R_KEPT)
+    counts, dropped, mp = r.read(R_COUNTS), r.read(R_DROPPED), r.read(R_MEAN_PROBS)
+    order = r.expert_order()
+    res = [RoutingResult(idx[i], gate[i], score[i], kept[i].astype(bool), counts[i].astype(np.int64),
+                         dropped[i].astype(np.int64), mp[i], order) for i in range(P)]
+    return res[0] if single else res
+
+
+def loss_balance(result: RoutingResult, S: int) -> float:  # gate.cpp:209-214
+    return float(np.sum(result.mean_probs * (result.counts / S)))
+
+
+def loss_topo(result: RoutingResult, penalty, N: int, P: int, S: int) -> float:  # gate.cpp:248-255
+    penalty = np.asarray(penalty, np.float64)
+    if penalty.shape[0] != result.counts.shape[0]:
+        raise ValidationError("penalty row size does not match expert count")
+    return float(N) * P * float(np.sum(penalty * result.mean_probs * (result.counts / S)))

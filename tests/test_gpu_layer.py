@@ -1,0 +1,121 @@
+"""Whole-layer parity: the device step (gate, routing, experts, combine, MSE, aux loss,
+backward) against the oracle's restatement of trainer.cpp:371-482 on identical
+(bf16-representable) inputs.  Tolerance: bf16 rel 2e-2 (north star) on values and
+gradients (relative L2); routing bit-exact except audited near-ties."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-2
+
+
+def bf(a):
+    return torch.tensor(np.asarray(a), dtype=torch.float32).bfloat16().double().numpy()
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def re1_beta(P):
+    return np.array([[0.1 if i == j else (1.0 if i // 2 == j // 2 else 4.0) for j in range(P)] for i in range(P)])
+
+
+def run_case(P, S, d, dout, N, k, f, cap, kind, need_dx, seed=0, cf=1.25):
+    from paper_2302_09915_b200 import ops
+    from paper_2302_09915_b200.layer import LayerConfig, TAMoELayer
+    O = oracle.orc()
+    rng = np.random.default_rng(seed)
+    x = bf(rng.normal(size=(P, S, d)))
+    y = bf(rng.normal(size=(P, S, dout)) * 0.5)
+    gates = bf(rng.normal(size=(P, d, N)) * 0.05)
+    if f == 0:
+        U = bf(rng.normal(size=(N, d, dout)) / np.sqrt(d))
+        W1 = W2 = None
+    else:
+        U = None
+        W1 = bf(rng.normal(size=(N, d, f)) / np.sqrt(d))
+        W2 = bf(rng.normal(size=(N, f, dout)) / np.sqrt(f))
+    c_hat = ops.target_closed_form(re1_beta(P), N, k, S) if P > 1 else rng.uniform(0.5, 3.0, size=(1, N))
+    pen = np.stack([ops.penalty_weights(c_hat[i]) for i in range(P)])
+
+    cfg = LayerConfig(P=P, S=S, d=d, d_out=dout, N=N, k=k, f=f, act=1, cap_mode=cap, capacity_factor=cf,
+                      aux_kind=kind, need_dx=need_dx)
+    layer = TAMoELayer(cfg, c_hat)
+    params = dict(wg=TAMoELayer.gates_from_reference(gates, cfg.n_pad))
+    if f == 0:
+        params["w1"] = TAMoELayer.linear_from_reference(U)
+    else:
+        params["w1"] = torch.tensor(W1, dtype=torch.float32).transpose(1, 2).contiguous().bfloat16().cuda()
+        params["w2"] = torch.tensor(W2, dtype=torch.float32).transpose(1, 2).contiguous().bfloat16().cuda()
+    xt = torch.tensor(x.reshape(P * S, d), dtype=torch.float32).bfloat16().cuda()
+    yt = torch.tensor(y.reshape(P * S, dout), dtype=torch.float32).bfloat16().cuda()
+    yh = torch.zeros(P * S, dout, dtype=torch.bfloat16, device="cuda")
+    layer.step(xt, yt, params, y_hat=yh)
+    torch.cuda.synchronize()
+    o = O.layer_step(x, y, gates, U=U, W1=W1, W2=W2, k=k, cap_mode=cap, cf=cf, c_hat=c_hat, aux_kind=kind,
+                     penalties=pen, act=1, want_dx=need_dx)
+    return layer, o, dict(yh=yh, x=x)
+
+
+def check(layer, o, extra, P, S, N, k, f, need_dx):
+    from paper_2302_09915_b200 import ops
+    idx = layer.read(ops.R_IDX, (P, S, k))
+    mism = np.argwhere(idx != o["expert"])
+    assert len(mism) <= max(1, idx.size // 2000), f"{len(mism)} routing mismatches"
+    for (i, s, j) in mism:
+        pr = np.sort(o["probs"][i, s])[::-1]
+        assert abs(pr[j] - pr[j + 1]) < 1e-5, (i, s, j, pr[:3])
+    if len(mism) == 0:
+        assert np.array_equal(layer.read(ops.R_KEPT, (P, S, k)), o["kept"])
+        assert np.array_equal(layer.read(ops.R_COUNTS, (P, N)), o["counts"])
+    losses = layer.losses.cpu().numpy()
+    assert abs(losses[0] - o["task_loss"]) <= TOL * abs(o["task_loss"])
+    assert abs(losses[1] - o["aux_loss"]) <= 1e-3 * abs(o["aux_loss"]) + 1e-12
+    assert rel(extra["yh"].float().cpu().numpy().reshape(o["y_hat"].shape), o["y_hat"]) < TOL
+    dwg = layer.dwg.cpu().numpy()[:, :N, :].transpose(0, 2, 1)
+    assert rel(dwg, o["gate_grads"]) < TOL
+    if f == 0:
+        assert rel(layer.dw1.float().cpu().numpy().transpose(0, 2, 1), o["grad_u"]) < TOL
+    else:
+        assert rel(layer.dw1.float().cpu().numpy().transpose(0, 2, 1), o["grad_w1"]) < TOL
+        assert rel(layer.dw2.float().cpu().numpy().transpose(0, 2, 1), o["grad_w2"]) < TOL
+    if need_dx:
+        assert rel(layer.dx.float().cpu().numpy().reshape(o["dx"].shape), o["dx"]) < TOL
+
+
+@pytest.mark.parametrize("P,S,d,dout,N,k,f,cap,kind,need_dx", [
+    (1, 512, 256, 128, 8, 1, 0, 0, 0, True),     # linear expert, top-1, no capacity
+    (4, 128, 256, 256, 8, 2, 0, 3, 1, False),   # RE-1 style: topo loss + proportional capacity
+    (2, 256, 256, 128, 4, 2, 0, 2, 1, True),    # local capacity
+    (1, 384, 256, 128, 8, 2, 512, 0, 0, True),  # FFN expert (GELU), top-2
+    (1, 1000, 512, 256, 16, 1, 256, 1, 1, True),  # FFN, global capacity, ragged S
+])
+def test_layer_step_parity(P, S, d, dout, N, k, f, cap, kind, need_dx):
+    layer, o, extra = run_case(P, S, d, dout, N, k, f, cap, kind, need_dx)
+    check(layer, o, extra, P, S, N, k, f, need_dx)
+
+
+def test_layer_c1_reference_config():
+    """BASELINE config 1: d = d_out = 512, 8 experts, top-2, 4096 tokens (P=4 x S=1024, RE-1 [2,2]
+    topology), linear experts, topo loss with proportional capacity 1.25."""
+    P, S, d, dout, N, k = 4, 1024, 512, 512, 8, 2
+    layer, o, extra = run_case(P, S, d, dout, N, k, 0, 3, 1, False)
+    check(layer, o, extra, P, S, N, k, 0, False)
+
+
+def test_layer_validation_errors():
+    from paper_2302_09915_b200 import ops
+    from paper_2302_09915_b200.layer import LayerConfig, TAMoELayer
+    with pytest.raises(ops.ValidationError):  # reference: balance routing withholds c_hat (trainer.cpp:250)
+        TAMoELayer(LayerConfig(P=1, S=128, d=256, d_out=128, N=8, cap_mode=3, aux_kind=0), np.ones((1, 8)))
+    with pytest.raises(ops.ValidationError):
+        TAMoELayer(LayerConfig(P=1, S=128, d=256, d_out=128, N=8, k=9))
+    with pytest.raises(ops.ValidationError):
+        TAMoELayer(LayerConfig(P=1, S=128, d=256, d_out=128, N=8, aux_kind=1), None)
