@@ -156,6 +156,13 @@ int tamoe_layer_destroy(tamoe_layer* l);
 int tamoe_layer_step(tamoe_layer* l, const tamoe_layer_io* io, void* stream);
 int tamoe_layer_read(tamoe_layer* l, int what, void* dst, long long bytes, void* stream);
 int tamoe_layer_n_pad(int N);
+/* Kernel launches of libtamoe per step (memsets excluded). */
+int tamoe_layer_launches_per_step(tamoe_layer* l);
+/* Per-launch CUDA-event timing of the step on its stream (enable != 0 turns it on and resets totals).
+ * tamoe_layer_timing reads accumulated milliseconds per launch slot: names[i] (static strings), ms[i];
+ * returns the slot count through *n and the number of timed steps through *steps. */
+int tamoe_layer_enable_timing(tamoe_layer* l, int enable);
+int tamoe_layer_timing(tamoe_layer* l, const char** names, double* ms, int cap, int* n, int* steps);
 
 #ifdef __cplusplus
 }

@@ -2,6 +2,7 @@
 // exceptions into the reference's status convention via guarded().
 #include "../../include/tamoe.h"
 
+#include <algorithm>
 #include <cstring>
 
 #include "capi_util.hpp"
@@ -230,5 +231,31 @@ int tamoe_layer_read(tamoe_layer* l, int what, void* dst, long long bytes, void*
 }
 
 int tamoe_layer_n_pad(int N) { return (N + 15) & ~15; }
+
+int tamoe_layer_launches_per_step(tamoe_layer* l) { return l ? l->impl.launches_per_step() : -1; }
+
+int tamoe_layer_enable_timing(tamoe_layer* l, int enable) {
+  return guarded([&] {
+    require(l != nullptr, "null layer");
+    PhaseTimer& t = l->impl.timer();
+    t.reset();
+    t.enabled = enable != 0;
+  });
+}
+
+int tamoe_layer_timing(tamoe_layer* l, const char** names, double* ms, int cap, int* n, int* steps) {
+  return guarded([&] {
+    require(l && names && ms && n && steps, "timing: null argument");
+    PhaseTimer& t = l->impl.timer();
+    t.fold();
+    const int m = std::min(cap, t.n);
+    for (int i = 0; i < m; ++i) {
+      names[i] = t.names[i];
+      ms[i] = t.total_ms[i];
+    }
+    *n = m;
+    *steps = t.steps;
+  });
+}
 
 }  // extern "C"

@@ -78,6 +78,60 @@ Router::Router(int P, int S, int N, int k) {
   arena.commit();
 }
 
+// ------------------------------------------------------------------------------------ timing
+void PhaseTimer::begin(cudaStream_t s) {
+  if (!enabled) return;
+  std::vector<cudaEvent_t> set;
+  if (!pool.empty()) {
+    set = std::move(pool.back());
+    pool.pop_back();
+  } else {
+    set.resize(kMax + 1);
+    for (auto& e : set) TAMOE_CUDA(cudaEventCreate(&e));
+  }
+  pending.push_back(std::move(set));
+  cur = &pending.back();
+  n = 0;
+  TAMOE_CUDA(cudaEventRecord((*cur)[0], s));
+}
+
+void PhaseTimer::mark(const char* name, cudaStream_t s) {
+  if (!enabled || cur == nullptr || n >= kMax) return;
+  names[n] = name;
+  TAMOE_CUDA(cudaEventRecord((*cur)[++n], s));
+}
+
+void PhaseTimer::end(cudaStream_t) {
+  cur = nullptr;
+  if (enabled && pending.size() >= 64) fold();
+}
+
+void PhaseTimer::fold() {
+  for (auto& set : pending) {
+    TAMOE_CUDA(cudaEventSynchronize(set[n]));
+    for (int i = 0; i < n; ++i) {
+      float ms = 0.f;
+      TAMOE_CUDA(cudaEventElapsedTime(&ms, set[i], set[i + 1]));
+      total_ms[i] += ms;
+    }
+    ++steps;
+    pool.push_back(std::move(set));
+  }
+  pending.clear();
+}
+
+void PhaseTimer::reset() {
+  fold();
+  steps = 0;
+  for (double& v : total_ms) v = 0.0;
+}
+
+PhaseTimer::~PhaseTimer() {
+  for (auto* v : {&pending, &pool})
+    for (auto& set : *v)
+      for (auto e : set) cudaEventDestroy(e);
+}
+
 // ------------------------------------------------------------------------------------ Layer
 Layer::Layer(const LayerConfig& c, const double* c_hat) : cfg_(c) {
   require(c.world_size == 1, "expert parallelism across ranks is configured through tamoe_layer_create_ep");
@@ -140,16 +194,26 @@ void Layer::step(const LayerIO& io, cudaStream_t s) {
   const RouteDims& dm = rw_.dims;
   const int E = c.N;  // experts on this device
   // ---- forward: gate + routing
+  PhaseTimer& tm = timer_;
+  tm.begin(s);
   TAMOE_CUDA(cudaMemsetAsync(b.bad, 0, sizeof(int), s));
   gate_forward(io.x, io.wg, n_pad_, dm, c.d, rw_.row_out(logits_, nullptr), s);
-  rw_.finish(c.cap_mode, s);
+  tm.mark("gate_fwd", s);
+  route_bucket(dm, b, s);
+  tm.mark("route_bucket", s);
+  route_capacity(dm, b, c.cap_mode, rw_.caps, s);
+  tm.mark("route_capacity", s);
   route_permute(dm, b, io.x, c.d, xp_, r_max_, dO_, c.d_out, s);
+  tm.mark("permute", s);
   // ---- forward: experts
   if (c.f == 0) {
     grouped_fwd(xp_, io.w1, E, c.d_out, c.d, r_max_, b.seg_start, b.seg_rows, O_, nullptr, kActNone, s);
+    tm.mark("expert_fwd", s);
   } else {
     grouped_fwd(xp_, io.w1, E, c.f, c.d, r_max_, b.seg_start, b.seg_rows, H_, A_, c.act, s);
+    tm.mark("expert_fwd1", s);
     grouped_fwd(H_, io.w2, E, c.d_out, c.f, r_max_, b.seg_start, b.seg_rows, O_, nullptr, kActNone, s);
+    tm.mark("expert_fwd2", s);
   }
   // ---- combine + task loss + dO
   CombineArgs ca{};
@@ -166,17 +230,26 @@ void Layer::step(const LayerIO& io, cudaStream_t s) {
   ca.dldg = dldg_;
   ca.loss_part = loss_part_;
   combine_loss(ca, s);
+  tm.mark("combine_loss", s);
   // ---- backward: experts
   if (c.f == 0) {
     grouped_wgrad(dO_, xp_, E, c.d_out, c.d, r_max_, b.seg_start, b.seg_rows, io.dw1, s);
-    if (c.need_dx)
+    tm.mark("expert_wgrad", s);
+    if (c.need_dx) {
       grouped_dgrad(dO_, io.w1, E, c.d, c.d_out, r_max_, b.seg_start, b.seg_rows, dxp_, nullptr, kActNone, s);
+      tm.mark("expert_dgrad", s);
+    }
   } else {
     grouped_dgrad(dO_, io.w2, E, c.f, c.d_out, r_max_, b.seg_start, b.seg_rows, dA_, A_, c.act, s);
+    tm.mark("expert_dgrad2", s);
     grouped_wgrad(dO_, H_, E, c.d_out, c.f, r_max_, b.seg_start, b.seg_rows, io.dw2, s);
+    tm.mark("expert_wgrad2", s);
     grouped_wgrad(dA_, xp_, E, c.f, c.d, r_max_, b.seg_start, b.seg_rows, io.dw1, s);
-    if (c.need_dx)
+    tm.mark("expert_wgrad1", s);
+    if (c.need_dx) {
       grouped_dgrad(dA_, io.w1, E, c.d, c.f, r_max_, b.seg_start, b.seg_rows, dxp_, nullptr, kActNone, s);
+      tm.mark("expert_dgrad1", s);
+    }
   }
   // ---- backward: gate
   GateDzArgs ga{};
@@ -201,8 +274,22 @@ void Layer::step(const LayerIO& io, cudaStream_t s) {
   ga.losses = io.losses;
   ga.dz = dz_;
   gate_dz(ga, s);
+  tm.mark("gate_dz", s);
   gate_dw(io.x, dz_, c.P, c.S, c.d, n64_, n_pad_, c.N, dw_part_, dw_splits_, io.dwg, s);
-  if (c.need_dx) gate_dx(dz_, io.wg, c.P, c.S, c.d, n64_, n_pad_, dxp_, b.pos, c.k, io.dx, s);
+  tm.mark("gate_dw", s);
+  if (c.need_dx) {
+    gate_dx(dz_, io.wg, c.P, c.S, c.d, n64_, n_pad_, dxp_, b.pos, c.k, io.dx, s);
+    tm.mark("gate_dx", s);
+  }
+  tm.end(s);
+}
+
+int Layer::launches_per_step() const {
+  // gate, bucket, capacity, permute, combine, dz, dW GEMM + reduce
+  int n = 8;
+  n += cfg_.f == 0 ? (1 + 1 + (cfg_.need_dx ? 1 : 0)) : (2 + 3 + (cfg_.need_dx ? 1 : 0));
+  if (cfg_.need_dx) n += 1;
+  return n;
 }
 
 }  // namespace tamoe

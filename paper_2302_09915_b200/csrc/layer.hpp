@@ -82,6 +82,26 @@ struct LayerIO {
   double* losses;
 };
 
+// Per-launch timing of the step: CUDA events recorded on the step's stream with no
+// host synchronisation inside the step; folded into per-launch totals on read.
+struct PhaseTimer {
+  static constexpr int kMax = 24;
+  bool enabled = false;
+  int n = 0;  // launch slots in a step
+  const char* names[kMax] = {};
+  double total_ms[kMax] = {};
+  int steps = 0;
+  std::vector<std::vector<cudaEvent_t>> pending;  // one event set per step not yet folded
+  std::vector<std::vector<cudaEvent_t>> pool;
+  std::vector<cudaEvent_t>* cur = nullptr;
+  void begin(cudaStream_t s);
+  void mark(const char* name, cudaStream_t s);
+  void end(cudaStream_t s);
+  void fold();  // synchronises on the recorded events
+  void reset();
+  ~PhaseTimer();
+};
+
 class Layer {
  public:
   Layer(const LayerConfig& cfg, const double* c_hat);
@@ -91,6 +111,8 @@ class Layer {
   int n_pad() const { return n_pad_; }
   int r_max() const { return r_max_; }
   const float* logits() const { return logits_; }
+  PhaseTimer& timer() { return timer_; }
+  int launches_per_step() const;
 
  private:
   LayerConfig cfg_;
@@ -103,6 +125,7 @@ class Layer {
   float *logits_ = nullptr, *dldg_ = nullptr, *dw_part_ = nullptr;
   double *penalties_ = nullptr, *loss_part_ = nullptr;
   int n_loss_part_ = 0;
+  PhaseTimer timer_;
 };
 
 }  // namespace tamoe

@@ -41,7 +41,13 @@ _lib.lib.tamoe_layer_destroy.argtypes = [ctypes.c_void_p]
 _lib.lib.tamoe_layer_step.argtypes = [ctypes.c_void_p, ctypes.POINTER(_IO), ctypes.c_void_p]
 _lib.lib.tamoe_layer_read.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_longlong,
                                       ctypes.c_void_p]
-for _n in ("tamoe_layer_create", "tamoe_layer_destroy", "tamoe_layer_step", "tamoe_layer_read"):
+_lib.lib.tamoe_layer_launches_per_step.argtypes = [ctypes.c_void_p]
+_lib.lib.tamoe_layer_enable_timing.argtypes = [ctypes.c_void_p, ctypes.c_int]
+_lib.lib.tamoe_layer_timing.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_char_p),
+                                        ctypes.POINTER(ctypes.c_double), ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                        ctypes.POINTER(ctypes.c_int)]
+for _n in ("tamoe_layer_create", "tamoe_layer_destroy", "tamoe_layer_step", "tamoe_layer_read",
+           "tamoe_layer_launches_per_step", "tamoe_layer_enable_timing", "tamoe_layer_timing"):
     getattr(_lib.lib, _n).restype = ctypes.c_int
 
 
@@ -138,6 +144,22 @@ class TAMoELayer:
         _lib.check(_lib.lib.tamoe_layer_read(self._h, what, out.ctypes.data_as(ctypes.c_void_p), out.nbytes,
                                              ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
         return out
+
+    def launches_per_step(self) -> int:
+        return _lib.lib.tamoe_layer_launches_per_step(self._h)
+
+    def enable_timing(self, on=True):
+        _lib.check(_lib.lib.tamoe_layer_enable_timing(self._h, int(on)))
+
+    def timing(self):
+        """{launch name: average ms per step} from the CUDA events recorded on the step stream."""
+        cap = 32
+        names = (ctypes.c_char_p * cap)()
+        ms = (ctypes.c_double * cap)()
+        n, steps = ctypes.c_int(), ctypes.c_int()
+        _lib.check(_lib.lib.tamoe_layer_timing(self._h, names, ms, cap, ctypes.byref(n), ctypes.byref(steps)))
+        st = max(steps.value, 1)
+        return {names[i].decode(): ms[i] / st for i in range(n.value)}, steps.value
 
     # ------------------------------------------------------------------ reference-layout converters
     @staticmethod
