@@ -35,59 +35,77 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
   return v;
 }
 
+// KT = compile-time top-k (0: runtime k <= kMaxTopK).  Each lane keeps kU 16-byte vectors of every
+// slot in flight before computing, so the warp has (k + 1) * kU * 512 B of loads outstanding.
+template <int KT>
 __global__ void __launch_bounds__(kCombWarps * 32) combine_loss_kernel(CombineArgs a) {
+  constexpr int KM = KT > 0 ? KT : kMaxTopK;
+  constexpr int kU = 4;
   __shared__ double wsum[kCombWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long t = static_cast<long long>(blockIdx.x) * kCombWarps + warp;
   double lsum = 0.0;
   if (t < a.T) {
-    const int k = a.k;
-    int rows[kMaxTopK];
-    float g[kMaxTopK], dot[kMaxTopK];
+    const int k = KT > 0 ? KT : a.k;
+    int rows[KM];
+    float g[KM], dot[KM];
 #pragma unroll
-    for (int j = 0; j < kMaxTopK; ++j) {
+    for (int j = 0; j < KM; ++j) {
       rows[j] = (j < k) ? a.pos[t * k + j] : -1;
       g[j] = (j < k) ? a.gate[t * k + j] : 0.f;
       dot[j] = 0.f;
     }
     const int nv = a.dout / 8;
-    const uint4* y4 = reinterpret_cast<const uint4*>(a.y + t * a.dout);
-    for (int v = lane; v < nv; v += 32) {
-      float yh[8];
+    const uint4* __restrict__ y4 = reinterpret_cast<const uint4*>(a.y + t * a.dout);
+    for (int v0 = lane; v0 < nv; v0 += 32 * kU) {
+      uint4 yv[kU], ov[KM][kU];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) yh[i] = 0.f;
-      float o[kMaxTopK][8];
+      for (int u = 0; u < kU; ++u) {
+        const int v = v0 + 32 * u;
+        yv[u] = v < nv ? y4[v] : make_uint4(0, 0, 0, 0);
 #pragma unroll
-      for (int j = 0; j < kMaxTopK; ++j) {
-        if (rows[j] >= 0) {
-          unpack8(reinterpret_cast<const uint4*>(a.O + static_cast<long long>(rows[j]) * a.dout)[v], o[j]);
+        for (int j = 0; j < KM; ++j)
+          ov[j][u] = (rows[j] >= 0 && v < nv)
+                         ? reinterpret_cast<const uint4*>(a.O + static_cast<long long>(rows[j]) * a.dout)[v]
+                         : make_uint4(0, 0, 0, 0);
+      }
 #pragma unroll
-          for (int i = 0; i < 8; ++i) yh[i] += g[j] * o[j][i];
+      for (int u = 0; u < kU; ++u) {
+        const int v = v0 + 32 * u;
+        if (v >= nv) break;
+        float yh[8], o[KM][8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) yh[i] = 0.f;
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {
+          unpack8(ov[j][u], o[j]);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) yh[i] += g[j] * o[j][i];  // dropped slots hold zeros
         }
-      }
-      if (a.y_hat) reinterpret_cast<uint4*>(a.y_hat + t * a.dout)[v] = pack8(yh);
-      float yy[8], r[8];
-      unpack8(y4[v], yy);
+        if (a.y_hat) reinterpret_cast<uint4*>(a.y_hat + t * a.dout)[v] = pack8(yh);
+        float yy[8], r[8];
+        unpack8(yv[u], yy);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        r[i] = yh[i] - yy[i];
-        lsum += static_cast<double>(r[i]) * r[i];
-      }
+        for (int i = 0; i < 8; ++i) {
+          r[i] = yh[i] - yy[i];
+          lsum += static_cast<double>(r[i]) * r[i];
+        }
 #pragma unroll
-      for (int j = 0; j < kMaxTopK; ++j) {
-        if (rows[j] >= 0) {
-          float go[8];
+        for (int j = 0; j < KM; ++j) {
+          if (rows[j] >= 0) {
+            float go[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            dot[j] += r[i] * o[j][i];
-            go[i] = a.mse_scale * g[j] * r[i];
+            for (int i = 0; i < 8; ++i) {
+              dot[j] += r[i] * o[j][i];
+              go[i] = a.mse_scale * g[j] * r[i];
+            }
+            reinterpret_cast<uint4*>(a.dO + static_cast<long long>(rows[j]) * a.dout)[v] = pack8(go);
           }
-          reinterpret_cast<uint4*>(a.dO + static_cast<long long>(rows[j]) * a.dout)[v] = pack8(go);
         }
       }
     }
 #pragma unroll
-    for (int j = 0; j < kMaxTopK; ++j) {
+    for (int j = 0; j < KM; ++j) {
       if (j < k) {
         float s = dot[j];
 #pragma unroll
@@ -114,7 +132,10 @@ int combine_blocks(long long T) { return static_cast<int>((T + kCombWarps - 1) /
 void combine_loss(const CombineArgs& a, cudaStream_t s) {
   require(a.dout % 8 == 0, "combine: d_out must be a multiple of 8");
   require(a.k >= 1 && a.k <= kMaxTopK, "combine: k out of range");
-  combine_loss_kernel<<<combine_blocks(a.T), kCombWarps * 32, 0, s>>>(a);
+  const int blocks = combine_blocks(a.T);
+  if (a.k == 1) combine_loss_kernel<1><<<blocks, kCombWarps * 32, 0, s>>>(a);
+  else if (a.k == 2) combine_loss_kernel<2><<<blocks, kCombWarps * 32, 0, s>>>(a);
+  else combine_loss_kernel<0><<<blocks, kCombWarps * 32, 0, s>>>(a);
   TAMOE_CUDA(cudaGetLastError());
 }
 

@@ -22,8 +22,9 @@ struct EpiGate {
     RowRouteOut o;
     int N, k, S, TB;
   };
+  static __device__ __forceinline__ void finish(const Params&, int, int) {}
   static __device__ __forceinline__ void run(const Params& e, const GemmParams& p, const TileInfo& ti,
-                                             uint32_t tmem_tile, int q, int lane) {
+                                             uint32_t tmem_tile, int q, int lane, uint8_t*) {
     const int row = q * 32 + lane;
     const int tok = ti.m0 + row;
     const bool valid = tok < e.S;

@@ -142,8 +142,9 @@ struct EpiGateDw {
     float* part;
     int d, n64, P;
   };
+  static __device__ __forceinline__ void finish(const Params&, int, int) {}
   static __device__ __forceinline__ void run(const Params& e, const GemmParams& p, const TileInfo& ti,
-                                             uint32_t tmem_tile, int q, int lane) {
+                                             uint32_t tmem_tile, int q, int lane, uint8_t*) {
     const int m = ti.m0 + q * 32 + lane;
     for (int c0 = 0; c0 < ti.n; c0 += 32) {
       float v[32];
@@ -185,8 +186,9 @@ struct EpiGateDx {
     const int* pos;
     int k, S, d;
   };
+  static __device__ __forceinline__ void finish(const Params&, int, int) {}
   static __device__ __forceinline__ void run(const Params& e, const GemmParams& p, const TileInfo& ti,
-                                             uint32_t tmem_tile, int q, int lane) {
+                                             uint32_t tmem_tile, int q, int lane, uint8_t*) {
     const int tok = ti.m0 + q * 32 + lane;
     const bool valid = tok < e.S;  // tcgen05.ld is warp-collective: every lane runs the loop
     const long long gtok = static_cast<long long>(ti.g) * e.S + tok;

@@ -9,7 +9,7 @@ template <int kMode, int BN, bool A_MN, bool B_MN, class Epi>
 void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, const typename Epi::Params& ep,
                  int grid_limit, cudaStream_t s) {
   auto kern = gemm_sm100_kernel<kMode, BN, A_MN, B_MN, Epi>;
-  const int smem = GemmSmem<BN>::kTotal;
+  const int smem = GemmSmem<BN, EpiSmem<Epi>::value>::kTotal;
   static bool configured = false;
   if (!configured) {
     TAMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

@@ -53,14 +53,28 @@ struct TileInfo {
   int bx, by;  // B TMA base coordinates
 };
 
-template <int BN>
+// Epilogues may declare `static constexpr int kSmemBytes` of scratch shared memory (per CTA).
+template <class Epi, class = void>
+struct EpiSmem {
+  static constexpr int value = 0;
+};
+template <class Epi>
+struct EpiSmem<Epi, decltype(void(Epi::kSmemBytes))> {
+  static constexpr int value = Epi::kSmemBytes;
+};
+
+template <int BN, int kEpiBytes = 0>
 struct GemmSmem {
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (BN >= 256) ? 4 : (BN >= 128 ? 6 : 8);
+  static constexpr int kBudget = 220 * 1024 - kEpiBytes - 8 * 1024;
+  static constexpr int kMaxStages = (BN >= 256) ? 4 : (BN >= 128 ? 6 : 8);
+  static constexpr int kStages = (kBudget / kStageBytes < kMaxStages) ? kBudget / kStageBytes : kMaxStages;
+  static_assert(kStages >= 2, "not enough shared memory for the pipeline");
+  static constexpr int kEpiOffset = kStages * kStageBytes;
   static constexpr int kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
-  static constexpr int kBarOffset = kStages * kStageBytes;
+  static constexpr int kBarOffset = kEpiOffset + ((kEpiBytes + 1023) / 1024) * 1024;
   // barriers: full[S], empty[S], tfull[2], tempty[2]; tmem addr; tile prefix
   static constexpr int kMiscBytes = (2 * kStages + 4) * 8 + 16 + (kMaxGroups + 1) * 4;
   static constexpr int kTotal = kBarOffset + kMiscBytes + 1024;  // + alignment slack
@@ -162,12 +176,14 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, const int* pref
 
 // Epilogue contract:
 //   struct Epi { struct Params; static __device__ void run(const Params&, const GemmParams&,
-//                const TileInfo&, uint32_t tmem_tile /*lane 0 col 0 of this tile*/, int q /*warp*/, int lane); };
+//                const TileInfo&, uint32_t tmem_tile /*lane 0 col 0 of this tile*/, int q /*warp*/, int lane,
+//                uint8_t* smem /*kSmemBytes scratch*/);
+//                static __device__ void finish(const Params&, int q, int lane); };
 template <int kMode, int BN, bool A_MN, bool B_MN, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                      const GemmParams p, const typename Epi::Params ep) {
-  using L = GemmSmem<BN>;
+                      const GemmParams p, const __grid_constant__ typename Epi::Params ep) {
+  using L = GemmSmem<BN, EpiSmem<Epi>::value>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
@@ -293,11 +309,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       ptx::mbar_wait(&tfull_bar[buf], use & 1);
       ptx::tc_fence_after();
       const uint32_t tmem_tile = tmem_base + buf * BN + (static_cast<uint32_t>(warp * 32) << 16);
-      Epi::run(ep, p, ti, tmem_tile, warp, lane);
+      Epi::run(ep, p, ti, tmem_tile, warp, lane, smem + L::kEpiOffset);
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&tempty_bar[buf]);
     }
+    Epi::finish(ep, warp, lane);
   }
   __syncthreads();
   if (warp == 5) {

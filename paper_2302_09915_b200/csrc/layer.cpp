@@ -42,6 +42,7 @@ void RouteWorkspace::reserve(Arena& a, int P, int S, int N, int k) {
   a.reserve(buf.pos, picks);
   a.reserve(buf.hist4, tw);
   a.reserve(buf.msum4, tw);
+  a.reserve(buf.base4, tw);
   a.reserve(buf.list_pick, picks);
   a.reserve(buf.list_score, picks);
   a.reserve(buf.clist, picks);
@@ -285,8 +286,8 @@ void Layer::step(const LayerIO& io, cudaStream_t s) {
 }
 
 int Layer::launches_per_step() const {
-  // gate, bucket, capacity, permute, combine, dz, dW GEMM + reduce
-  int n = 8;
+  // gate, scan, bucket, capacity, permute, combine, dz, dW GEMM + reduce
+  int n = 9;
   n += cfg_.f == 0 ? (1 + 1 + (cfg_.need_dx ? 1 : 0)) : (2 + 3 + (cfg_.need_dx ? 1 : 0));
   if (cfg_.need_dx) n += 1;
   return n;

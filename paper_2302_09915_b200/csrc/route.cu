@@ -56,58 +56,71 @@ __device__ int block_excl_scan(int* a, int n, int* wtmp) {
   return total;
 }
 
+// ---------------------------------------------------------------- scan
+// One CTA per expert: exclusive prefix of the per-(tile, warp) pick counts in
+// (process, token) order -> base4, plus per-(process, expert) bucket ranges.
+constexpr int kScanThreads = 512;
+
+__global__ void __launch_bounds__(kScanThreads) route_scan_kernel(RouteDims d, RouteBuffers b) {
+  __shared__ int wsum[32];
+  __shared__ int carry_s;
+  const int e = blockIdx.x, N = d.N;
+  const int entries = d.tiles() * 4;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) carry_s = 0;
+  __syncthreads();
+  for (int j0 = 0; j0 < entries; j0 += blockDim.x) {
+    const int j = j0 + threadIdx.x;
+    const int c = j < entries ? b.hist4[static_cast<long long>(j) * N + e] : 0;
+    int x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    int before = carry_s;
+    for (int i = 0; i < w; ++i) before += wsum[i];
+    const int excl = before + x - c;
+    if (j < entries) {
+      b.base4[static_cast<long long>(j) * N + e] = excl;
+      if (j % (d.TB * 4) == 0) b.bucket_start[(j / (d.TB * 4)) * N + e] = excl;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int i = 0; i < nw; ++i) carry_s += wsum[i];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) b.list_count[e] = carry_s;
+  __syncthreads();
+  for (int pr = threadIdx.x; pr < d.P; pr += blockDim.x) {
+    const int st = b.bucket_start[pr * N + e];
+    const int en = pr + 1 < d.P ? b.bucket_start[(pr + 1) * N + e] : carry_s;
+    b.bucket_count[pr * N + e] = en - st;
+  }
+}
+
 // ---------------------------------------------------------------- bucket
 // One CTA per 128-token tile.  Position of a pick in its expert's list =
-// list_start[e] + picks to e in earlier tiles + earlier warps + earlier lanes.
+// list_start[e] + picks to e in earlier (tile, warp) slots + earlier lanes of its warp.
 __global__ void __launch_bounds__(kRouteTile) route_bucket_kernel(RouteDims d, RouteBuffers b) {
   extern __shared__ int sm[];
   const int N = d.N, k = d.k;
-  int* base = sm;                      // [N]  list start + earlier tiles
-  int* wbase = base + N;               // [4*N]
+  int* wbase = sm;                     // [4*N]
   int* sel = wbase + 4 * N;            // [128*k]
   int* wtmp = sel + kRouteTile * k;    // [32]
-  int* tot = wtmp + 32;                // [N]
+  int* ls = wtmp + 32;                 // [N]
   const int tile = blockIdx.x;
-  const int tiles = d.tiles();
-  for (int e = threadIdx.x; e < N; e += blockDim.x) {
-    int before = 0, all = 0;
-    for (int t = 0; t < tiles; ++t) {
-      const int* h = b.hist4 + static_cast<long long>(t) * 4 * N + e;
-      const int c = h[0] + h[N] + h[2 * N] + h[3 * N];
-      all += c;
-      if (t < tile) before += c;
-    }
-    tot[e] = all;
-    base[e] = before;
-  }
+  for (int e = threadIdx.x; e < N; e += blockDim.x) ls[e] = b.list_count[e];
   __syncthreads();
-  block_excl_scan(tot, N, wtmp);  // tot -> list_start
-  for (int e = threadIdx.x; e < N; e += blockDim.x) {
-    const int* h = b.hist4 + static_cast<long long>(tile) * 4 * N + e;
-    int acc = tot[e] + base[e];
-    for (int w = 0; w < 4; ++w) {
-      wbase[w * N + e] = acc;
-      acc += h[w * N];
-    }
+  block_excl_scan(ls, N, wtmp);
+  for (int i = threadIdx.x; i < 4 * N; i += blockDim.x) {
+    const int w = i / N, e = i % N;
+    wbase[i] = ls[e] + b.base4[(static_cast<long long>(tile) * 4 + w) * N + e];
   }
-  if (blockIdx.x == 0) {
-    // expert list starts / counts and per-(process, expert) buckets, written once
-    for (int e = threadIdx.x; e < N; e += blockDim.x) {
-      b.list_start[e] = tot[e];
-      int acc = 0;
-      for (int pr = 0; pr < d.P; ++pr) {
-        int c = 0;
-        for (int t = pr * d.TB; t < (pr + 1) * d.TB; ++t) {
-          const int* h = b.hist4 + static_cast<long long>(t) * 4 * N + e;
-          c += h[0] + h[N] + h[2 * N] + h[3 * N];
-        }
-        b.bucket_start[pr * N + e] = acc;
-        b.bucket_count[pr * N + e] = c;
-        acc += c;
-      }
-      b.list_count[e] = acc;
-    }
-  }
+  if (blockIdx.x == 0)
+    for (int e = threadIdx.x; e < N; e += blockDim.x) b.list_start[e] = ls[e];
   const int proc = tile / d.TB;
   const int tok = (tile % d.TB) * kRouteTile + threadIdx.x;
   const bool valid = tok < d.S;
@@ -115,7 +128,7 @@ __global__ void __launch_bounds__(kRouteTile) route_bucket_kernel(RouteDims d, R
   for (int j = 0; j < k; ++j) sel[threadIdx.x * k + j] = valid ? b.idx[gtok * k + j] : -1;
   __syncthreads();
   if (!valid) return;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int w = threadIdx.x >> 5;
   for (int a = 0; a < k; ++a) {
     const int e = sel[threadIdx.x * k + a];
     int r = 0;
@@ -125,7 +138,6 @@ __global__ void __launch_bounds__(kRouteTile) route_bucket_kernel(RouteDims d, R
     b.list_pick[pos] = static_cast<int>(gtok * k + a);
     b.list_score[pos] = b.score[gtok * k + a];
   }
-  (void)lane;
 }
 
 // ---------------------------------------------------------------- capacity
@@ -243,17 +255,43 @@ __global__ void __launch_bounds__(kCapThreads) route_capacity_kernel(RouteDims d
     }
     __syncthreads();
   }
-  // per-bucket kept / dropped counts and mean probabilities (fixed-order sums)
-  for (int pr = threadIdx.x; pr < d.P; pr += blockDim.x) {
+  // per-bucket kept / dropped counts and mean probabilities (block-parallel, fixed-order sums)
+  __shared__ double dred[32];
+  __shared__ int ired[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int pr = 0; pr < d.P; ++pr) {
     const int bs = b.bucket_start[pr * N + e], bc = b.bucket_count[pr * N + e];
     int kc = 0;
-    for (int j = 0; j < bc; ++j) kc += b.list_keep[ls + bs + j];
-    b.counts[pr * N + e] = kc;
-    b.dropped[pr * N + e] = bc - kc;
+    if (mode == 1) {
+      for (int j = threadIdx.x; j < bc; j += blockDim.x) kc += b.list_keep[ls + bs + j];
+    } else if (threadIdx.x == 0) {
+      kc = mode == 0 ? bc : min(bc, max(caps[pr * N + e], 0));  // exactly cap picks survive
+    }
     double m = 0.0;
-    for (int t = pr * d.TB; t < (pr + 1) * d.TB; ++t)
-      for (int w = 0; w < 4; ++w) m += b.msum4[(static_cast<long long>(t) * 4 + w) * N + e];
-    b.mean_probs[pr * N + e] = m / d.S;
+    const int t0 = pr * d.TB * 4, t1 = (pr + 1) * d.TB * 4;
+    for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) m += b.msum4[static_cast<long long>(t) * N + e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      kc += __shfl_xor_sync(0xffffffffu, kc, o);
+      m += __shfl_xor_sync(0xffffffffu, m, o);
+    }
+    if (lane == 0) {
+      ired[w] = kc;
+      dred[w] = m;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int kt = 0;
+      double mt = 0.0;
+      for (int i = 0; i < nw; ++i) {
+        kt += ired[i];
+        mt += dred[i];
+      }
+      b.counts[pr * N + e] = kt;
+      b.dropped[pr * N + e] = bc - kt;
+      b.mean_probs[pr * N + e] = mt / d.S;
+    }
+    __syncthreads();
   }
 }
 
@@ -318,7 +356,9 @@ __global__ void __launch_bounds__(kPermWarps * 32) route_permute_kernel(RouteDim
 }  // namespace
 
 void route_bucket(const RouteDims& d, const RouteBuffers& b, cudaStream_t s) {
-  const size_t smem = sizeof(int) * (6 * d.N + kRouteTile * d.k + 32);
+  route_scan_kernel<<<d.N, kScanThreads, 0, s>>>(d, b);
+  TAMOE_CUDA(cudaGetLastError());
+  const size_t smem = sizeof(int) * (5 * d.N + kRouteTile * d.k + 32);
   route_bucket_kernel<<<d.tiles(), kRouteTile, smem, s>>>(d, b);
   TAMOE_CUDA(cudaGetLastError());
 }

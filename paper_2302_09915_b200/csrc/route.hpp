@@ -31,6 +31,7 @@ struct RouteBuffers {
   // per (tile, warp, expert) [tiles*4*N]
   int* hist4 = nullptr;
   double* msum4 = nullptr;
+  int* base4 = nullptr;  // exclusive prefix of hist4 per expert (route_scan)
   // expert lists [P*S*k]
   int* list_pick = nullptr;     // pre-capacity, expert-major, (process, token) order inside
   double* list_score = nullptr;

@@ -43,4 +43,20 @@ inline CUtensorMap make_tmap_bf16(const void* base, uint64_t inner, uint64_t out
   return m;
 }
 
+// General 2D bf16 map: box {box_inner, box_outer}, chosen swizzle (store-side epilogues).
+inline CUtensorMap make_tmap_bf16_box(const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+                                      uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swz) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw std::runtime_error("cuTensorMapEncodeTiled (store map) failed (" + std::to_string(static_cast<int>(r)) + ")");
+  return m;
+}
+
 }  // namespace tamoe
