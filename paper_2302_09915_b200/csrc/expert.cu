@@ -45,83 +45,96 @@ __device__ __forceinline__ float act_grad(int act, float x) {
 
 // ---------------------------------------------------------------- swap-AB epilogue
 // acc[lane = weight row m][col = token c]  ->  out[token row][m]
-// Per epilogue warp (32 features) and 32-token chunk: tcgen05.ld -> (x act'(pre), prefetched with
-// cp.async) -> bf16 staging tile [32 tokens][32 features] in smem -> one TMA bulk store.
+// Per epilogue warp (32 features, every other 32-token chunk): tcgen05.ld -> (x act'(pre), prefetched with
+// cp.async two chunks ahead, starting before the accumulator is ready) -> bf16 staging tile
+// [32 tokens][32 features] in smem -> one TMA bulk store.
+struct SwapParams {
+  CUtensorMap out32, out16;  // store maps of `out`: box {32 features, 32 | 16 tokens}
+  CUtensorMap pre32, pre16;  // store maps of `pre_out`
+  const __nv_bfloat16* pre_in;  // pre-activation for act' (dgrad)
+  int ld;
+  int act_out;   // activation applied on store (forward)
+  int act_grad;  // activation derivative multiplied in (dgrad)
+};
+
+// V = 0: plain store; 1: also store the pre-activation; 2: multiply act'(pre_in).
+template <int V>
 struct EpiSwap {
-  static constexpr int kChunk = 2048;            // 32 x 32 bf16
-  static constexpr int kWarpBytes = 6 * kChunk;  // out x2, pre_out x2, pre_in prefetch x2
-  static constexpr int kSmemBytes = 4 * kWarpBytes;
-  struct Params {
-    CUtensorMap out32, out16;  // store maps of `out`: box {32 features, 32 | 16 tokens}
-    CUtensorMap pre32, pre16;  // store maps of `pre_out`
-    const __nv_bfloat16* pre_in;  // optional: pre-activation for act' (dgrad)
-    int ld;
-    int act_out;   // activation applied on store (forward)
-    int act_grad;  // activation derivative multiplied in (dgrad)
-    int has_pre_out;
-  };
-  static __device__ __forceinline__ void run(const Params& e, const GemmParams& p, const TileInfo& ti,
-                                             uint32_t tmem_tile, int q, int lane, uint8_t* smem) {
-    uint8_t* ws = smem + q * kWarpBytes;
-    __nv_bfloat16* st_out = reinterpret_cast<__nv_bfloat16*>(ws);
-    __nv_bfloat16* st_pre = reinterpret_cast<__nv_bfloat16*>(ws + 2 * kChunk);
-    __nv_bfloat16* pf = reinterpret_cast<__nv_bfloat16*>(ws + 4 * kChunk);
-    const int mcol = ti.m0 + q * 32;
-    const int row0 = p.seg_start[ti.g] + ti.n0;
+  static constexpr int kChunk = 2048;  // 32 x 32 bf16
+  static constexpr int kPf = 2;        // own chunks of pre_in in flight
+  static constexpr int kWarpBytes = V == 0 ? 2 * kChunk : 4 * kChunk;
+  using Params = SwapParams;
+  static __device__ __forceinline__ void load_chunk(const Params& e, const TileInfo& ti, int row0, int mcol, int ch,
+                                                    __nv_bfloat16* slot, int lane) {
     const int nch = (ti.n + 31) / 32;
-    const bool has_pre_in = e.pre_in != nullptr;
-    // all earlier bulk stores of this warp must have finished reading the staging tiles
-    if (lane == 0) ptx::bulk_wait_read<0>();
-    __syncwarp();
-    auto prefetch = [&](int ch) {
-      __nv_bfloat16* dst = pf + (ch & 1) * 1024;
+    if (ch < nch) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int vid = lane + 32 * i;
         const int r = vid >> 2, part = vid & 3;
         const bool ok = ch * 32 + r < ti.n;
-        const __nv_bfloat16* src = e.pre_in + static_cast<long long>(row0 + ch * 32 + (ok ? r : 0)) * e.ld + mcol + part * 8;
-        ptx::cp_async_16(dst + r * 32 + part * 8, src, ok);
+        const __nv_bfloat16* src =
+            e.pre_in + static_cast<long long>(row0 + ch * 32 + (ok ? r : 0)) * e.ld + mcol + part * 8;
+        ptx::cp_async_16(slot + r * 32 + part * 8, src, ok);
       }
-      ptx::cp_async_commit();
-    };
-    if (has_pre_in) prefetch(0);
-    for (int ch = 0; ch < nch; ++ch) {
-      const int buf = ch & 1;
-      if (has_pre_in) {
-        if (ch + 1 < nch) prefetch(ch + 1);
-        else ptx::cp_async_commit();
-        ptx::cp_async_wait<1>();
+    }
+    ptx::cp_async_commit();  // uniform group count, even when empty
+  }
+  static __device__ __forceinline__ void prefetch(const Params& e, const GemmParams&, const TileInfo& ti, int q, int h,
+                                                  int lane, uint8_t* wsm, const int* s_start) {
+    if constexpr (V == 2) {
+      __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(wsm + 2 * kChunk);
+      const int row0 = s_start[ti.g] + ti.n0;
+      const int mcol = ti.m0 + q * 32;
+      for (int j = 0; j < kPf; ++j) load_chunk(e, ti, row0, mcol, h + 2 * j, ring + j * 1024, lane);
+    }
+  }
+  static __device__ __forceinline__ void run(const Params& e, const GemmParams&, const TileInfo& ti,
+                                             uint32_t tmem_tile, int q, int h, int lane, uint8_t* wsm,
+                                             const int* s_start) {
+    __nv_bfloat16* st_out = reinterpret_cast<__nv_bfloat16*>(wsm);
+    __nv_bfloat16* extra = reinterpret_cast<__nv_bfloat16*>(wsm + 2 * kChunk);  // pre_out staging | pre_in ring
+    const int mcol = ti.m0 + q * 32;
+    const int row0 = s_start[ti.g] + ti.n0;
+    const int nch = (ti.n + 31) / 32;
+    if (lane == 0) ptx::bulk_wait_read<0>();  // staging tiles free again
+    __syncwarp();
+    int j = 0;
+    for (int ch = h; ch < nch; ch += 2, ++j) {
+      if constexpr (V == 2) {
+        ptx::cp_async_wait<kPf - 1>();
         __syncwarp();
       }
       float v[32];
       load_acc32(tmem_tile, ch * 32, v);
-      if (ch >= 2) {
+      if (j >= 2) {
         if (lane == 0) ptx::bulk_wait_read<1>();
         __syncwarp();
       }
-      __nv_bfloat16* so = st_out + buf * 1024;
-      __nv_bfloat16* sp = st_pre + buf * 1024;
-      const __nv_bfloat16* pin = pf + buf * 1024;
+      __nv_bfloat16* so = st_out + (j & 1) * 1024;
+      __nv_bfloat16* sx = extra + (j & 1) * 1024;
 #pragma unroll
       for (int c = 0; c < 32; ++c) {
         float x = v[c];
-        if (has_pre_in) x *= act_grad(e.act_grad, __bfloat162float(pin[c * 32 + lane]));
-        if (e.has_pre_out) sp[c * 32 + lane] = __float2bfloat16(x);
+        if constexpr (V == 2) x *= act_grad(e.act_grad, __bfloat162float(sx[c * 32 + lane]));
+        if constexpr (V == 1) sx[c * 32 + lane] = __float2bfloat16(x);
         so[c * 32 + lane] = __float2bfloat16(act_fwd(e.act_out, x));
       }
       ptx::fence_proxy_async_smem();
       __syncwarp();
+      if constexpr (V == 2) load_chunk(e, ti, row0, mcol, ch + 2 * kPf, sx, lane);  // refill the consumed slot
       if (lane == 0) {
         const int rows = min(32, ti.n - ch * 32);
         const int y = row0 + ch * 32;
         ptx::tma_store_2d(rows == 32 ? &e.out32 : &e.out16, so, mcol, y);
-        if (e.has_pre_out) ptx::tma_store_2d(rows == 32 ? &e.pre32 : &e.pre16, sp, mcol, y);
+        if constexpr (V == 1) ptx::tma_store_2d(rows == 32 ? &e.pre32 : &e.pre16, sx, mcol, y);
         ptx::bulk_commit();
       }
     }
+    if constexpr (V == 2) ptx::cp_async_wait<0>();
+    __syncwarp();
   }
-  static __device__ __forceinline__ void finish(const Params&, int, int lane) {
+  static __device__ __forceinline__ void finish(const Params&, int lane) {
     if (lane == 0) ptx::bulk_wait<0>();
     __syncwarp();
   }
@@ -129,21 +142,23 @@ struct EpiSwap {
 
 // ---------------------------------------------------------------- wgrad epilogue
 // acc[lane = row m][col = n]  ->  out[g][m][n]  (zeros for empty groups).  Per warp and 32-column
-// chunk: bf16 staging tile [32 rows][32 cols] in the TMA 64-byte swizzle layout, one bulk store.
+// chunk (every other chunk): bf16 staging tile [32 rows][32 cols] in the TMA 64-byte swizzle layout,
+// one bulk store.
 struct EpiWgrad {
   static constexpr int kWarpBytes = 2 * 2048;
-  static constexpr int kSmemBytes = 4 * kWarpBytes;
   struct Params {
     CUtensorMap out;  // [G*Mw x Nw], box {32, 32}, 64B swizzle
   };
+  static __device__ __forceinline__ void prefetch(const Params&, const GemmParams&, const TileInfo&, int, int, int,
+                                                  uint8_t*, const int*) {}
   static __device__ __forceinline__ void run(const Params& e, const GemmParams& p, const TileInfo& ti,
-                                             uint32_t tmem_tile, int q, int lane, uint8_t* smem) {
-    uint8_t* ws = smem + q * kWarpBytes;
+                                             uint32_t tmem_tile, int q, int h, int lane, uint8_t* wsm, const int*) {
     if (lane == 0) ptx::bulk_wait_read<0>();
     __syncwarp();
     const int row = ti.g * p.Mw + ti.m0 + q * 32;
     const int sw = (lane >> 1) & 3;
-    for (int c0 = 0, ch = 0; c0 < ti.n; c0 += 32, ++ch) {
+    int j = 0;
+    for (int c0 = 32 * h; c0 < ti.n; c0 += 64, ++j) {
       float v[32];
       if (ti.k_len > 0) {
         load_acc32(tmem_tile, c0, v);
@@ -151,41 +166,48 @@ struct EpiWgrad {
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = 0.f;
       }
-      if (ch >= 2) {
+      if (j >= 2) {
         if (lane == 0) ptx::bulk_wait_read<1>();
         __syncwarp();
       }
-      uint8_t* st = ws + (ch & 1) * 2048 + lane * 64;
+      uint8_t* st = wsm + (j & 1) * 2048 + lane * 64;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int jj = 0; jj < 4; ++jj) {
         uint4 pk;
-        __nv_bfloat162 h0 = __floats2bfloat162_rn(v[8 * j + 0], v[8 * j + 1]);
-        __nv_bfloat162 h1 = __floats2bfloat162_rn(v[8 * j + 2], v[8 * j + 3]);
-        __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * j + 4], v[8 * j + 5]);
-        __nv_bfloat162 h3 = __floats2bfloat162_rn(v[8 * j + 6], v[8 * j + 7]);
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(v[8 * jj + 0], v[8 * jj + 1]);
+        __nv_bfloat162 h1 = __floats2bfloat162_rn(v[8 * jj + 2], v[8 * jj + 3]);
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * jj + 4], v[8 * jj + 5]);
+        __nv_bfloat162 h3 = __floats2bfloat162_rn(v[8 * jj + 6], v[8 * jj + 7]);
         pk.x = *reinterpret_cast<uint32_t*>(&h0);
         pk.y = *reinterpret_cast<uint32_t*>(&h1);
         pk.z = *reinterpret_cast<uint32_t*>(&h2);
         pk.w = *reinterpret_cast<uint32_t*>(&h3);
-        *reinterpret_cast<uint4*>(st + ((j ^ sw) * 16)) = pk;
+        *reinterpret_cast<uint4*>(st + ((jj ^ sw) * 16)) = pk;
       }
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        ptx::tma_store_2d(&e.out, ws + (ch & 1) * 2048, ti.n0 + c0, row);
+        ptx::tma_store_2d(&e.out, wsm + (j & 1) * 2048, ti.n0 + c0, row);
         ptx::bulk_commit();
       }
     }
   }
-  static __device__ __forceinline__ void finish(const Params&, int, int lane) {
+  static __device__ __forceinline__ void finish(const Params&, int lane) {
     if (lane == 0) ptx::bulk_wait<0>();
     __syncwarp();
   }
 };
 
-static EpiSwap::Params swap_params(__nv_bfloat16* out, __nv_bfloat16* pre_out, const __nv_bfloat16* pre_in, int M,
-                                   int R, int act_out, int act_grad) {
-  EpiSwap::Params e;
+template <int kMode, int BN, bool A_MN, bool B_MN, class Epi>
+static void launch_pair_or_single(bool pair, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
+                                  const typename Epi::Params& ep, cudaStream_t s) {
+  if (pair) launch_gemm<kMode, BN, A_MN, B_MN, Epi, 2>(ta, tb, p, ep, 0, s);
+  else launch_gemm<kMode, BN, A_MN, B_MN, Epi, 1>(ta, tb, p, ep, 0, s);
+}
+
+static SwapParams swap_params(__nv_bfloat16* out, __nv_bfloat16* pre_out, const __nv_bfloat16* pre_in, int M,
+                              int R, int act_out, int act_grad) {
+  SwapParams e;
   e.out32 = make_tmap_bf16_box(out, M, R, M, 32, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
   e.out16 = make_tmap_bf16_box(out, M, R, M, 32, 16, CU_TENSOR_MAP_SWIZZLE_NONE);
   if (pre_out) {
@@ -199,7 +221,6 @@ static EpiSwap::Params swap_params(__nv_bfloat16* out, __nv_bfloat16* pre_out, c
   e.ld = M;
   e.act_out = act_out;
   e.act_grad = act_grad;
-  e.has_pre_out = pre_out != nullptr;
   return e;
 }
 
@@ -211,11 +232,13 @@ void grouped_fwd(const __nv_bfloat16* tokens, const __nv_bfloat16* w, int G, int
   check_groups(G);
   require(M % kBM == 0, "grouped_fwd: M must be a multiple of 128");
   require(K % 64 == 0, "grouped_fwd: K must be a multiple of 64");
+  const bool pair = M % 256 == 0;
   CUtensorMap ta = make_tmap_bf16(w, K, static_cast<uint64_t>(G) * M, K, kBM);
-  CUtensorMap tb = make_tmap_bf16(tokens, K, R, K, 256);
+  CUtensorMap tb = make_tmap_bf16(tokens, K, R, K, pair ? 128 : 256);
   GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1};
-  EpiSwap::Params ep = swap_params(out, pre_out, nullptr, M, R, act, kActNone);
-  launch_gemm<kModeSwap, 256, false, false, EpiSwap>(ta, tb, p, ep, 0, s);
+  SwapParams ep = swap_params(out, pre_out, nullptr, M, R, act, kActNone);
+  if (pre_out) launch_pair_or_single<kModeSwap, 256, false, false, EpiSwap<1>>(pair, ta, tb, p, ep, s);
+  else launch_pair_or_single<kModeSwap, 256, false, false, EpiSwap<0>>(pair, ta, tb, p, ep, s);
 }
 
 void grouped_dgrad(const __nv_bfloat16* grad_tokens, const __nv_bfloat16* w, int G, int M, int K, int R,
@@ -225,11 +248,13 @@ void grouped_dgrad(const __nv_bfloat16* grad_tokens, const __nv_bfloat16* w, int
   check_groups(G);
   require(M % kBM == 0, "grouped_dgrad: M must be a multiple of 128");
   require(K % 64 == 0, "grouped_dgrad: K must be a multiple of 64");
+  const bool pair = M % 256 == 0;
   CUtensorMap ta = make_tmap_bf16(w, M, static_cast<uint64_t>(G) * K, M, 64);
-  CUtensorMap tb = make_tmap_bf16(grad_tokens, K, R, K, 256);
+  CUtensorMap tb = make_tmap_bf16(grad_tokens, K, R, K, pair ? 128 : 256);
   GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1};
-  EpiSwap::Params ep = swap_params(out, nullptr, pre_in, M, R, kActNone, pre_in ? act : kActNone);
-  launch_gemm<kModeSwap, 256, true, false, EpiSwap>(ta, tb, p, ep, 0, s);
+  SwapParams ep = swap_params(out, nullptr, pre_in, M, R, kActNone, pre_in ? act : kActNone);
+  if (pre_in) launch_pair_or_single<kModeSwap, 256, true, false, EpiSwap<2>>(pair, ta, tb, p, ep, s);
+  else launch_pair_or_single<kModeSwap, 256, true, false, EpiSwap<0>>(pair, ta, tb, p, ep, s);
 }
 
 void grouped_wgrad(const __nv_bfloat16* a_tokens, const __nv_bfloat16* b_tokens, int G, int M, int N, int R,
@@ -242,7 +267,7 @@ void grouped_wgrad(const __nv_bfloat16* a_tokens, const __nv_bfloat16* b_tokens,
   CUtensorMap tb = make_tmap_bf16(b_tokens, N, R, N, 64);
   GemmParams p{G, seg_start, seg_rows, M, N, 0, 1, 1, 1, 1};
   EpiWgrad::Params ep{make_tmap_bf16_box(out, N, static_cast<uint64_t>(G) * M, N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)};
-  launch_gemm<kModeWgrad, 256, true, true, EpiWgrad>(ta, tb, p, ep, 0, s);
+  launch_pair_or_single<kModeWgrad, 256, true, true, EpiWgrad>(M % 256 == 0, ta, tb, p, ep, s);
 }
 
 }  // namespace tamoe

@@ -17,14 +17,20 @@
 
 namespace tamoe {
 
+struct GateEpiParams {
+  RowRouteOut o;
+  int N, k, S, TB;
+};
+
+template <int KM>
 struct EpiGate {
-  struct Params {
-    RowRouteOut o;
-    int N, k, S, TB;
-  };
-  static __device__ __forceinline__ void finish(const Params&, int, int) {}
+  using Params = GateEpiParams;
+  static __device__ __forceinline__ void finish(const Params&, int) {}
+  static __device__ __forceinline__ void prefetch(const Params&, const GemmParams&, const TileInfo&, int, int, int,
+                                                  uint8_t*, const int*) {}
   static __device__ __forceinline__ void run(const Params& e, const GemmParams& p, const TileInfo& ti,
-                                             uint32_t tmem_tile, int q, int lane, uint8_t*) {
+                                             uint32_t tmem_tile, int q, int h, int lane, uint8_t*, const int*) {
+    if (h != 0) return;  // the softmax needs whole rows: one warp per lane quarter
     const int row = q * 32 + lane;
     const int tok = ti.m0 + row;
     const bool valid = tok < e.S;
@@ -58,22 +64,23 @@ struct EpiGate {
         if (c0 + c < N) denom += valid ? exp(static_cast<double>(v[c]) - dmx) : 0.0;
     }
     // pass 3: probabilities, top-k, probability sums
-    TopK tk;
+    TopK<KM> tk;
     tk.init();
     double* msum = e.o.msum4 + static_cast<long long>(tile_warp) * N;
     for (int c0 = 0; c0 < N; c0 += 32) {
       float v[32];
+      double pr[32];
       load_acc32(tmem_tile, c0, v);
 #pragma unroll
       for (int c = 0; c < 32; ++c) {
+        pr[c] = (valid && c0 + c < N) ? exp(static_cast<double>(v[c]) - dmx) / denom : 0.0;
         if (c0 + c < N) {
-          const double pr = valid ? exp(static_cast<double>(v[c]) - dmx) / denom : 0.0;
-          if (valid && e.o.probs) e.o.probs[gtok * N + c0 + c] = pr;
-          tk.insert(pr, c0 + c, e.k);
-          const double s = warp_sum_f64(pr);
-          if (lane == 0) msum[c0 + c] = s;
+          if (valid && e.o.probs) e.o.probs[gtok * N + c0 + c] = pr[c];
+          tk.insert(pr[c], c0 + c, e.k);
         }
       }
+      const double colsum = warp_transpose_sum32(pr, lane);
+      if (c0 + lane < N) msum[c0 + lane] = colsum;
     }
     finish_row(tk, valid, gtok, e.k, N, tile_warp, e.o, lane);
   }
@@ -89,7 +96,7 @@ __global__ void __launch_bounds__(kRouteTile) route_rows_kernel(const double* __
   const long long gtok = static_cast<long long>(proc) * d.S + tok;
   const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile_warp = tile * 4 + q;
-  TopK tk;
+  TopK<kMaxTopK> tk;
   tk.init();
   double* msum = o.msum4 + static_cast<long long>(tile_warp) * d.N;
   const double* row = probs + gtok * d.N;
@@ -109,9 +116,15 @@ void route_rows_from_probs(const double* probs, const RouteDims& d, const RowRou
 }
 
 template <int BN>
-static void gate_launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, const EpiGate::Params& ep,
-                        cudaStream_t s) {
-  launch_gemm<kModeGate, BN, false, false, EpiGate>(ta, tb, p, ep, 0, s);
+static void gate_launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
+                        const GateEpiParams& ep, cudaStream_t s) {
+  if (ep.k == 1) {
+    launch_gemm<kModeGate, BN, false, false, EpiGate<1>>(ta, tb, p, ep, 0, s);
+  } else if (ep.k == 2) {
+    launch_gemm<kModeGate, BN, false, false, EpiGate<2>>(ta, tb, p, ep, 0, s);
+  } else {
+    launch_gemm<kModeGate, BN, false, false, EpiGate<kMaxTopK>>(ta, tb, p, ep, 0, s);
+  }
 }
 
 void gate_forward(const __nv_bfloat16* x, const __nv_bfloat16* wg, int n_pad, const RouteDims& d, int dm,
@@ -124,7 +137,7 @@ void gate_forward(const __nv_bfloat16* x, const __nv_bfloat16* wg, int n_pad, co
   CUtensorMap ta = make_tmap_bf16(x, dm, T, dm, kBM);
   CUtensorMap tb = make_tmap_bf16(wg, dm, static_cast<uint64_t>(d.P) * n_pad, dm, BNsel);
   GemmParams p{1, nullptr, nullptr, 0, n_pad, dm, 1, d.S, n_pad, d.P};
-  EpiGate::Params ep{o, d.N, d.k, d.S, d.TB};
+  GateEpiParams ep{o, d.N, d.k, d.S, d.TB};
   switch (BNsel) {
     case 32: gate_launch<32>(ta, tb, p, ep, s); break;
     case 64: gate_launch<64>(ta, tb, p, ep, s); break;

@@ -142,11 +142,13 @@ struct EpiGateDw {
     float* part;
     int d, n64, P;
   };
-  static __device__ __forceinline__ void finish(const Params&, int, int) {}
+  static __device__ __forceinline__ void finish(const Params&, int) {}
+  static __device__ __forceinline__ void prefetch(const Params&, const GemmParams&, const TileInfo&, int, int, int,
+                                                  uint8_t*, const int*) {}
   static __device__ __forceinline__ void run(const Params& e, const GemmParams& p, const TileInfo& ti,
-                                             uint32_t tmem_tile, int q, int lane, uint8_t*) {
+                                             uint32_t tmem_tile, int q, int h, int lane, uint8_t*, const int*) {
     const int m = ti.m0 + q * 32 + lane;
-    for (int c0 = 0; c0 < ti.n; c0 += 32) {
+    for (int c0 = 32 * h; c0 < ti.n; c0 += 64) {
       float v[32];
       if (ti.k_len > 0) {
         load_acc32(tmem_tile, c0, v);
@@ -186,16 +188,18 @@ struct EpiGateDx {
     const int* pos;
     int k, S, d;
   };
-  static __device__ __forceinline__ void finish(const Params&, int, int) {}
+  static __device__ __forceinline__ void finish(const Params&, int) {}
+  static __device__ __forceinline__ void prefetch(const Params&, const GemmParams&, const TileInfo&, int, int, int,
+                                                  uint8_t*, const int*) {}
   static __device__ __forceinline__ void run(const Params& e, const GemmParams& p, const TileInfo& ti,
-                                             uint32_t tmem_tile, int q, int lane, uint8_t*) {
+                                             uint32_t tmem_tile, int q, int h, int lane, uint8_t*, const int*) {
     const int tok = ti.m0 + q * 32 + lane;
     const bool valid = tok < e.S;  // tcgen05.ld is warp-collective: every lane runs the loop
     const long long gtok = static_cast<long long>(ti.g) * e.S + tok;
     int rows[kMaxTopK];
 #pragma unroll
     for (int j = 0; j < kMaxTopK; ++j) rows[j] = (valid && j < e.k) ? e.pos[gtok * e.k + j] : -1;
-    for (int c0 = 0; c0 < ti.n; c0 += 32) {
+    for (int c0 = 32 * h; c0 < ti.n; c0 += 64) {
       float v[32];
       load_acc32(tmem_tile, c0, v);
       const int col = ti.n0 + c0;

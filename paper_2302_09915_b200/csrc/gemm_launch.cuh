@@ -5,11 +5,12 @@
 
 namespace tamoe {
 
-template <int kMode, int BN, bool A_MN, bool B_MN, class Epi>
+// kCG = 2 launches CTA pairs (cluster 2x1x1) running tcgen05.mma.cta_group::2 (M = 256 per pair).
+template <int kMode, int BN, bool A_MN, bool B_MN, class Epi, int kCG = 1>
 void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, const typename Epi::Params& ep,
                  int grid_limit, cudaStream_t s) {
-  auto kern = gemm_sm100_kernel<kMode, BN, A_MN, B_MN, Epi>;
-  const int smem = GemmSmem<BN, EpiSmem<Epi>::value>::kTotal;
+  auto kern = gemm_sm100_kernel<kMode, BN, A_MN, B_MN, Epi, kCG>;
+  const int smem = GemmSmem<BN, EpiSmem<Epi>::value, kCG>::kTotal;
   static bool configured = false;
   if (!configured) {
     TAMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -17,8 +18,20 @@ void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams&
   }
   int grid = num_sms();
   if (grid_limit > 0 && grid_limit < grid) grid = grid_limit;
-  kern<<<grid, kGemmThreads, smem, s>>>(ta, tb, p, ep);
-  TAMOE_CUDA(cudaGetLastError());
+  grid = (grid / kCG) * kCG;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TAMOE_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, p, ep));
 }
 
 }  // namespace tamoe

@@ -2,9 +2,9 @@
 // contraction on the TA-MoE hot path (fused gate logits, expert FFN forward /
 // dgrad / wgrad, gate dW and dX).
 //
-//   warps 0-3 : epilogue (warp q owns TMEM lanes 32q..32q+31)
-//   warp 4    : TMA producer (one elected lane)
-//   warp 5    : TMEM allocator + MMA issuer (one elected lane)
+//   warps 0-7 : epilogue (warp w owns TMEM lanes 32(w%4).. and column half w/4)
+//   warp 8    : TMA producer (one elected lane)
+//   warp 9    : TMEM allocator + MMA issuer (one elected lane)
 //
 // A tile is always M=128 (TMEM lanes) x N<=BN (TMEM columns) x K (multiple of
 // 16).  Operands are staged by TMA with 128-byte swizzle; each operand can be
@@ -21,7 +21,10 @@ namespace tamoe {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;
-constexpr int kGemmThreads = 192;
+constexpr int kEpiWarps = 8;
+constexpr int kProducerWarp = kEpiWarps;
+constexpr int kMmaWarp = kEpiWarps + 1;
+constexpr int kGemmThreads = (kEpiWarps + 2) * 32;
 constexpr int kMaxGroups = 1024;
 
 enum GemmMode : int {
@@ -53,42 +56,54 @@ struct TileInfo {
   int bx, by;  // B TMA base coordinates
 };
 
-// Epilogues may declare `static constexpr int kSmemBytes` of scratch shared memory (per CTA).
+// Epilogues may declare `static constexpr int kWarpBytes` of scratch shared memory per epilogue warp.
 template <class Epi, class = void>
 struct EpiSmem {
+  static constexpr int warp = 0;
   static constexpr int value = 0;
 };
 template <class Epi>
-struct EpiSmem<Epi, decltype(void(Epi::kSmemBytes))> {
-  static constexpr int value = Epi::kSmemBytes;
+struct EpiSmem<Epi, decltype(void(Epi::kWarpBytes))> {
+  static constexpr int warp = Epi::kWarpBytes;
+  static constexpr int value = Epi::kWarpBytes * kEpiWarps;
 };
 
-template <int BN, int kEpiBytes = 0>
+template <int BN, int kEpiBytes = 0, int kCG = 1>
 struct GemmSmem {
   static constexpr int kABytes = kBM * kBK * 2;
-  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kBBytes = (BN / kCG) * kBK * 2;  // a CTA pair splits B's N between its CTAs
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kBudget = 220 * 1024 - kEpiBytes - 8 * 1024;
-  static constexpr int kMaxStages = (BN >= 256) ? 4 : (BN >= 128 ? 6 : 8);
+  // barriers: full[S], empty[S], tfull[2], tempty[2]; tmem addr; tile prefix; group starts / rows
+  static constexpr int kMiscBytes = (2 * 8 + 4) * 8 + 16 + (3 * kMaxGroups + 1) * 4;
+  static constexpr int kBudget = 227 * 1024 - ((kEpiBytes + 1023) / 1024) * 1024 - kMiscBytes - 2048;
+  static constexpr int kMaxStages = 8;
   static constexpr int kStages = (kBudget / kStageBytes < kMaxStages) ? kBudget / kStageBytes : kMaxStages;
   static_assert(kStages >= 2, "not enough shared memory for the pipeline");
   static constexpr int kEpiOffset = kStages * kStageBytes;
   static constexpr int kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
   static constexpr int kBarOffset = kEpiOffset + ((kEpiBytes + 1023) / 1024) * 1024;
-  // barriers: full[S], empty[S], tfull[2], tempty[2]; tmem addr; tile prefix
-  static constexpr int kMiscBytes = (2 * kStages + 4) * 8 + 16 + (kMaxGroups + 1) * 4;
   static constexpr int kTotal = kBarOffset + kMiscBytes + 1024;  // + alignment slack
+  static_assert(kTotal <= 227 * 1024, "shared memory over the sm_100 per-CTA limit");
 };
 
 __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
-// Number of tiles of group g (device side; prefix built once per CTA).
-template <int kMode, int BN>
-__device__ __forceinline__ int group_tiles(const GemmParams& p, int g) {
+// Token tiles of a swap-mode group: rows split into ceil(rows / BN) balanced tiles (multiples of 16).
+template <int BN>
+__device__ __forceinline__ int swap_ntiles(int rows) { return ceil_div(rows, BN); }
+template <int BN>
+__device__ __forceinline__ int swap_nsize(int rows) {
+  const int nb = ceil_div(rows, BN);
+  return nb > 0 ? ((ceil_div(rows, nb) + 15) & ~15) : 0;
+}
+
+// Number of tiles of group g (device side; prefix built once per CTA).  `rows` = seg_rows[g].
+template <int kMode, int BN, int kCG = 1>
+__device__ __forceinline__ int group_tiles(const GemmParams& p, int rows) {
   if constexpr (kMode == kModeSwap) {
-    return (p.Mw / kBM) * ceil_div(p.seg_rows[g], BN);
+    return (p.Mw / (kBM * kCG)) * swap_ntiles<BN>(rows);
   } else if constexpr (kMode == kModeWgrad) {
-    return (p.Mw / kBM) * (p.Nw / BN);
+    return (p.Mw / (kBM * kCG)) * (p.Nw / BN);
   } else if constexpr (kMode == kModeGate) {
     return p.procs * ceil_div(p.tokens_per_proc, kBM);
   } else if constexpr (kMode == kModeGateDw) {
@@ -98,8 +113,9 @@ __device__ __forceinline__ int group_tiles(const GemmParams& p, int g) {
   }
 }
 
-template <int kMode, int BN>
-__device__ __forceinline__ void decode_tile(const GemmParams& p, const int* prefix, int t, TileInfo& ti) {
+template <int kMode, int BN, int kCG = 1>
+__device__ __forceinline__ void decode_tile(const GemmParams& p, const int* prefix, const int* s_start,
+                                            const int* s_rows, int t, TileInfo& ti) {
   // find group: prefix[g] <= t < prefix[g+1]
   int lo = 0, hi = p.num_groups - 1;
   while (lo < hi) {
@@ -111,24 +127,25 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, const int* pref
   ti.g = g;
   ti.ks = 0;
   if constexpr (kMode == kModeSwap) {
-    const int rows = p.seg_rows[g];
-    const int nb = ceil_div(rows, BN);
+    const int rows = s_rows[g];
+    const int nb = swap_ntiles<BN>(rows);
+    const int ns = swap_nsize<BN>(rows);
     const int mb = r / nb, nbk = r % nb;
-    ti.m0 = mb * kBM;
-    ti.n0 = nbk * BN;
-    ti.n = min(BN, rows - ti.n0);
+    ti.m0 = mb * kBM * kCG;
+    ti.n0 = nbk * ns;
+    ti.n = min(ns, rows - ti.n0);
     ti.k_len = p.Kw;
     // A (weights): K-major -> (k, g*Mw + m0) ; MN-major -> (m0, g*Kw + k)
     ti.ax = 0; ti.ay = g * p.Mw + ti.m0;  // overwritten below for MN-major A by caller convention
-    ti.bx = 0; ti.by = p.seg_start[g] + ti.n0;
+    ti.bx = 0; ti.by = s_start[g] + ti.n0;
   } else if constexpr (kMode == kModeWgrad) {
     const int nb = p.Nw / BN;
-    ti.m0 = (r / nb) * kBM;
+    ti.m0 = (r / nb) * kBM * kCG;
     ti.n0 = (r % nb) * BN;
     ti.n = BN;
-    ti.k_len = p.seg_rows[g];
-    ti.ax = ti.m0; ti.ay = p.seg_start[g];
-    ti.bx = ti.n0; ti.by = p.seg_start[g];
+    ti.k_len = s_rows[g];
+    ti.ax = ti.m0; ti.ay = s_start[g];
+    ti.bx = ti.n0; ti.by = s_start[g];
   } else if constexpr (kMode == kModeGate) {
     // tile r -> (process, 128-token block); rows beyond the process' S are masked by the epilogue
     const int tb = ceil_div(p.tokens_per_proc, kBM);
@@ -176,14 +193,16 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, const int* pref
 
 // Epilogue contract:
 //   struct Epi { struct Params; static __device__ void run(const Params&, const GemmParams&,
-//                const TileInfo&, uint32_t tmem_tile /*lane 0 col 0 of this tile*/, int q /*warp*/, int lane,
-//                uint8_t* smem /*kSmemBytes scratch*/);
-//                static __device__ void finish(const Params&, int q, int lane); };
-template <int kMode, int BN, bool A_MN, bool B_MN, class Epi>
+//                const TileInfo&, uint32_t tmem_tile /*lane 32q, col 0 of this tile*/, int q /*lane quarter*/,
+//                int h /*column half*/, int lane, uint8_t* smem /*this warp's kWarpBytes*/, const int* s_start);
+//                static __device__ void prefetch(...same without tmem_tile...);   // before the accumulator wait
+//                static __device__ void finish(const Params&, int lane); };
+template <int kMode, int BN, bool A_MN, bool B_MN, class Epi, int kCG>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const GemmParams p, const __grid_constant__ typename Epi::Params ep) {
-  using L = GemmSmem<BN, EpiSmem<Epi>::value>;
+  static_assert(kCG == 1 || kMode == kModeSwap || kMode == kModeWgrad, "CTA pairs only for grouped modes");
+  using L = GemmSmem<BN, EpiSmem<Epi>::value, kCG>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
@@ -192,21 +211,41 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   int* prefix = reinterpret_cast<int*>(tmem_slot + 4);
+  int* s_start = prefix + kMaxGroups + 1;
+  int* s_rows = s_start + kMaxGroups;
 
   const int warp = ptx::warp_id();
   const int lane = ptx::lane_id();
+  const uint32_t rank = kCG == 2 ? ptx::cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const int cluster_id = blockIdx.x / kCG;
+  const int num_clusters = gridDim.x / kCG;
 
-  // tile prefix over groups
+  // group table -> smem (parallel loads), then a warp-parallel prefix of the tile counts
   const int G = p.num_groups;
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int g = 0; g < G; ++g) {
-      prefix[g] = acc;
-      acc += group_tiles<kMode, BN>(p, g);
-    }
-    prefix[G] = acc;
+  const bool grouped = (kMode == kModeSwap || kMode == kModeWgrad);
+  for (int g = threadIdx.x; g < G; g += blockDim.x) {
+    s_start[g] = grouped ? p.seg_start[g] : 0;
+    s_rows[g] = grouped ? p.seg_rows[g] : 0;
   }
-  if (warp == 4 && lane == 0) {
+  __syncthreads();
+  if (warp == 0) {
+    int carry = 0;
+    for (int g0 = 0; g0 < G; g0 += 32) {
+      const int g = g0 + lane;
+      const int c = g < G ? group_tiles<kMode, BN, kCG>(p, s_rows[g]) : 0;
+      int x = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (g < G) prefix[g] = carry + x - c;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) prefix[G] = carry;
+  }
+  if (warp == kProducerWarp && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
     for (int s = 0; s < L::kStages; ++s) {
@@ -215,111 +254,162 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull_bar[b], 1);
-      ptx::mbar_init(&tempty_bar[b], 4);
+      ptx::mbar_init(&tempty_bar[b], kEpiWarps * kCG);
     }
     ptx::fence_barrier_init();
   }
-  if (warp == 5) ptx::tmem_alloc<L::kTmemCols>(tmem_slot);
+  if (warp == kMmaWarp) {
+    if constexpr (kCG == 2) ptx::tmem_alloc_cg2<L::kTmemCols>(tmem_slot);
+    else ptx::tmem_alloc<L::kTmemCols>(tmem_slot);
+  }
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (kCG == 2) ptx::cluster_sync();
+  else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int total_tiles = prefix[G];
 
-  if (warp == 4) {
-    // ------------------------------------------------------------ TMA producer
+  if (warp == kProducerWarp) {
+    // ------------------------------------------------------------ TMA producer (both CTAs of a pair)
     if (ptx::elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      for (int t = cluster_id; t < total_tiles; t += num_clusters) {
         TileInfo ti;
-        decode_tile<kMode, BN>(p, prefix, t, ti);
-        if constexpr (kMode == kModeSwap && A_MN) { ti.ax = ti.m0; ti.ay = ti.g * p.Kw; }
+        decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, t, ti);
+        const int my_m0 = ti.m0 + static_cast<int>(rank) * kBM;
+        if constexpr (kMode == kModeSwap) {
+          if constexpr (A_MN) { ti.ax = my_m0; ti.ay = ti.g * p.Kw; }
+          else { ti.ay = ti.g * p.Mw + my_m0; }
+          ti.by += static_cast<int>(rank) * (ti.n / kCG);  // this CTA's half of the token tile
+        } else if constexpr (kMode == kModeWgrad) {
+          ti.ax = my_m0;
+          ti.bx += static_cast<int>(rank) * (BN / kCG);
+        }
         const int nkb = ceil_div(ti.k_len, kBK);
         for (int kb = 0; kb < nkb; ++kb) {
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * L::kStageBytes;
           uint8_t* sb = sa + L::kABytes;
-          ptx::mbar_arrive_expect_tx(&full_bar[stage], L::kStageBytes);
-          if constexpr (A_MN) {
-            ptx::tma_load_2d(sa, &tmA, &full_bar[stage], ti.ax, ti.ay + kb * kBK);
-            ptx::tma_load_2d(sa + 8192, &tmA, &full_bar[stage], ti.ax + 64, ti.ay + kb * kBK);
-          } else {
-            ptx::tma_load_2d(sa, &tmA, &full_bar[stage], ti.ax + kb * kBK, ti.ay);
-          }
-          if constexpr (B_MN) {
+          if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], kCG * L::kStageBytes);
+          if constexpr (kCG == 2) {
+            const uint32_t bar = ptx::mapa(&full_bar[stage], 0);
+            if constexpr (A_MN) {
+              ptx::tma_load_2d_cg2(sa, &tmA, bar, ti.ax, ti.ay + kb * kBK);
+              ptx::tma_load_2d_cg2(sa + 8192, &tmA, bar, ti.ax + 64, ti.ay + kb * kBK);
+            } else {
+              ptx::tma_load_2d_cg2(sa, &tmA, bar, ti.ax + kb * kBK, ti.ay);
+            }
+            if constexpr (B_MN) {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              ptx::tma_load_2d(sb + j * 8192, &tmB, &full_bar[stage], ti.bx + 64 * j, ti.by + kb * kBK);
+              for (int j = 0; j < BN / 128; ++j)
+                ptx::tma_load_2d_cg2(sb + j * 8192, &tmB, bar, ti.bx + 64 * j, ti.by + kb * kBK);
+            } else {
+              ptx::tma_load_2d_cg2(sb, &tmB, bar, ti.bx + kb * kBK, ti.by);
+            }
           } else {
-            ptx::tma_load_2d(sb, &tmB, &full_bar[stage], ti.bx + kb * kBK, ti.by);
+            if constexpr (A_MN) {
+              ptx::tma_load_2d(sa, &tmA, &full_bar[stage], ti.ax, ti.ay + kb * kBK);
+              ptx::tma_load_2d(sa + 8192, &tmA, &full_bar[stage], ti.ax + 64, ti.ay + kb * kBK);
+            } else {
+              ptx::tma_load_2d(sa, &tmA, &full_bar[stage], ti.ax + kb * kBK, ti.ay);
+            }
+            if constexpr (B_MN) {
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j)
+                ptx::tma_load_2d(sb + j * 8192, &tmB, &full_bar[stage], ti.bx + 64 * j, ti.by + kb * kBK);
+            } else {
+              ptx::tma_load_2d(sb, &tmB, &full_bar[stage], ti.bx + kb * kBK, ti.by);
+            }
           }
           if (++stage == L::kStages) { stage = 0; phase ^= 1; }
         }
       }
     }
-  } else if (warp == 5) {
-    // ------------------------------------------------------------ MMA issuer
-    int stage = 0;
-    uint32_t phase = 0;
-    int it = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
-      TileInfo ti;
-      decode_tile<kMode, BN>(p, prefix, t, ti);
-      const int buf = it & 1;
-      const uint32_t use = static_cast<uint32_t>(it >> 1);
-      ptx::mbar_wait(&tempty_bar[buf], (use & 1) ^ 1);
-      ptx::tc_fence_after();
-      const uint32_t d_tmem = tmem_base + buf * BN;
-      const uint32_t idesc = ptx::idesc_bf16(kBM, ti.n, A_MN, B_MN);
-      const int nkb = ceil_div(ti.k_len, kBK);
-      for (int kb = 0; kb < nkb; ++kb) {
-        ptx::mbar_wait(&full_bar[stage], phase);
+  } else if (warp == kMmaWarp) {
+    // ------------------------------------------------------------ MMA issuer (pair leader only)
+    if (leader) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = cluster_id; t < total_tiles; t += num_clusters, ++it) {
+        TileInfo ti;
+        decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, t, ti);
+        const int buf = it & 1;
+        const uint32_t use = static_cast<uint32_t>(it >> 1);
+        ptx::mbar_wait(&tempty_bar[buf], (use & 1) ^ 1);
         ptx::tc_fence_after();
-        if (ptx::elect_one()) {
-          const uint32_t sa = ptx::smem_u32(smem + stage * L::kStageBytes);
-          const uint32_t sb = sa + L::kABytes;
-          const int nk = min(kBK, ti.k_len - kb * kBK) / 16;
-          for (int kk = 0; kk < nk; ++kk) {
-            const uint64_t adesc = A_MN ? ptx::smem_desc_sw128(sa + kk * 2048, 8192, 1024)
-                                        : ptx::smem_desc_sw128(sa + kk * 32, 16, 1024);
-            const uint64_t bdesc = B_MN ? ptx::smem_desc_sw128(sb + kk * 2048, 8192, 1024)
-                                        : ptx::smem_desc_sw128(sb + kk * 32, 16, 1024);
-            ptx::mma_bf16(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
+        const uint32_t d_tmem = tmem_base + buf * BN;
+        const uint32_t idesc = ptx::idesc_bf16(kBM * kCG, ti.n, A_MN, B_MN);
+        const int nkb = ceil_div(ti.k_len, kBK);
+        for (int kb = 0; kb < nkb; ++kb) {
+          ptx::mbar_wait(&full_bar[stage], phase);
+          ptx::tc_fence_after();
+          if (ptx::elect_one()) {
+            const uint32_t sa = ptx::smem_u32(smem + stage * L::kStageBytes);
+            const uint32_t sb = sa + L::kABytes;
+            const int nk = min(kBK, ti.k_len - kb * kBK) / 16;
+            for (int kk = 0; kk < nk; ++kk) {
+              const uint64_t adesc = A_MN ? ptx::smem_desc_sw128(sa + kk * 2048, 8192, 1024)
+                                          : ptx::smem_desc_sw128(sa + kk * 32, 16, 1024);
+              const uint64_t bdesc = B_MN ? ptx::smem_desc_sw128(sb + kk * 2048, 8192, 1024)
+                                          : ptx::smem_desc_sw128(sb + kk * 32, 16, 1024);
+              if constexpr (kCG == 2) ptx::mma_bf16_cg2(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
+              else ptx::mma_bf16(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
+            }
+            if constexpr (kCG == 2) ptx::mma_commit_cg2(&empty_bar[stage], 0x3);
+            else ptx::mma_commit(&empty_bar[stage]);
           }
-          ptx::mma_commit(&empty_bar[stage]);
+          __syncwarp();
+          if (++stage == L::kStages) { stage = 0; phase ^= 1; }
+        }
+        if (ptx::elect_one()) {
+          if (nkb > 0) {
+            if constexpr (kCG == 2) ptx::mma_commit_cg2(&tfull_bar[buf], 0x3);
+            else ptx::mma_commit(&tfull_bar[buf]);
+          } else {
+            if constexpr (kCG == 2) {
+              ptx::mbar_arrive_remote(ptx::mapa(&tfull_bar[buf], 0));
+              ptx::mbar_arrive_remote(ptx::mapa(&tfull_bar[buf], 1));
+            } else {
+              ptx::mbar_arrive(&tfull_bar[buf]);
+            }
+          }
         }
         __syncwarp();
-        if (++stage == L::kStages) { stage = 0; phase ^= 1; }
       }
-      if (ptx::elect_one()) {
-        if (nkb > 0) ptx::mma_commit(&tfull_bar[buf]);
-        else ptx::mbar_arrive(&tfull_bar[buf]);
-      }
-      __syncwarp();
     }
   } else {
-    // ------------------------------------------------------------ epilogue warps 0..3
+    // ------------------------------------------------------------ epilogue warps 0..7 (both CTAs)
+    const int q = warp & 3, h = warp >> 2;
+    uint8_t* wsm = smem + L::kEpiOffset + warp * EpiSmem<Epi>::warp;
     int it = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
+    for (int t = cluster_id; t < total_tiles; t += num_clusters, ++it) {
       TileInfo ti;
-      decode_tile<kMode, BN>(p, prefix, t, ti);
+      decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, t, ti);
+      ti.m0 += static_cast<int>(rank) * kBM;  // this CTA's 128 accumulator rows
       const int buf = it & 1;
       const uint32_t use = static_cast<uint32_t>(it >> 1);
+      Epi::prefetch(ep, p, ti, q, h, lane, wsm, s_start);
       ptx::mbar_wait(&tfull_bar[buf], use & 1);
       ptx::tc_fence_after();
-      const uint32_t tmem_tile = tmem_base + buf * BN + (static_cast<uint32_t>(warp * 32) << 16);
-      Epi::run(ep, p, ti, tmem_tile, warp, lane, smem + L::kEpiOffset);
+      const uint32_t tmem_tile = tmem_base + buf * BN + (static_cast<uint32_t>(q * 32) << 16);
+      Epi::run(ep, p, ti, tmem_tile, q, h, lane, wsm, s_start);
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tempty_bar[buf]);
+      if (lane == 0) {
+        if constexpr (kCG == 2) ptx::mbar_arrive_remote(ptx::mapa(&tempty_bar[buf], 0));
+        else ptx::mbar_arrive(&tempty_bar[buf]);
+      }
     }
-    Epi::finish(ep, warp, lane);
+    Epi::finish(ep, lane);
   }
-  __syncthreads();
-  if (warp == 5) {
+  if constexpr (kCG == 2) ptx::cluster_sync();
+  else __syncthreads();
+  if (warp == kMmaWarp) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<L::kTmemCols>(tmem_base);
+    if constexpr (kCG == 2) ptx::tmem_dealloc_cg2<L::kTmemCols>(tmem_base);
+    else ptx::tmem_dealloc<L::kTmemCols>(tmem_base);
   }
 }
 

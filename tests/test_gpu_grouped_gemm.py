@@ -26,7 +26,8 @@ def _rel(a, b):
     return (a.float() - b.float()).norm().item() / max(b.float().norm().item(), 1e-30)
 
 
-@pytest.mark.parametrize("counts,M,K", [([5, 0, 300, 17, 256], 256, 128), ([1000], 128, 64), ([33, 64, 1, 270], 384, 256)])
+@pytest.mark.parametrize("counts,M,K", [([5, 0, 300, 17, 256], 256, 128), ([1000], 128, 64), ([33, 64, 1, 270], 384, 256),
+                                        ([16, 48, 272, 511, 0, 700], 512, 192)])
 def test_grouped_fwd(dev, counts, M, K):
     from paper_2302_09915_b200 import _lib
     G = len(counts)
@@ -45,7 +46,8 @@ def test_grouped_fwd(dev, counts, M, K):
         assert _rel(out[s:s + r], torch.nn.functional.gelu(ref, approximate="tanh")) < 1e-2, g
 
 
-@pytest.mark.parametrize("counts,M,K", [([5, 0, 300, 17, 256], 256, 128), ([33, 64, 1, 270], 128, 192)])
+@pytest.mark.parametrize("counts,M,K", [([5, 0, 300, 17, 256], 256, 128), ([33, 64, 1, 270], 128, 192),
+                                        ([16, 48, 272, 511, 0, 700], 512, 256)])
 def test_grouped_dgrad(dev, counts, M, K):
     from paper_2302_09915_b200 import _lib
     G = len(counts)
@@ -63,7 +65,8 @@ def test_grouped_dgrad(dev, counts, M, K):
         assert _rel(out[s:s + r], ref) < 1e-2, g
 
 
-@pytest.mark.parametrize("counts,M,N", [([5, 0, 300, 17, 256], 128, 256), ([1000, 3], 256, 512)])
+@pytest.mark.parametrize("counts,M,N", [([5, 0, 300, 17, 256], 128, 256), ([1000, 3], 256, 512),
+                                        ([16, 0, 272, 48], 512, 256)])
 def test_grouped_wgrad(dev, counts, M, N):
     from paper_2302_09915_b200 import _lib
     G = len(counts)
