@@ -3,9 +3,12 @@
 #include "../../include/tamoe.h"
 
 #include <algorithm>
+#include <memory>
+#include <string>
 #include <cstring>
 
 #include "capi_util.hpp"
+#include "ep.hpp"
 #include "expert.hpp"
 #include "gate.hpp"
 #include "host_topology.hpp"
@@ -20,7 +23,8 @@ struct tamoe_router {
 };
 struct tamoe_layer {
   Layer impl;
-  tamoe_layer(const LayerConfig& c, const double* ch) : impl(c, ch) {}
+  tamoe_layer(const LayerConfig& c, const double* ch, std::unique_ptr<EpComm> ep = nullptr)
+      : impl(c, ch, std::move(ep)) {}
 };
 
 namespace {
@@ -204,6 +208,45 @@ int tamoe_layer_create(const tamoe_layer_config* cfg, const double* c_hat, tamoe
                   cfg->capacity_factor, cfg->aux_kind, cfg->aux_weight, cfg->penalty_norm, cfg->temperature,
                   cfg->need_dx, cfg->world_size, cfg->rank};
     *out = new tamoe_layer(c, c_hat);
+  });
+}
+
+int tamoe_nccl_unique_id(void* out128) {
+  return guarded([&] {
+    require(out128 != nullptr, "nccl_unique_id: null output");
+    static_assert(sizeof(ncclUniqueId) == 128, "unexpected ncclUniqueId size");
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) throw std::runtime_error(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+int tamoe_layer_create_ep(const tamoe_layer_config* cfg, const double* c_hat, const void* nccl_id128,
+                          tamoe_layer** out) {
+  return guarded([&] {
+    require(cfg && out && nccl_id128, "layer_create_ep: null argument");
+    LayerConfig c{cfg->P, cfg->S, cfg->d, cfg->d_out, cfg->N, cfg->k, cfg->f, cfg->act, cfg->cap_mode,
+                  cfg->capacity_factor, cfg->aux_kind, cfg->aux_weight, cfg->penalty_norm, cfg->temperature,
+                  cfg->need_dx, cfg->world_size, cfg->rank};
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id128, sizeof(id));
+    auto ep = std::make_unique<EpComm>(c.world_size, c.rank, id);
+    *out = new tamoe_layer(c, c_hat, std::move(ep));
+  });
+}
+
+int tamoe_layer_a2a_bytes(tamoe_layer* l, long long* out4) {
+  return guarded([&] {
+    require(l && out4, "a2a_bytes: null argument");
+    for (int i = 0; i < 4; ++i) out4[i] = l->impl.a2a_bytes()[i];
+  });
+}
+
+int tamoe_ep_plan(int P, int E, const long long* recv, int* seg_start, int* seg_rows, long long* recv_off) {
+  return guarded([&] {
+    require(P >= 1 && E >= 1 && recv && seg_start && seg_rows && recv_off, "ep_plan: bad arguments");
+    ep_plan(P, E, recv, seg_start, seg_rows, recv_off);
   });
 }
 

@@ -1,0 +1,117 @@
+#include "ep.hpp"
+
+#include <stdexcept>
+#include <string>
+
+#include "common.hpp"
+
+namespace tamoe {
+
+static void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw std::runtime_error(std::string(what) + ": " + ncclGetErrorString(r));
+}
+#define TAMOE_NCCL(expr) nccl_check((expr), #expr)
+
+void ep_plan(int P, int E, const long long* recv, int* seg_start, int* seg_rows, long long* recv_off) {
+  long long row = 0;
+  for (int e = 0; e < E; ++e) {
+    long long real = 0;
+    seg_start[e] = static_cast<int>(row);
+    for (int i = 0; i < P; ++i) {
+      recv_off[i * E + e] = row + real;
+      real += recv[i * E + e];
+    }
+    seg_rows[e] = static_cast<int>((real + 15) / 16 * 16);
+    row += seg_rows[e];
+  }
+}
+
+EpComm::EpComm(int world, int rank, const ncclUniqueId& id) : world_(world), rank_(rank) {
+  require(world >= 1 && rank >= 0 && rank < world, "bad expert-parallel world / rank");
+  TAMOE_NCCL(ncclCommInitRank(&comm_, world, id, rank));
+}
+
+EpComm::~EpComm() {
+  if (comm_) ncclCommDestroy(comm_);
+  if (h_counts_) cudaFreeHost(h_counts_);
+}
+
+void EpComm::exchange_counts(const int* my_counts, int* recv_counts, int N, cudaStream_t s) {
+  require(N % world_ == 0, "N must be divisible by the number of ranks");
+  E_ = N / world_;
+  if (!h_counts_) TAMOE_CUDA(cudaMallocHost(&h_counts_, sizeof(int) * (N + world_ * E_)));
+  TAMOE_NCCL(ncclGroupStart());
+  for (int j = 0; j < world_; ++j) {
+    TAMOE_NCCL(ncclSend(my_counts + j * E_, E_, ncclInt32, j, comm_, s));
+    TAMOE_NCCL(ncclRecv(recv_counts + j * E_, E_, ncclInt32, j, comm_, s));
+  }
+  TAMOE_NCCL(ncclGroupEnd());
+  TAMOE_CUDA(cudaMemcpyAsync(h_counts_, my_counts, sizeof(int) * N, cudaMemcpyDeviceToHost, s));
+  TAMOE_CUDA(cudaMemcpyAsync(h_counts_ + N, recv_counts, sizeof(int) * world_ * E_, cudaMemcpyDeviceToHost, s));
+  TAMOE_CUDA(cudaStreamSynchronize(s));
+  plan(N);
+}
+
+void EpComm::plan(int N) {
+  send_cnt_.assign(h_counts_, h_counts_ + N);
+  send_off_.assign(N, 0);
+  long long acc = 0;
+  for (int g = 0; g < N; ++g) {
+    send_off_[g] = acc;
+    acc += send_cnt_[g];
+  }
+  recv_cnt_.assign(h_counts_ + N, h_counts_ + N + world_ * E_);
+  recv_off_.assign(world_ * E_, 0);
+  seg_start_.assign(E_, 0);
+  seg_rows_.assign(E_, 0);
+  seg_real_.assign(E_, 0);
+  ep_plan(world_, E_, recv_cnt_.data(), seg_start_.data(), seg_rows_.data(), recv_off_.data());
+  recv_rows_ = 0;
+  for (int e = 0; e < E_; ++e) {
+    long long real = 0;
+    for (int i = 0; i < world_; ++i) real += recv_cnt_[i * E_ + e];
+    seg_real_[e] = static_cast<int>(real);
+    recv_rows_ += seg_rows_[e];
+  }
+}
+
+void EpComm::dispatch(const __nv_bfloat16* send, __nv_bfloat16* recv, int w, cudaStream_t s) {
+  last_bytes_ = 0;
+  TAMOE_NCCL(ncclGroupStart());
+  for (int j = 0; j < world_; ++j)
+    for (int e = 0; e < E_; ++e) {
+      const int g = j * E_ + e;
+      if (send_cnt_[g] > 0) {
+        TAMOE_NCCL(ncclSend(send + send_off_[g] * w, static_cast<size_t>(send_cnt_[g]) * w, ncclBfloat16, j, comm_, s));
+        if (j != rank_) last_bytes_ += send_cnt_[g] * w * 2;
+      }
+    }
+  for (int i = 0; i < world_; ++i)
+    for (int e = 0; e < E_; ++e) {
+      const long long c = recv_cnt_[i * E_ + e];
+      if (c > 0) TAMOE_NCCL(ncclRecv(recv + recv_off_[i * E_ + e] * w, static_cast<size_t>(c) * w, ncclBfloat16, i, comm_, s));
+    }
+  TAMOE_NCCL(ncclGroupEnd());
+}
+
+void EpComm::combine(const __nv_bfloat16* recv, __nv_bfloat16* send, int w, cudaStream_t s) {
+  last_bytes_ = 0;
+  TAMOE_NCCL(ncclGroupStart());
+  for (int i = 0; i < world_; ++i)
+    for (int e = 0; e < E_; ++e) {
+      const long long c = recv_cnt_[i * E_ + e];
+      if (c > 0) {
+        TAMOE_NCCL(ncclSend(recv + recv_off_[i * E_ + e] * w, static_cast<size_t>(c) * w, ncclBfloat16, i, comm_, s));
+        if (i != rank_) last_bytes_ += c * w * 2;
+      }
+    }
+  for (int j = 0; j < world_; ++j)
+    for (int e = 0; e < E_; ++e) {
+      const int g = j * E_ + e;
+      if (send_cnt_[g] > 0)
+        TAMOE_NCCL(ncclRecv(send + send_off_[g] * w, static_cast<size_t>(send_cnt_[g]) * w, ncclBfloat16, j, comm_, s));
+    }
+  TAMOE_NCCL(ncclGroupEnd());
+}
+
+}  // namespace tamoe

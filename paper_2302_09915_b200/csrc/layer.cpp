@@ -134,12 +134,16 @@ PhaseTimer::~PhaseTimer() {
 }
 
 // ------------------------------------------------------------------------------------ Layer
-Layer::Layer(const LayerConfig& c, const double* c_hat) : cfg_(c) {
-  require(c.world_size == 1, "expert parallelism across ranks is configured through tamoe_layer_create_ep");
+Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> ep) : cfg_(c), ep_(std::move(ep)) {
+  require(c.world_size >= 1 && c.rank >= 0 && c.rank < c.world_size, "bad world_size / rank");
+  require(c.world_size == 1 || ep_ != nullptr, "expert parallelism needs a communicator (tamoe_layer_create_ep)");
+  require(c.world_size == 1 || c.P == 1, "expert parallelism runs one logical process per rank (P = 1)");
+  require(c.N % c.world_size == 0, "N must be divisible by world_size");
+  require(c.world_size == 1 || c.cap_mode != 1,
+          "global capacity across ranks needs an owner-side selection exchange (not supported yet)");
   require(c.d % 256 == 0, "layer: d must be a multiple of 256");
   require(c.d_out % 128 == 0, "layer: d_out must be a multiple of 128");
   require(c.f == 0 || (c.f % 256 == 0), "layer: f must be 0 (linear expert) or a multiple of 256");
-  require(c.f != 0 || c.d % 256 == 0, "layer: linear experts need d % 256 == 0");
   require(c.P == 1 || c.S % 16 == 0, "layer: S must be a multiple of 16 when P > 1 processes share a device");
   require(c.cap_mode >= 0 && c.cap_mode <= 3, "unknown capacity mode");
   require(c.aux_kind == 0 || c.aux_kind == 1, "unknown aux loss kind");
@@ -147,8 +151,10 @@ Layer::Layer(const LayerConfig& c, const double* c_hat) : cfg_(c) {
   P_global_ = c.P * c.world_size;
   n_pad_ = (c.N + 15) & ~15;
   n64_ = expert_pad64(c.N);
+  const int E = c.N / c.world_size;
   const long long T = static_cast<long long>(c.P) * c.S;
-  r_max_ = static_cast<int>(T * c.k + 16LL * c.N);
+  // receive side: worst case every token of every rank picks this rank's experts
+  r_max_ = static_cast<int>(static_cast<long long>(c.world_size) * T * c.k + 16LL * E);
   rw_.reserve(arena_, c.P, c.S, c.N, c.k);
   arena_.reserve(xp_, static_cast<long long>(r_max_) * c.d);
   arena_.reserve(O_, static_cast<long long>(r_max_) * c.d_out);
@@ -159,6 +165,17 @@ Layer::Layer(const LayerConfig& c, const double* c_hat) : cfg_(c) {
     arena_.reserve(dA_, static_cast<long long>(r_max_) * c.f);
   }
   if (c.need_dx) arena_.reserve(dxp_, static_cast<long long>(r_max_) * c.d);
+  if (ep_) {
+    r_send_ = static_cast<int>(T * c.k);
+    arena_.reserve(x_send_, static_cast<long long>(r_send_) * c.d);
+    arena_.reserve(o_back_, static_cast<long long>(r_send_) * c.d_out);
+    arena_.reserve(do_send_, static_cast<long long>(r_send_) * c.d_out);
+    if (c.need_dx) arena_.reserve(dx_send_, static_cast<long long>(r_send_) * c.d);
+    arena_.reserve(recv_counts_, static_cast<long long>(c.world_size) * E);
+    arena_.reserve(seg_start_r_, E);
+    arena_.reserve(seg_rows_r_, E);
+    arena_.reserve(seg_real_r_, E);
+  }
   arena_.reserve(dz_, T * n64_);
   arena_.reserve(logits_, T * c.N);
   arena_.reserve(dldg_, T * c.k);
@@ -168,6 +185,7 @@ Layer::Layer(const LayerConfig& c, const double* c_hat) : cfg_(c) {
   n_loss_part_ = combine_blocks(T);
   arena_.reserve(loss_part_, n_loss_part_);
   arena_.commit();
+  if (ep_) TAMOE_CUDA(cudaMallocHost(&h_seg_, sizeof(int) * 3 * E));
 
   // host-side, once per topology: penalties p = Norm(1/c_hat) and capacities (gate.cpp:151-180, 222-246)
   std::vector<double> pen(static_cast<size_t>(c.P) * c.N, 1.0 / c.N);
@@ -186,37 +204,136 @@ Layer::Layer(const LayerConfig& c, const double* c_hat) : cfg_(c) {
   rw_.upload_caps(caps.data() + static_cast<size_t>(c.rank) * c.P * c.N, nullptr);
 }
 
+Layer::~Layer() {
+  if (h_seg_) cudaFreeHost(h_seg_);
+}
+
+void Layer::experts_forward(const LayerIO& io, int E, const int* seg_start, const int* seg_rows, int rows,
+                            cudaStream_t s) {
+  const LayerConfig& c = cfg_;
+  PhaseTimer& tm = timer_;
+  if (c.f == 0) {
+    grouped_fwd(xp_, io.w1, E, c.d_out, c.d, rows, seg_start, seg_rows, O_, nullptr, kActNone, s);
+    tm.mark("expert_fwd", s);
+  } else {
+    grouped_fwd(xp_, io.w1, E, c.f, c.d, rows, seg_start, seg_rows, H_, A_, c.act, s);
+    tm.mark("expert_fwd1", s);
+    grouped_fwd(H_, io.w2, E, c.d_out, c.f, rows, seg_start, seg_rows, O_, nullptr, kActNone, s);
+    tm.mark("expert_fwd2", s);
+  }
+}
+
+void Layer::experts_backward(const LayerIO& io, int E, const int* seg_start, const int* seg_rows, int rows,
+                             cudaStream_t s) {
+  const LayerConfig& c = cfg_;
+  PhaseTimer& tm = timer_;
+  if (c.f == 0) {
+    grouped_wgrad(dO_, xp_, E, c.d_out, c.d, rows, seg_start, seg_rows, io.dw1, s);
+    tm.mark("expert_wgrad", s);
+    if (c.need_dx) {
+      grouped_dgrad(dO_, io.w1, E, c.d, c.d_out, rows, seg_start, seg_rows, dxp_, nullptr, kActNone, s);
+      tm.mark("expert_dgrad", s);
+    }
+  } else {
+    grouped_dgrad(dO_, io.w2, E, c.f, c.d_out, rows, seg_start, seg_rows, dA_, A_, c.act, s);
+    tm.mark("expert_dgrad2", s);
+    grouped_wgrad(dO_, H_, E, c.d_out, c.f, rows, seg_start, seg_rows, io.dw2, s);
+    tm.mark("expert_wgrad2", s);
+    grouped_wgrad(dA_, xp_, E, c.f, c.d, rows, seg_start, seg_rows, io.dw1, s);
+    tm.mark("expert_wgrad1", s);
+    if (c.need_dx) {
+      grouped_dgrad(dA_, io.w1, E, c.d, c.f, rows, seg_start, seg_rows, dxp_, nullptr, kActNone, s);
+      tm.mark("expert_dgrad1", s);
+    }
+  }
+}
+
 void Layer::step(const LayerIO& io, cudaStream_t s) {
   const LayerConfig& c = cfg_;
   require(io.x && io.y && io.wg && io.w1 && io.dwg && io.dw1 && io.losses, "layer step: missing buffer");
   require(c.f == 0 || (io.w2 && io.dw2), "layer step: FFN experts need w2 / dw2");
   require(!c.need_dx || io.dx, "layer step: need_dx set but dx is null");
+  if (ep_) step_ep(io, s);
+  else step_local(io, s);
+}
+
+// Shared front: gate + histogram/scan + capacity.
+static void route_front(Layer& L, RouteWorkspace& rw, PhaseTimer& tm, const LayerIO& io, int n_pad, int d,
+                        int cap_mode, float* logits, cudaStream_t s) {
+  const RouteBuffers& b = rw.buf;
+  TAMOE_CUDA(cudaMemsetAsync(b.bad, 0, sizeof(int), s));
+  gate_forward(io.x, io.wg, n_pad, rw.dims, d, rw.row_out(logits, nullptr), s);
+  tm.mark("gate_fwd", s);
+  route_bucket(rw.dims, b, s);
+  tm.mark("route_bucket", s);
+  route_capacity(rw.dims, b, cap_mode, rw.caps, s);
+  tm.mark("route_capacity", s);
+  (void)L;
+}
+
+void Layer::step_local(const LayerIO& io, cudaStream_t s) {
+  const LayerConfig& c = cfg_;
   const RouteBuffers& b = rw_.buf;
-  const RouteDims& dm = rw_.dims;
-  const int E = c.N;  // experts on this device
-  // ---- forward: gate + routing
   PhaseTimer& tm = timer_;
   tm.begin(s);
-  TAMOE_CUDA(cudaMemsetAsync(b.bad, 0, sizeof(int), s));
-  gate_forward(io.x, io.wg, n_pad_, dm, c.d, rw_.row_out(logits_, nullptr), s);
-  tm.mark("gate_fwd", s);
-  route_bucket(dm, b, s);
-  tm.mark("route_bucket", s);
-  route_capacity(dm, b, c.cap_mode, rw_.caps, s);
-  tm.mark("route_capacity", s);
-  route_permute(dm, b, io.x, c.d, xp_, r_max_, dO_, c.d_out, s);
+  route_front(*this, rw_, tm, io, n_pad_, c.d, c.cap_mode, logits_, s);
+  route_permute(rw_.dims, b, io.x, c.d, xp_, r_max_, dO_, c.d_out, s);
   tm.mark("permute", s);
-  // ---- forward: experts
-  if (c.f == 0) {
-    grouped_fwd(xp_, io.w1, E, c.d_out, c.d, r_max_, b.seg_start, b.seg_rows, O_, nullptr, kActNone, s);
-    tm.mark("expert_fwd", s);
-  } else {
-    grouped_fwd(xp_, io.w1, E, c.f, c.d, r_max_, b.seg_start, b.seg_rows, H_, A_, c.act, s);
-    tm.mark("expert_fwd1", s);
-    grouped_fwd(H_, io.w2, E, c.d_out, c.f, r_max_, b.seg_start, b.seg_rows, O_, nullptr, kActNone, s);
-    tm.mark("expert_fwd2", s);
+  experts_forward(io, c.N, b.seg_start, b.seg_rows, r_max_, s);
+  combine(io, O_, dO_, s);
+  experts_backward(io, c.N, b.seg_start, b.seg_rows, r_max_, s);
+  gate_backward(io, dxp_, s);
+  tm.end(s);
+}
+
+void Layer::step_ep(const LayerIO& io, cudaStream_t s) {
+  const LayerConfig& c = cfg_;
+  const RouteBuffers& b = rw_.buf;
+  PhaseTimer& tm = timer_;
+  const int E = c.N / c.world_size;
+  tm.begin(s);
+  route_front(*this, rw_, tm, io, n_pad_, c.d, c.cap_mode, logits_, s);
+  // packed send layout: this rank's kept picks, expert-major (= destination-rank-major)
+  route_permute(rw_.dims, b, io.x, c.d, x_send_, r_send_, nullptr, 0, s, /*pad=*/1);
+  tm.mark("permute", s);
+  // counts all-to-all + receiver plan (host)
+  ep_->exchange_counts(b.counts, recv_counts_, c.N, s);
+  for (int e = 0; e < E; ++e) {
+    h_seg_[e] = ep_->seg_start()[e];
+    h_seg_[E + e] = ep_->seg_rows()[e];
+    h_seg_[2 * E + e] = ep_->seg_real()[e];
   }
-  // ---- combine + task loss + dO
+  TAMOE_CUDA(cudaMemcpyAsync(seg_start_r_, h_seg_, sizeof(int) * E, cudaMemcpyHostToDevice, s));
+  TAMOE_CUDA(cudaMemcpyAsync(seg_rows_r_, h_seg_ + E, sizeof(int) * E, cudaMemcpyHostToDevice, s));
+  TAMOE_CUDA(cudaMemcpyAsync(seg_real_r_, h_seg_ + 2 * E, sizeof(int) * E, cudaMemcpyHostToDevice, s));
+  tm.mark("a2a_counts", s);
+  // dispatch all-to-all straight into the padded expert-major layout
+  ep_->dispatch(x_send_, xp_, c.d, s);
+  last_a2a_bytes_[0] = ep_->last_offrank_bytes();
+  zero_pad_rows(seg_start_r_, seg_rows_r_, seg_real_r_, E, xp_, c.d, nullptr, 0, s);
+  tm.mark("a2a_dispatch", s);
+  experts_forward(io, E, seg_start_r_, seg_rows_r_, r_max_, s);
+  ep_->combine(O_, o_back_, c.d_out, s);
+  last_a2a_bytes_[1] = ep_->last_offrank_bytes();
+  tm.mark("a2a_combine", s);
+  combine(io, o_back_, do_send_, s);
+  ep_->dispatch(do_send_, dO_, c.d_out, s);
+  last_a2a_bytes_[2] = ep_->last_offrank_bytes();
+  zero_pad_rows(seg_start_r_, seg_rows_r_, seg_real_r_, E, dO_, c.d_out, nullptr, 0, s);
+  tm.mark("a2a_dispatch_grad", s);
+  experts_backward(io, E, seg_start_r_, seg_rows_r_, r_max_, s);
+  if (c.need_dx) {
+    ep_->combine(dxp_, dx_send_, c.d, s);
+    last_a2a_bytes_[3] = ep_->last_offrank_bytes();
+    tm.mark("a2a_combine_grad", s);
+  }
+  gate_backward(io, dx_send_, s);
+  tm.end(s);
+}
+
+void Layer::combine(const LayerIO& io, const __nv_bfloat16* O_rows, __nv_bfloat16* dO_rows, cudaStream_t s) {
+  const LayerConfig& c = cfg_;
+  const RouteBuffers& b = rw_.buf;
   CombineArgs ca{};
   ca.T = static_cast<long long>(c.P) * c.S;
   ca.k = c.k;
@@ -224,35 +341,20 @@ void Layer::step(const LayerIO& io, cudaStream_t s) {
   ca.mse_scale = static_cast<float>(2.0 / (static_cast<double>(P_global_) * c.S * c.d_out));
   ca.pos = b.pos;
   ca.gate = b.gate;
-  ca.O = O_;
+  ca.O = O_rows;
   ca.y = io.y;
   ca.y_hat = io.y_hat;
-  ca.dO = dO_;
+  ca.dO = dO_rows;
   ca.dldg = dldg_;
   ca.loss_part = loss_part_;
   combine_loss(ca, s);
-  tm.mark("combine_loss", s);
-  // ---- backward: experts
-  if (c.f == 0) {
-    grouped_wgrad(dO_, xp_, E, c.d_out, c.d, r_max_, b.seg_start, b.seg_rows, io.dw1, s);
-    tm.mark("expert_wgrad", s);
-    if (c.need_dx) {
-      grouped_dgrad(dO_, io.w1, E, c.d, c.d_out, r_max_, b.seg_start, b.seg_rows, dxp_, nullptr, kActNone, s);
-      tm.mark("expert_dgrad", s);
-    }
-  } else {
-    grouped_dgrad(dO_, io.w2, E, c.f, c.d_out, r_max_, b.seg_start, b.seg_rows, dA_, A_, c.act, s);
-    tm.mark("expert_dgrad2", s);
-    grouped_wgrad(dO_, H_, E, c.d_out, c.f, r_max_, b.seg_start, b.seg_rows, io.dw2, s);
-    tm.mark("expert_wgrad2", s);
-    grouped_wgrad(dA_, xp_, E, c.f, c.d, r_max_, b.seg_start, b.seg_rows, io.dw1, s);
-    tm.mark("expert_wgrad1", s);
-    if (c.need_dx) {
-      grouped_dgrad(dA_, io.w1, E, c.d, c.f, r_max_, b.seg_start, b.seg_rows, dxp_, nullptr, kActNone, s);
-      tm.mark("expert_dgrad1", s);
-    }
-  }
-  // ---- backward: gate
+  timer_.mark("combine_loss", s);
+}
+
+void Layer::gate_backward(const LayerIO& io, const __nv_bfloat16* dx_rows, cudaStream_t s) {
+  const LayerConfig& c = cfg_;
+  const RouteBuffers& b = rw_.buf;
+  PhaseTimer& tm = timer_;
   GateDzArgs ga{};
   ga.P = c.P;
   ga.S = c.S;
@@ -279,15 +381,14 @@ void Layer::step(const LayerIO& io, cudaStream_t s) {
   gate_dw(io.x, dz_, c.P, c.S, c.d, n64_, n_pad_, c.N, dw_part_, dw_splits_, io.dwg, s);
   tm.mark("gate_dw", s);
   if (c.need_dx) {
-    gate_dx(dz_, io.wg, c.P, c.S, c.d, n64_, n_pad_, dxp_, b.pos, c.k, io.dx, s);
+    gate_dx(dz_, io.wg, c.P, c.S, c.d, n64_, n_pad_, dx_rows, b.pos, c.k, io.dx, s);
     tm.mark("gate_dx", s);
   }
-  tm.end(s);
 }
 
 int Layer::launches_per_step() const {
-  // gate, scan, bucket, capacity, permute, combine, dz, dW GEMM + reduce
-  int n = 9;
+  // gate, scan, bucket, capacity, permute, combine, dz, dW GEMM + reduce (+ 2 pad-zeroing kernels with EP)
+  int n = 9 + (ep_ ? 2 : 0);
   n += cfg_.f == 0 ? (1 + 1 + (cfg_.need_dx ? 1 : 0)) : (2 + 3 + (cfg_.need_dx ? 1 : 0));
   if (cfg_.need_dx) n += 1;
   return n;

@@ -302,7 +302,8 @@ constexpr int kPermWarps = 8;
 __global__ void __launch_bounds__(kPermWarps * 32) route_permute_kernel(RouteDims d, RouteBuffers b,
                                                                         const __nv_bfloat16* __restrict__ x, int dx,
                                                                         __nv_bfloat16* __restrict__ xp, int r_max,
-                                                                        __nv_bfloat16* __restrict__ zrows, int zdim) {
+                                                                        __nv_bfloat16* __restrict__ zrows, int zdim,
+                                                                        int pad) {
   extern __shared__ int sm[];
   const int N = d.N;
   int* start = sm;          // [N]
@@ -312,14 +313,14 @@ __global__ void __launch_bounds__(kPermWarps * 32) route_permute_kernel(RouteDim
     int c = 0;
     for (int pr = 0; pr < d.P; ++pr) c += b.counts[pr * N + e];
     cnt[e] = c;
-    start[e] = (c + 15) & ~15;
+    start[e] = (c + pad - 1) / pad * pad;
   }
   __syncthreads();
   const int total = block_excl_scan(start, N, wtmp);
   if (blockIdx.x == 0) {
     for (int e = threadIdx.x; e < N; e += blockDim.x) {
       b.seg_start[e] = start[e];
-      b.seg_rows[e] = (cnt[e] + 15) & ~15;
+      b.seg_rows[e] = (cnt[e] + pad - 1) / pad * pad;
     }
     if (threadIdx.x == 0) *b.total_rows = total;
   }
@@ -353,7 +354,29 @@ __global__ void __launch_bounds__(kPermWarps * 32) route_permute_kernel(RouteDim
   }
 }
 
+// Zero the padding rows [start + real, start + rows) of each segment in up to two row buffers.
+__global__ void zero_pad_rows_kernel(const int* __restrict__ seg_start, const int* __restrict__ seg_rows,
+                                     const int* __restrict__ seg_real, int G, __nv_bfloat16* a, int wa,
+                                     __nv_bfloat16* b, int wb) {
+  const int g = blockIdx.x;
+  if (g >= G) return;
+  const int r0 = seg_start[g] + seg_real[g], r1 = seg_start[g] + seg_rows[g];
+  const uint4 z = make_uint4(0, 0, 0, 0);
+  for (int r = r0; r < r1; ++r) {
+    if (a)
+      for (int v = threadIdx.x; v < wa / 8; v += blockDim.x) reinterpret_cast<uint4*>(a + static_cast<long long>(r) * wa)[v] = z;
+    if (b)
+      for (int v = threadIdx.x; v < wb / 8; v += blockDim.x) reinterpret_cast<uint4*>(b + static_cast<long long>(r) * wb)[v] = z;
+  }
+}
+
 }  // namespace
+
+void zero_pad_rows(const int* seg_start, const int* seg_rows, const int* seg_real, int G, __nv_bfloat16* a, int wa,
+                   __nv_bfloat16* b, int wb, cudaStream_t s) {
+  zero_pad_rows_kernel<<<G, 128, 0, s>>>(seg_start, seg_rows, seg_real, G, a, wa, b, wb);
+  TAMOE_CUDA(cudaGetLastError());
+}
 
 void route_bucket(const RouteDims& d, const RouteBuffers& b, cudaStream_t s) {
   route_scan_kernel<<<d.N, kScanThreads, 0, s>>>(d, b);
@@ -370,11 +393,11 @@ void route_capacity(const RouteDims& d, const RouteBuffers& b, int mode, const i
 }
 
 void route_permute(const RouteDims& d, const RouteBuffers& b, const __nv_bfloat16* x, int dx, __nv_bfloat16* xp,
-                   int r_max, __nv_bfloat16* zero_rows, int zdim, cudaStream_t s) {
+                   int r_max, __nv_bfloat16* zero_rows, int zdim, cudaStream_t s, int pad) {
   require(dx % 8 == 0 && (zero_rows == nullptr || zdim % 8 == 0), "permute: row widths must be multiples of 8");
   const int blocks = (r_max + kPermWarps - 1) / kPermWarps;
   const size_t smem = sizeof(int) * (2 * d.N + 32);
-  route_permute_kernel<<<blocks, kPermWarps * 32, smem, s>>>(d, b, x, dx, xp, r_max, zero_rows, zdim);
+  route_permute_kernel<<<blocks, kPermWarps * 32, smem, s>>>(d, b, x, dx, xp, r_max, zero_rows, zdim, pad);
   TAMOE_CUDA(cudaGetLastError());
 }
 

@@ -73,7 +73,11 @@ void route_bucket(const RouteDims& d, const RouteBuffers& b, cudaStream_t s);
 void route_capacity(const RouteDims& d, const RouteBuffers& b, int mode, const int* caps, cudaStream_t s);
 // padded expert segments + gather of token rows into the expert-sorted buffer.
 // x: [P*S x dx] bf16; xp: [R_max x dx]; zero_rows (optional): second buffer whose pad rows are zeroed.
+// pad = 16: padded segments for the local expert GEMMs; pad = 1: packed send layout (expert parallelism).
 void route_permute(const RouteDims& d, const RouteBuffers& b, const __nv_bfloat16* x, int dx, __nv_bfloat16* xp,
-                   int r_max, __nv_bfloat16* zero_rows, int zdim, cudaStream_t s);
+                   int r_max, __nv_bfloat16* zero_rows, int zdim, cudaStream_t s, int pad = 16);
+// Zero rows [seg_start + seg_real, seg_start + seg_rows) of each of G segments in buffers a and b.
+void zero_pad_rows(const int* seg_start, const int* seg_rows, const int* seg_real, int G, __nv_bfloat16* a, int wa,
+                   __nv_bfloat16* b, int wb, cudaStream_t s);
 
 }  // namespace tamoe

@@ -41,13 +41,21 @@ _lib.lib.tamoe_layer_destroy.argtypes = [ctypes.c_void_p]
 _lib.lib.tamoe_layer_step.argtypes = [ctypes.c_void_p, ctypes.POINTER(_IO), ctypes.c_void_p]
 _lib.lib.tamoe_layer_read.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_longlong,
                                       ctypes.c_void_p]
+_lib.lib.tamoe_layer_create_ep.argtypes = [ctypes.POINTER(_Cfg), ctypes.POINTER(ctypes.c_double), ctypes.c_char_p,
+                                           ctypes.POINTER(ctypes.c_void_p)]
+_lib.lib.tamoe_nccl_unique_id.argtypes = [ctypes.c_void_p]
+_lib.lib.tamoe_layer_a2a_bytes.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_longlong)]
+_lib.lib.tamoe_ep_plan.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_longlong),
+                                   ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                   ctypes.POINTER(ctypes.c_longlong)]
 _lib.lib.tamoe_layer_launches_per_step.argtypes = [ctypes.c_void_p]
 _lib.lib.tamoe_layer_enable_timing.argtypes = [ctypes.c_void_p, ctypes.c_int]
 _lib.lib.tamoe_layer_timing.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_char_p),
                                         ctypes.POINTER(ctypes.c_double), ctypes.c_int, ctypes.POINTER(ctypes.c_int),
                                         ctypes.POINTER(ctypes.c_int)]
 for _n in ("tamoe_layer_create", "tamoe_layer_destroy", "tamoe_layer_step", "tamoe_layer_read",
-           "tamoe_layer_launches_per_step", "tamoe_layer_enable_timing", "tamoe_layer_timing"):
+           "tamoe_layer_launches_per_step", "tamoe_layer_enable_timing", "tamoe_layer_timing", "tamoe_layer_create_ep",
+           "tamoe_nccl_unique_id", "tamoe_layer_a2a_bytes", "tamoe_ep_plan"):
     getattr(_lib.lib, _n).restype = ctypes.c_int
 
 
@@ -84,8 +92,30 @@ def _ptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for tamoe_layer_create_ep (broadcast it to every rank)."""
+    buf = ctypes.create_string_buffer(128)
+    _lib.check(_lib.lib.tamoe_nccl_unique_id(buf))
+    return buf.raw
+
+
+def ep_plan(recv):
+    """Receiver plan for recv[P, E] rows per (source rank, local expert): (seg_start[E], seg_rows[E],
+    recv_off[P, E]) -- the C++ host logic the expert-parallel exchange uses."""
+    r = np.ascontiguousarray(recv, np.int64)
+    P, E = r.shape
+    st = np.zeros(E, np.int32)
+    rows = np.zeros(E, np.int32)
+    off = np.zeros((P, E), np.int64)
+    _lib.check(_lib.lib.tamoe_ep_plan(P, E, r.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong)),
+                                      st.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                                      rows.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                                      off.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong))))
+    return st, rows, off
+
+
 class TAMoELayer:
-    def __init__(self, cfg: LayerConfig, c_hat=None, device="cuda"):
+    def __init__(self, cfg: LayerConfig, c_hat=None, device="cuda", nccl_id: bytes = None):
         self.cfg = cfg
         self.device = torch.device(device)
         c = _Cfg(cfg.P, cfg.S, cfg.d, cfg.d_out, cfg.N, cfg.k, cfg.f, cfg.act, cfg.cap_mode, cfg.capacity_factor,
@@ -93,9 +123,13 @@ class TAMoELayer:
                  cfg.rank)
         self._c_hat = np.ascontiguousarray(c_hat, np.float64) if c_hat is not None else None
         h = ctypes.c_void_p()
-        _lib.check(_lib.lib.tamoe_layer_create(
-            ctypes.byref(c), self._c_hat.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if self._c_hat is not None
-            else None, ctypes.byref(h)))
+        chp = self._c_hat.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if self._c_hat is not None else None
+        if cfg.world_size > 1:
+            if nccl_id is None or len(nccl_id) != 128:
+                raise ValueError("expert parallelism needs the 128-byte NCCL id from nccl_unique_id()")
+            _lib.check(_lib.lib.tamoe_layer_create_ep(ctypes.byref(c), chp, nccl_id, ctypes.byref(h)))
+        else:
+            _lib.check(_lib.lib.tamoe_layer_create(ctypes.byref(c), chp, ctypes.byref(h)))
         self._h = h
         E = cfg.experts_local
         bf = dict(dtype=torch.bfloat16, device=self.device)
@@ -144,6 +178,12 @@ class TAMoELayer:
         _lib.check(_lib.lib.tamoe_layer_read(self._h, what, out.ctypes.data_as(ctypes.c_void_p), out.nbytes,
                                              ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
         return out
+
+    def a2a_bytes(self):
+        """Off-rank payload bytes of the last step's all-to-alls: dispatch, combine, grad dispatch, grad combine."""
+        out = (ctypes.c_longlong * 4)()
+        _lib.check(_lib.lib.tamoe_layer_a2a_bytes(self._h, out))
+        return list(out)
 
     def launches_per_step(self) -> int:
         return _lib.lib.tamoe_layer_launches_per_step(self._h)
