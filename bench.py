@@ -204,15 +204,22 @@ def main():
         return
 
     from paper_2302_09915_b200 import ops
-    from paper_2302_09915_b200.layer import LayerConfig, TAMoELayer, LOSS_TOPO, ACT_GELU
+    from paper_2302_09915_b200.layer import LayerConfig, TAMoELayer, LOSS_TOPO, ACT_GELU, nccl_unique_id
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     S = args.tokens
     cfg = LayerConfig(P=1, S=S, d=C2["d"], d_out=C2["d_out"], N=C2["N"], k=C2["k"], f=C2["f"], act=ACT_GELU,
-                      cap_mode=0, aux_kind=LOSS_TOPO, need_dx=True)
-    c_hat = ops.target_closed_form([[1.0]], C2["N"], C2["k"], S)  # homogeneous profile (one process per GPU)
-    layer = TAMoELayer(cfg, c_hat)
+                      cap_mode=0, aux_kind=LOSS_TOPO, need_dx=True, world_size=world, rank=rank)
+    # homogeneous NVSwitch profile: every off-diagonal beta equal, so c_hat is the even pattern
+    beta = [[1.0] * world for _ in range(world)]
+    c_hat = ops.target_closed_form(beta, C2["N"], C2["k"], S)
+    nccl_id = None
+    if world > 1:
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    layer = TAMoELayer(cfg, c_hat, nccl_id=nccl_id)
     params = layer.init_params(seed=1 + rank)
     g = torch.Generator(device=dev).manual_seed(100 + rank)
     x = torch.randn(S, cfg.d, generator=g, device=dev).bfloat16()
@@ -248,6 +255,18 @@ def main():
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     phases, tsteps = layer.timing()
     layer.enable_timing(False)
+    a2a = None
+    if world > 1:
+        nbytes = layer.a2a_bytes()  # off-rank bytes of the last step (dispatch, combine, grad dispatch, grad combine)
+        names = ["a2a_dispatch", "a2a_combine", "a2a_dispatch_grad", "a2a_combine_grad"]
+        a2a_ms = sum(phases.get(n, 0.0) for n in names)
+        tot = float(sum(nbytes))
+        bus = tot / (a2a_ms / 1e3) / 1e9 if a2a_ms > 0 else 0.0
+        a2a = {"offrank_bytes_per_step_rank0": nbytes, "ms_per_step": a2a_ms, "counts_exchange_ms":
+               phases.get("a2a_counts", 0.0), "bus_gbs": bus, "peak_gbs": 900.0, "frac_of_nvlink": bus / 900.0,
+               "measured_peer_peak_gbs": 770.0,
+               "note": "busBW = off-rank bytes sent per rank / time of the 4 payload all-to-alls (NCCL grouped "
+                       "send/recv, CUDA events on the step stream)"}
     losses = layer.losses.cpu().tolist()
     value = world * S / (ms / 1e3)
 
@@ -305,7 +324,8 @@ def main():
     T = S
     gemm_names = [n for n in phases if n.startswith("expert_")]
     gemm_ms = sum(phases[n] for n in gemm_names)
-    flops = len(gemm_names) * 2.0 * T * cfg.k * cfg.d * cfg.f  # every expert GEMM is 2*T*k*d*f
+    # every expert GEMM is 2*rows*d*f; with EP the rows a rank receives average T*k (all ranks route T*k picks)
+    flops = len(gemm_names) * 2.0 * T * cfg.k * cfg.d * cfg.f
     achieved = flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
     roof = {"kernel": "expert grouped GEMM (tcgen05, 6 launches/step: fwd1, fwd2, dgrad2, wgrad2, wgrad1, dgrad1)",
             "bound": "tensor", "achieved": achieved, "peak": pk["bf16_sus"], "unit": "TFLOP/s",
@@ -331,10 +351,11 @@ def main():
                 "config": {"workload": "C2: GPT-MoE layer d_model=1024 ffn=4096 64 experts top-1 "
                                        f"{S} tokens/GPU, GELU FFN experts, topo aux loss, capacity none, dX on",
                            "tokens_per_gpu": S, "global_tokens": world * S,
-                           "parallelism": "replicas (1 process per GPU, all 64 experts local)" if world > 1
+                           "parallelism": f"ep{world} (expert parallel, {C2['N'] // world} experts per GPU, "
+                                          "NCCL all-to-all over NVLink)" if world > 1
                            else "single GPU, 64 local experts",
                            "l2": "working set > L2 (1.07 GB expert weights + ~0.6 GB activations per step)"},
-                "roofline": roof, "phases_ms": phases, "timed_steps_for_phases": tsteps,
+                "roofline": roof, "all_to_all": a2a, "phases_ms": phases, "timed_steps_for_phases": tsteps,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": layer.launches_per_step() * args.steps,
                 "clocks": clk.summary(), "losses_last_step": losses}
         print(json.dumps(line), flush=True)

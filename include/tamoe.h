@@ -165,8 +165,11 @@ int tamoe_layer_create_ep(const tamoe_layer_config* cfg, const double* c_hat, co
 /* Off-rank payload bytes of the last step's all-to-alls: out[4] = dispatch, combine, grad dispatch, grad combine. */
 int tamoe_layer_a2a_bytes(tamoe_layer* l, long long* out4);
 /* Host-side receive plan (CPU-testable): recv[P x E] rows per (source rank, local expert) ->
- * padded segments seg_start/seg_rows [E] and the row offset of every (source, expert) block [P x E]. */
-int tamoe_ep_plan(int P, int E, const long long* recv, int* seg_start, int* seg_rows, long long* recv_off);
+ * 16-row padded (source, expert) segments seg_start/seg_rows [P x E] (source-major) and the receive block
+ * offset / rows of every source rank [P].  The sender's block for this rank is its own padded expert-major
+ * layout restricted to this rank's experts, so one NCCL send/recv pair per peer moves it. */
+int tamoe_ep_plan(int P, int E, const long long* recv, int* seg_start, int* seg_rows, long long* blk_off,
+                  long long* blk_rows);
 int tamoe_layer_destroy(tamoe_layer* l);
 int tamoe_layer_step(tamoe_layer* l, const tamoe_layer_io* io, void* stream);
 int tamoe_layer_read(tamoe_layer* l, int what, void* dst, long long bytes, void* stream);

@@ -12,17 +12,18 @@ static void nccl_check(ncclResult_t r, const char* what) {
 }
 #define TAMOE_NCCL(expr) nccl_check((expr), #expr)
 
-void ep_plan(int P, int E, const long long* recv, int* seg_start, int* seg_rows, long long* recv_off) {
+void ep_plan(int P, int E, const long long* recv, int* seg_start, int* seg_rows, long long* blk_off,
+             long long* blk_rows) {
   long long row = 0;
-  for (int e = 0; e < E; ++e) {
-    long long real = 0;
-    seg_start[e] = static_cast<int>(row);
-    for (int i = 0; i < P; ++i) {
-      recv_off[i * E + e] = row + real;
-      real += recv[i * E + e];
+  for (int i = 0; i < P; ++i) {
+    blk_off[i] = row;
+    for (int e = 0; e < E; ++e) {
+      const long long r = (recv[i * E + e] + 15) / 16 * 16;
+      seg_start[i * E + e] = static_cast<int>(row);
+      seg_rows[i * E + e] = static_cast<int>(r);
+      row += r;
     }
-    seg_rows[e] = static_cast<int>((real + 15) / 16 * 16);
-    row += seg_rows[e];
+    blk_rows[i] = row - blk_off[i];
   }
 }
 
@@ -54,43 +55,37 @@ void EpComm::exchange_counts(const int* my_counts, int* recv_counts, int N, cuda
 
 void EpComm::plan(int N) {
   send_cnt_.assign(h_counts_, h_counts_ + N);
-  send_off_.assign(N, 0);
-  long long acc = 0;
-  for (int g = 0; g < N; ++g) {
-    send_off_[g] = acc;
-    acc += send_cnt_[g];
+  send_blk_off_.assign(world_, 0);
+  send_blk_rows_.assign(world_, 0);
+  long long row = 0;
+  for (int j = 0; j < world_; ++j) {
+    send_blk_off_[j] = row;
+    for (int e = 0; e < E_; ++e) row += (send_cnt_[j * E_ + e] + 15) / 16 * 16;
+    send_blk_rows_[j] = row - send_blk_off_[j];
   }
   recv_cnt_.assign(h_counts_ + N, h_counts_ + N + world_ * E_);
-  recv_off_.assign(world_ * E_, 0);
-  seg_start_.assign(E_, 0);
-  seg_rows_.assign(E_, 0);
-  seg_real_.assign(E_, 0);
-  ep_plan(world_, E_, recv_cnt_.data(), seg_start_.data(), seg_rows_.data(), recv_off_.data());
-  recv_rows_ = 0;
-  for (int e = 0; e < E_; ++e) {
-    long long real = 0;
-    for (int i = 0; i < world_; ++i) real += recv_cnt_[i * E_ + e];
-    seg_real_[e] = static_cast<int>(real);
-    recv_rows_ += seg_rows_[e];
-  }
+  seg_start_.assign(world_ * E_, 0);
+  seg_rows_.assign(world_ * E_, 0);
+  recv_blk_off_.assign(world_, 0);
+  recv_blk_rows_.assign(world_, 0);
+  ep_plan(world_, E_, recv_cnt_.data(), seg_start_.data(), seg_rows_.data(), recv_blk_off_.data(),
+          recv_blk_rows_.data());
+  recv_rows_ = static_cast<int>(recv_blk_off_[world_ - 1] + recv_blk_rows_[world_ - 1]);
 }
 
 void EpComm::dispatch(const __nv_bfloat16* send, __nv_bfloat16* recv, int w, cudaStream_t s) {
   last_bytes_ = 0;
   TAMOE_NCCL(ncclGroupStart());
   for (int j = 0; j < world_; ++j)
-    for (int e = 0; e < E_; ++e) {
-      const int g = j * E_ + e;
-      if (send_cnt_[g] > 0) {
-        TAMOE_NCCL(ncclSend(send + send_off_[g] * w, static_cast<size_t>(send_cnt_[g]) * w, ncclBfloat16, j, comm_, s));
-        if (j != rank_) last_bytes_ += send_cnt_[g] * w * 2;
-      }
+    if (send_blk_rows_[j] > 0) {
+      TAMOE_NCCL(ncclSend(send + send_blk_off_[j] * w, static_cast<size_t>(send_blk_rows_[j]) * w, ncclBfloat16, j,
+                          comm_, s));
+      if (j != rank_) last_bytes_ += send_blk_rows_[j] * w * 2;
     }
   for (int i = 0; i < world_; ++i)
-    for (int e = 0; e < E_; ++e) {
-      const long long c = recv_cnt_[i * E_ + e];
-      if (c > 0) TAMOE_NCCL(ncclRecv(recv + recv_off_[i * E_ + e] * w, static_cast<size_t>(c) * w, ncclBfloat16, i, comm_, s));
-    }
+    if (recv_blk_rows_[i] > 0)
+      TAMOE_NCCL(ncclRecv(recv + recv_blk_off_[i] * w, static_cast<size_t>(recv_blk_rows_[i]) * w, ncclBfloat16, i,
+                          comm_, s));
   TAMOE_NCCL(ncclGroupEnd());
 }
 
@@ -98,19 +93,15 @@ void EpComm::combine(const __nv_bfloat16* recv, __nv_bfloat16* send, int w, cuda
   last_bytes_ = 0;
   TAMOE_NCCL(ncclGroupStart());
   for (int i = 0; i < world_; ++i)
-    for (int e = 0; e < E_; ++e) {
-      const long long c = recv_cnt_[i * E_ + e];
-      if (c > 0) {
-        TAMOE_NCCL(ncclSend(recv + recv_off_[i * E_ + e] * w, static_cast<size_t>(c) * w, ncclBfloat16, i, comm_, s));
-        if (i != rank_) last_bytes_ += c * w * 2;
-      }
+    if (recv_blk_rows_[i] > 0) {
+      TAMOE_NCCL(ncclSend(recv + recv_blk_off_[i] * w, static_cast<size_t>(recv_blk_rows_[i]) * w, ncclBfloat16, i,
+                          comm_, s));
+      if (i != rank_) last_bytes_ += recv_blk_rows_[i] * w * 2;
     }
   for (int j = 0; j < world_; ++j)
-    for (int e = 0; e < E_; ++e) {
-      const int g = j * E_ + e;
-      if (send_cnt_[g] > 0)
-        TAMOE_NCCL(ncclRecv(send + send_off_[g] * w, static_cast<size_t>(send_cnt_[g]) * w, ncclBfloat16, j, comm_, s));
-    }
+    if (send_blk_rows_[j] > 0)
+      TAMOE_NCCL(ncclRecv(send + send_blk_off_[j] * w, static_cast<size_t>(send_blk_rows_[j]) * w, ncclBfloat16, j,
+                          comm_, s));
   TAMOE_NCCL(ncclGroupEnd());
 }
 

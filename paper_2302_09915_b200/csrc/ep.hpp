@@ -22,18 +22,19 @@ class EpComm {
   // Then both are copied to the host (pinned) and the stream is synchronised; build the plan.
   void exchange_counts(const int* my_counts, int* recv_counts, int N, cudaStream_t s);
 
-  // Receiver layout: local expert e gets, in ascending source-rank order, recv[src][e] rows padded to 16
-  // (the reference bucket order: process, then token).  Host arrays, valid after exchange_counts.
-  const std::vector<int>& seg_start() const { return seg_start_; }
-  const std::vector<int>& seg_rows() const { return seg_rows_; }
-  const std::vector<int>& seg_real() const { return seg_real_; }
+  // Layouts.  Send side = the local padded expert-major layout (route_permute, 16-row segments), so
+  // the rows for destination j are one contiguous block.  Receive side = one block per source rank,
+  // each holding the source's 16-padded segments of this rank's E experts: segment (src, e) at index
+  // src*E + e.  The grouped GEMMs consume these (source, expert) segments directly (w_mod / nsub).
+  const std::vector<int>& seg_start() const { return seg_start_; }  // [P*E]
+  const std::vector<int>& seg_rows() const { return seg_rows_; }    // [P*E]
   const std::vector<long long>& send_counts() const { return send_cnt_; }
   const std::vector<long long>& recv_counts() const { return recv_cnt_; }
   int recv_rows() const { return recv_rows_; }
 
-  // send layout (packed, expert-major rows of width w) -> receiver layout (padded segments)
+  // send layout (padded, expert-major rows of width w) -> receive layout (one NCCL op per peer)
   void dispatch(const __nv_bfloat16* send, __nv_bfloat16* recv, int w, cudaStream_t s);
-  // receiver layout -> send layout (reverse of dispatch)
+  // receive layout -> send layout (reverse of dispatch)
   void combine(const __nv_bfloat16* recv, __nv_bfloat16* send, int w, cudaStream_t s);
 
   // bytes sent to other ranks by the last dispatch / combine (all-to-all bus accounting)
@@ -44,14 +45,16 @@ class EpComm {
   int world_, rank_, E_ = 0;
   ncclComm_t comm_ = nullptr;
   int* h_counts_ = nullptr;  // pinned: [N] mine, then [P x E] received
-  std::vector<long long> send_cnt_, send_off_, recv_cnt_, recv_off_;
-  std::vector<int> seg_start_, seg_rows_, seg_real_;
+  std::vector<long long> send_cnt_, recv_cnt_;
+  std::vector<long long> send_blk_off_, send_blk_rows_, recv_blk_off_, recv_blk_rows_;
+  std::vector<int> seg_start_, seg_rows_;
   int recv_rows_ = 0;
   long long last_bytes_ = 0;
 };
 
-// Host-side plan (also used by the CPU tests): given recv[src][e] (P x E), the padded receiver
-// segments and the row offset of every (src, e) block.
-void ep_plan(int P, int E, const long long* recv, int* seg_start, int* seg_rows, long long* recv_off);
+// Host-side receive plan (also used by the CPU tests): recv[src][e] (P x E) rows -> (source, expert)
+// segments seg_start/seg_rows [P*E] (16-row padded, source-major) and block offsets/rows per source [P].
+void ep_plan(int P, int E, const long long* recv, int* seg_start, int* seg_rows, long long* blk_off,
+             long long* blk_rows);
 
 }  // namespace tamoe

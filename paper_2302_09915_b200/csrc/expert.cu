@@ -226,16 +226,18 @@ static SwapParams swap_params(__nv_bfloat16* out, __nv_bfloat16* pre_out, const 
 
 static void check_groups(int G) { require(G >= 1 && G <= kMaxGroups, "group count out of range [1, 1024]"); }
 
+
 void grouped_fwd(const __nv_bfloat16* tokens, const __nv_bfloat16* w, int G, int M, int K, int R,
                  const int* seg_start, const int* seg_rows, __nv_bfloat16* out, __nv_bfloat16* pre_out, int act,
-                 cudaStream_t s) {
+                 cudaStream_t s, int w_mod) {
   check_groups(G);
   require(M % kBM == 0, "grouped_fwd: M must be a multiple of 128");
   require(K % 64 == 0, "grouped_fwd: K must be a multiple of 64");
   const bool pair = M % 256 == 0;
-  CUtensorMap ta = make_tmap_bf16(w, K, static_cast<uint64_t>(G) * M, K, kBM);
+  const int Gw = w_mod > 0 ? w_mod : G;  // distinct weight matrices
+  CUtensorMap ta = make_tmap_bf16(w, K, static_cast<uint64_t>(Gw) * M, K, kBM);
   CUtensorMap tb = make_tmap_bf16(tokens, K, R, K, pair ? 128 : 256);
-  GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1};
+  GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1, w_mod, 1};
   SwapParams ep = swap_params(out, pre_out, nullptr, M, R, act, kActNone);
   if (pre_out) launch_pair_or_single<kModeSwap, 256, false, false, EpiSwap<1>>(pair, ta, tb, p, ep, s);
   else launch_pair_or_single<kModeSwap, 256, false, false, EpiSwap<0>>(pair, ta, tb, p, ep, s);
@@ -243,29 +245,31 @@ void grouped_fwd(const __nv_bfloat16* tokens, const __nv_bfloat16* w, int G, int
 
 void grouped_dgrad(const __nv_bfloat16* grad_tokens, const __nv_bfloat16* w, int G, int M, int K, int R,
                    const int* seg_start, const int* seg_rows, __nv_bfloat16* out, const __nv_bfloat16* pre_in,
-                   int act, cudaStream_t s) {
+                   int act, cudaStream_t s, int w_mod) {
   // out[R x M] = grad_tokens[R x K] . W_g[K x M]  (W_g stored K x M: MN-major A operand)
   check_groups(G);
   require(M % kBM == 0, "grouped_dgrad: M must be a multiple of 128");
   require(K % 64 == 0, "grouped_dgrad: K must be a multiple of 64");
   const bool pair = M % 256 == 0;
-  CUtensorMap ta = make_tmap_bf16(w, M, static_cast<uint64_t>(G) * K, M, 64);
+  const int Gw = w_mod > 0 ? w_mod : G;
+  CUtensorMap ta = make_tmap_bf16(w, M, static_cast<uint64_t>(Gw) * K, M, 64);
   CUtensorMap tb = make_tmap_bf16(grad_tokens, K, R, K, pair ? 128 : 256);
-  GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1};
+  GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1, w_mod, 1};
   SwapParams ep = swap_params(out, nullptr, pre_in, M, R, kActNone, pre_in ? act : kActNone);
   if (pre_in) launch_pair_or_single<kModeSwap, 256, true, false, EpiSwap<2>>(pair, ta, tb, p, ep, s);
   else launch_pair_or_single<kModeSwap, 256, true, false, EpiSwap<0>>(pair, ta, tb, p, ep, s);
 }
 
 void grouped_wgrad(const __nv_bfloat16* a_tokens, const __nv_bfloat16* b_tokens, int G, int M, int N, int R,
-                   const int* seg_start, const int* seg_rows, __nv_bfloat16* out, cudaStream_t s) {
+                   const int* seg_start, const int* seg_rows, __nv_bfloat16* out, cudaStream_t s, int nsub) {
   // out[g][M x N] = a_tokens[seg_g]^T . b_tokens[seg_g]
   check_groups(G);
   require(M % kBM == 0, "grouped_wgrad: M must be a multiple of 128");
   require(N % 256 == 0, "grouped_wgrad: N must be a multiple of 256");
   CUtensorMap ta = make_tmap_bf16(a_tokens, M, R, M, 64);
   CUtensorMap tb = make_tmap_bf16(b_tokens, N, R, N, 64);
-  GemmParams p{G, seg_start, seg_rows, M, N, 0, 1, 1, 1, 1};
+  require(nsub >= 1 && G * nsub <= kMaxGroups, "grouped_wgrad: too many sub-segments");
+  GemmParams p{G, seg_start, seg_rows, M, N, 0, 1, 1, 1, 1, 0, nsub};
   EpiWgrad::Params ep{make_tmap_bf16_box(out, N, static_cast<uint64_t>(G) * M, N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)};
   launch_pair_or_single<kModeWgrad, 256, true, true, EpiWgrad>(M % 256 == 0, ta, tb, p, ep, s);
 }

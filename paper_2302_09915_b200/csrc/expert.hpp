@@ -10,15 +10,17 @@ enum ActKind : int { kActNone = 0, kActGelu = 1, kActRelu = 2 };
 // pre-activation for the backward pass.
 void grouped_fwd(const __nv_bfloat16* tokens, const __nv_bfloat16* w, int G, int M, int K, int R,
                  const int* seg_start, const int* seg_rows, __nv_bfloat16* out, __nv_bfloat16* pre_out, int act,
-                 cudaStream_t s);
+                 cudaStream_t s, int w_mod = 0);
 
 // out[R x M] = (grad_tokens[seg_g] . W_g) * act'(pre_in), W_g = w[g] stored K x M.
 void grouped_dgrad(const __nv_bfloat16* grad_tokens, const __nv_bfloat16* w, int G, int M, int K, int R,
                    const int* seg_start, const int* seg_rows, __nv_bfloat16* out, const __nv_bfloat16* pre_in,
-                   int act, cudaStream_t s);
+                   int act, cudaStream_t s, int w_mod = 0);
 
-// out[g] (M x N) = a_tokens[seg_g]^T . b_tokens[seg_g]; zeros for empty groups.
+// out[g] (M x N) = sum over sub-segments s < nsub of a_tokens[seg_{s*G+g}]^T . b_tokens[seg_{s*G+g}];
+// zeros for empty groups.  (w_mod / nsub let expert-parallel receive layouts -- (source, expert)
+// segments -- feed the GEMMs without a staging copy.)
 void grouped_wgrad(const __nv_bfloat16* a_tokens, const __nv_bfloat16* b_tokens, int G, int M, int N, int R,
-                   const int* seg_start, const int* seg_rows, __nv_bfloat16* out, cudaStream_t s);
+                   const int* seg_start, const int* seg_rows, __nv_bfloat16* out, cudaStream_t s, int nsub = 1);
 
 }  // namespace tamoe

@@ -44,10 +44,13 @@ struct GemmParams {
   int tokens_per_proc;   // rows per logical process (gate modes)
   int w_rows_per_proc;   // weight rows per process (gate modes)
   int procs;             // logical processes (gate modes)
+  int w_mod;             // kModeSwap: weight of group g is g % w_mod (0: g) -- (source, expert) segments
+  int nsub;              // kModeWgrad: K of group g = sub-segments s*num_groups + g, s < nsub
 };
 
 struct TileInfo {
   int g;       // group
+  int wg;      // weight index (kModeSwap)
   int m0, n0;  // offsets within the group's output
   int n;       // valid N columns (multiple of 16, <= BN)
   int k_len;   // K extent (multiple of 16)
@@ -131,6 +134,7 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, const int* pref
     const int nb = swap_ntiles<BN>(rows);
     const int ns = swap_nsize<BN>(rows);
     const int mb = r / nb, nbk = r % nb;
+    ti.wg = p.w_mod > 0 ? g % p.w_mod : g;
     ti.m0 = mb * kBM * kCG;
     ti.n0 = nbk * ns;
     ti.n = min(ns, rows - ti.n0);
@@ -143,7 +147,8 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, const int* pref
     ti.m0 = (r / nb) * kBM * kCG;
     ti.n0 = (r % nb) * BN;
     ti.n = BN;
-    ti.k_len = s_rows[g];
+    ti.k_len = 0;
+    for (int sub = 0; sub < p.nsub; ++sub) ti.k_len += s_rows[sub * p.num_groups + g];
     ti.ax = ti.m0; ti.ay = s_start[g];
     ti.bx = ti.n0; ti.by = s_start[g];
   } else if constexpr (kMode == kModeGate) {
@@ -224,7 +229,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   // group table -> smem (parallel loads), then a warp-parallel prefix of the tile counts
   const int G = p.num_groups;
   const bool grouped = (kMode == kModeSwap || kMode == kModeWgrad);
-  for (int g = threadIdx.x; g < G; g += blockDim.x) {
+  const int nseg = (kMode == kModeWgrad) ? G * p.nsub : G;
+  for (int g = threadIdx.x; g < nseg; g += blockDim.x) {
     s_start[g] = grouped ? p.seg_start[g] : 0;
     s_rows[g] = grouped ? p.seg_rows[g] : 0;
   }
@@ -279,50 +285,61 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, t, ti);
         const int my_m0 = ti.m0 + static_cast<int>(rank) * kBM;
         if constexpr (kMode == kModeSwap) {
-          if constexpr (A_MN) { ti.ax = my_m0; ti.ay = ti.g * p.Kw; }
-          else { ti.ay = ti.g * p.Mw + my_m0; }
+          if constexpr (A_MN) { ti.ax = my_m0; ti.ay = ti.wg * p.Kw; }
+          else { ti.ay = ti.wg * p.Mw + my_m0; }
           ti.by += static_cast<int>(rank) * (ti.n / kCG);  // this CTA's half of the token tile
         } else if constexpr (kMode == kModeWgrad) {
           ti.ax = my_m0;
           ti.bx += static_cast<int>(rank) * (BN / kCG);
         }
-        const int nkb = ceil_div(ti.k_len, kBK);
-        for (int kb = 0; kb < nkb; ++kb) {
-          ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * L::kStageBytes;
-          uint8_t* sb = sa + L::kABytes;
-          if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], kCG * L::kStageBytes);
-          if constexpr (kCG == 2) {
-            const uint32_t bar = ptx::mapa(&full_bar[stage], 0);
-            if constexpr (A_MN) {
-              ptx::tma_load_2d_cg2(sa, &tmA, bar, ti.ax, ti.ay + kb * kBK);
-              ptx::tma_load_2d_cg2(sa + 8192, &tmA, bar, ti.ax + 64, ti.ay + kb * kBK);
-            } else {
-              ptx::tma_load_2d_cg2(sa, &tmA, bar, ti.ax + kb * kBK, ti.ay);
-            }
-            if constexpr (B_MN) {
-#pragma unroll
-              for (int j = 0; j < BN / 128; ++j)
-                ptx::tma_load_2d_cg2(sb + j * 8192, &tmB, bar, ti.bx + 64 * j, ti.by + kb * kBK);
-            } else {
-              ptx::tma_load_2d_cg2(sb, &tmB, bar, ti.bx + kb * kBK, ti.by);
-            }
-          } else {
-            if constexpr (A_MN) {
-              ptx::tma_load_2d(sa, &tmA, &full_bar[stage], ti.ax, ti.ay + kb * kBK);
-              ptx::tma_load_2d(sa + 8192, &tmA, &full_bar[stage], ti.ax + 64, ti.ay + kb * kBK);
-            } else {
-              ptx::tma_load_2d(sa, &tmA, &full_bar[stage], ti.ax + kb * kBK, ti.ay);
-            }
-            if constexpr (B_MN) {
-#pragma unroll
-              for (int j = 0; j < BN / 64; ++j)
-                ptx::tma_load_2d(sb + j * 8192, &tmB, &full_bar[stage], ti.bx + 64 * j, ti.by + kb * kBK);
-            } else {
-              ptx::tma_load_2d(sb, &tmB, &full_bar[stage], ti.bx + kb * kBK, ti.by);
-            }
+        // K ranges: wgrad walks the group's (source) sub-segments; every other mode has one range
+        const int nsub = (kMode == kModeWgrad) ? p.nsub : 1;
+        for (int sub = 0; sub < nsub; ++sub) {
+          int klen = ti.k_len, krow = 0;
+          if constexpr (kMode == kModeWgrad) {
+            klen = s_rows[sub * G + ti.g];
+            krow = s_start[sub * G + ti.g];
+            ti.ay = krow;
+            ti.by = krow;
           }
-          if (++stage == L::kStages) { stage = 0; phase ^= 1; }
+          const int nkb = ceil_div(klen, kBK);
+          for (int kb = 0; kb < nkb; ++kb) {
+            ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * L::kStageBytes;
+            uint8_t* sb = sa + L::kABytes;
+            if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], kCG * L::kStageBytes);
+            if constexpr (kCG == 2) {
+              const uint32_t bar = ptx::mapa(&full_bar[stage], 0);
+              if constexpr (A_MN) {
+                ptx::tma_load_2d_cg2(sa, &tmA, bar, ti.ax, ti.ay + kb * kBK);
+                ptx::tma_load_2d_cg2(sa + 8192, &tmA, bar, ti.ax + 64, ti.ay + kb * kBK);
+              } else {
+                ptx::tma_load_2d_cg2(sa, &tmA, bar, ti.ax + kb * kBK, ti.ay);
+              }
+              if constexpr (B_MN) {
+#pragma unroll
+                for (int j = 0; j < BN / 128; ++j)
+                  ptx::tma_load_2d_cg2(sb + j * 8192, &tmB, bar, ti.bx + 64 * j, ti.by + kb * kBK);
+              } else {
+                ptx::tma_load_2d_cg2(sb, &tmB, bar, ti.bx + kb * kBK, ti.by);
+              }
+            } else {
+              if constexpr (A_MN) {
+                ptx::tma_load_2d(sa, &tmA, &full_bar[stage], ti.ax, ti.ay + kb * kBK);
+                ptx::tma_load_2d(sa + 8192, &tmA, &full_bar[stage], ti.ax + 64, ti.ay + kb * kBK);
+              } else {
+                ptx::tma_load_2d(sa, &tmA, &full_bar[stage], ti.ax + kb * kBK, ti.ay);
+              }
+              if constexpr (B_MN) {
+#pragma unroll
+                for (int j = 0; j < BN / 64; ++j)
+                  ptx::tma_load_2d(sb + j * 8192, &tmB, &full_bar[stage], ti.bx + 64 * j, ti.by + kb * kBK);
+              } else {
+                ptx::tma_load_2d(sb, &tmB, &full_bar[stage], ti.bx + kb * kBK, ti.by);
+              }
+            }
+            if (++stage == L::kStages) { stage = 0; phase ^= 1; }
+          }
         }
       }
     }
@@ -341,28 +358,38 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * BN;
         const uint32_t idesc = ptx::idesc_bf16(kBM * kCG, ti.n, A_MN, B_MN);
-        const int nkb = ceil_div(ti.k_len, kBK);
-        for (int kb = 0; kb < nkb; ++kb) {
-          ptx::mbar_wait(&full_bar[stage], phase);
-          ptx::tc_fence_after();
-          if (ptx::elect_one()) {
-            const uint32_t sa = ptx::smem_u32(smem + stage * L::kStageBytes);
-            const uint32_t sb = sa + L::kABytes;
-            const int nk = min(kBK, ti.k_len - kb * kBK) / 16;
-            for (int kk = 0; kk < nk; ++kk) {
-              const uint64_t adesc = A_MN ? ptx::smem_desc_sw128(sa + kk * 2048, 8192, 1024)
-                                          : ptx::smem_desc_sw128(sa + kk * 32, 16, 1024);
-              const uint64_t bdesc = B_MN ? ptx::smem_desc_sw128(sb + kk * 2048, 8192, 1024)
-                                          : ptx::smem_desc_sw128(sb + kk * 32, 16, 1024);
-              if constexpr (kCG == 2) ptx::mma_bf16_cg2(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
-              else ptx::mma_bf16(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
+        const int nsub = (kMode == kModeWgrad) ? p.nsub : 1;
+        uint32_t acc = 0;
+        int nkb_total = 0;
+        for (int sub = 0; sub < nsub; ++sub) {
+          const int klen = (kMode == kModeWgrad) ? s_rows[sub * G + ti.g] : ti.k_len;
+          const int nkb = ceil_div(klen, kBK);
+          nkb_total += nkb;
+          for (int kb = 0; kb < nkb; ++kb) {
+            ptx::mbar_wait(&full_bar[stage], phase);
+            ptx::tc_fence_after();
+            const int nk = min(kBK, klen - kb * kBK) / 16;  // warp-uniform
+            if (ptx::elect_one()) {
+              const uint32_t sa = ptx::smem_u32(smem + stage * L::kStageBytes);
+              const uint32_t sb = sa + L::kABytes;
+              for (int kk = 0; kk < nk; ++kk) {
+                const uint64_t adesc = A_MN ? ptx::smem_desc_sw128(sa + kk * 2048, 8192, 1024)
+                                            : ptx::smem_desc_sw128(sa + kk * 32, 16, 1024);
+                const uint64_t bdesc = B_MN ? ptx::smem_desc_sw128(sb + kk * 2048, 8192, 1024)
+                                            : ptx::smem_desc_sw128(sb + kk * 32, 16, 1024);
+                const uint32_t accum = (acc | static_cast<uint32_t>(kk > 0)) ? 1u : 0u;
+                if constexpr (kCG == 2) ptx::mma_bf16_cg2(d_tmem, adesc, bdesc, idesc, accum);
+                else ptx::mma_bf16(d_tmem, adesc, bdesc, idesc, accum);
+              }
+              if constexpr (kCG == 2) ptx::mma_commit_cg2(&empty_bar[stage], 0x3);
+              else ptx::mma_commit(&empty_bar[stage]);
             }
-            if constexpr (kCG == 2) ptx::mma_commit_cg2(&empty_bar[stage], 0x3);
-            else ptx::mma_commit(&empty_bar[stage]);
+            if (nk > 0) acc = 1u;
+            __syncwarp();
+            if (++stage == L::kStages) { stage = 0; phase ^= 1; }
           }
-          __syncwarp();
-          if (++stage == L::kStages) { stage = 0; phase ^= 1; }
         }
+        const int nkb = nkb_total;
         if (ptx::elect_one()) {
           if (nkb > 0) {
             if constexpr (kCG == 2) ptx::mma_commit_cg2(&tfull_bar[buf], 0x3);

@@ -154,7 +154,7 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
   const int E = c.N / c.world_size;
   const long long T = static_cast<long long>(c.P) * c.S;
   // receive side: worst case every token of every rank picks this rank's experts
-  r_max_ = static_cast<int>(static_cast<long long>(c.world_size) * T * c.k + 16LL * E);
+  r_max_ = static_cast<int>(static_cast<long long>(c.world_size) * (T * c.k + 16LL * E));
   rw_.reserve(arena_, c.P, c.S, c.N, c.k);
   arena_.reserve(xp_, static_cast<long long>(r_max_) * c.d);
   arena_.reserve(O_, static_cast<long long>(r_max_) * c.d_out);
@@ -166,15 +166,13 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
   }
   if (c.need_dx) arena_.reserve(dxp_, static_cast<long long>(r_max_) * c.d);
   if (ep_) {
-    r_send_ = static_cast<int>(T * c.k);
+    r_send_ = static_cast<int>(T * c.k + 16LL * c.N);
     arena_.reserve(x_send_, static_cast<long long>(r_send_) * c.d);
     arena_.reserve(o_back_, static_cast<long long>(r_send_) * c.d_out);
     arena_.reserve(do_send_, static_cast<long long>(r_send_) * c.d_out);
     if (c.need_dx) arena_.reserve(dx_send_, static_cast<long long>(r_send_) * c.d);
     arena_.reserve(recv_counts_, static_cast<long long>(c.world_size) * E);
-    arena_.reserve(seg_start_r_, E);
-    arena_.reserve(seg_rows_r_, E);
-    arena_.reserve(seg_real_r_, E);
+    arena_.reserve(seg_start_r_, 2LL * c.world_size * E);  // seg_start [P*E] then seg_rows [P*E]
   }
   arena_.reserve(dz_, T * n64_);
   arena_.reserve(logits_, T * c.N);
@@ -185,7 +183,10 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
   n_loss_part_ = combine_blocks(T);
   arena_.reserve(loss_part_, n_loss_part_);
   arena_.commit();
-  if (ep_) TAMOE_CUDA(cudaMallocHost(&h_seg_, sizeof(int) * 3 * E));
+  if (ep_) {
+    seg_rows_r_ = seg_start_r_ + c.world_size * E;
+    TAMOE_CUDA(cudaMallocHost(&h_seg_, sizeof(int) * 2 * c.world_size * E));
+  }
 
   // host-side, once per topology: penalties p = Norm(1/c_hat) and capacities (gate.cpp:151-180, 222-246)
   std::vector<double> pen(static_cast<size_t>(c.P) * c.N, 1.0 / c.N);
@@ -208,41 +209,45 @@ Layer::~Layer() {
   if (h_seg_) cudaFreeHost(h_seg_);
 }
 
-void Layer::experts_forward(const LayerIO& io, int E, const int* seg_start, const int* seg_rows, int rows,
-                            cudaStream_t s) {
+// Segments: G groups; group g uses weight g % E (E = G when nsub == 1).  For wgrad the E experts'
+// K ranges are the nsub = G / E sub-segments s*E + e.
+void Layer::experts_forward(const LayerIO& io, int G, int E, int /*nsub*/, const int* seg_start, const int* seg_rows,
+                            int rows, cudaStream_t s) {
   const LayerConfig& c = cfg_;
   PhaseTimer& tm = timer_;
+  const int wm = G == E ? 0 : E;
   if (c.f == 0) {
-    grouped_fwd(xp_, io.w1, E, c.d_out, c.d, rows, seg_start, seg_rows, O_, nullptr, kActNone, s);
+    grouped_fwd(xp_, io.w1, G, c.d_out, c.d, rows, seg_start, seg_rows, O_, nullptr, kActNone, s, wm);
     tm.mark("expert_fwd", s);
   } else {
-    grouped_fwd(xp_, io.w1, E, c.f, c.d, rows, seg_start, seg_rows, H_, A_, c.act, s);
+    grouped_fwd(xp_, io.w1, G, c.f, c.d, rows, seg_start, seg_rows, H_, A_, c.act, s, wm);
     tm.mark("expert_fwd1", s);
-    grouped_fwd(H_, io.w2, E, c.d_out, c.f, rows, seg_start, seg_rows, O_, nullptr, kActNone, s);
+    grouped_fwd(H_, io.w2, G, c.d_out, c.f, rows, seg_start, seg_rows, O_, nullptr, kActNone, s, wm);
     tm.mark("expert_fwd2", s);
   }
 }
 
-void Layer::experts_backward(const LayerIO& io, int E, const int* seg_start, const int* seg_rows, int rows,
-                             cudaStream_t s) {
+void Layer::experts_backward(const LayerIO& io, int G, int E, int nsub, const int* seg_start, const int* seg_rows,
+                             int rows, cudaStream_t s) {
   const LayerConfig& c = cfg_;
   PhaseTimer& tm = timer_;
+  const int wm = G == E ? 0 : E;
   if (c.f == 0) {
-    grouped_wgrad(dO_, xp_, E, c.d_out, c.d, rows, seg_start, seg_rows, io.dw1, s);
+    grouped_wgrad(dO_, xp_, E, c.d_out, c.d, rows, seg_start, seg_rows, io.dw1, s, nsub);
     tm.mark("expert_wgrad", s);
     if (c.need_dx) {
-      grouped_dgrad(dO_, io.w1, E, c.d, c.d_out, rows, seg_start, seg_rows, dxp_, nullptr, kActNone, s);
+      grouped_dgrad(dO_, io.w1, G, c.d, c.d_out, rows, seg_start, seg_rows, dxp_, nullptr, kActNone, s, wm);
       tm.mark("expert_dgrad", s);
     }
   } else {
-    grouped_dgrad(dO_, io.w2, E, c.f, c.d_out, rows, seg_start, seg_rows, dA_, A_, c.act, s);
+    grouped_dgrad(dO_, io.w2, G, c.f, c.d_out, rows, seg_start, seg_rows, dA_, A_, c.act, s, wm);
     tm.mark("expert_dgrad2", s);
-    grouped_wgrad(dO_, H_, E, c.d_out, c.f, rows, seg_start, seg_rows, io.dw2, s);
+    grouped_wgrad(dO_, H_, E, c.d_out, c.f, rows, seg_start, seg_rows, io.dw2, s, nsub);
     tm.mark("expert_wgrad2", s);
-    grouped_wgrad(dA_, xp_, E, c.f, c.d, rows, seg_start, seg_rows, io.dw1, s);
+    grouped_wgrad(dA_, xp_, E, c.f, c.d, rows, seg_start, seg_rows, io.dw1, s, nsub);
     tm.mark("expert_wgrad1", s);
     if (c.need_dx) {
-      grouped_dgrad(dA_, io.w1, E, c.d, c.f, rows, seg_start, seg_rows, dxp_, nullptr, kActNone, s);
+      grouped_dgrad(dA_, io.w1, G, c.d, c.f, rows, seg_start, seg_rows, dxp_, nullptr, kActNone, s, wm);
       tm.mark("expert_dgrad1", s);
     }
   }
@@ -279,9 +284,9 @@ void Layer::step_local(const LayerIO& io, cudaStream_t s) {
   route_front(*this, rw_, tm, io, n_pad_, c.d, c.cap_mode, logits_, s);
   route_permute(rw_.dims, b, io.x, c.d, xp_, r_max_, dO_, c.d_out, s);
   tm.mark("permute", s);
-  experts_forward(io, c.N, b.seg_start, b.seg_rows, r_max_, s);
+  experts_forward(io, c.N, c.N, 1, b.seg_start, b.seg_rows, r_max_, s);
   combine(io, O_, dO_, s);
-  experts_backward(io, c.N, b.seg_start, b.seg_rows, r_max_, s);
+  experts_backward(io, c.N, c.N, 1, b.seg_start, b.seg_rows, r_max_, s);
   gate_backward(io, dxp_, s);
   tm.end(s);
 }
@@ -290,38 +295,34 @@ void Layer::step_ep(const LayerIO& io, cudaStream_t s) {
   const LayerConfig& c = cfg_;
   const RouteBuffers& b = rw_.buf;
   PhaseTimer& tm = timer_;
-  const int E = c.N / c.world_size;
+  const int W = c.world_size, E = c.N / W;
   tm.begin(s);
   route_front(*this, rw_, tm, io, n_pad_, c.d, c.cap_mode, logits_, s);
-  // packed send layout: this rank's kept picks, expert-major (= destination-rank-major)
-  route_permute(rw_.dims, b, io.x, c.d, x_send_, r_send_, nullptr, 0, s, /*pad=*/1);
+  // send layout = the local padded expert-major layout: destination blocks are contiguous, pad rows zero
+  route_permute(rw_.dims, b, io.x, c.d, x_send_, r_send_, do_send_, c.d_out, s);
   tm.mark("permute", s);
-  // counts all-to-all + receiver plan (host)
+  // counts all-to-all + receive plan (host)
   ep_->exchange_counts(b.counts, recv_counts_, c.N, s);
-  for (int e = 0; e < E; ++e) {
-    h_seg_[e] = ep_->seg_start()[e];
-    h_seg_[E + e] = ep_->seg_rows()[e];
-    h_seg_[2 * E + e] = ep_->seg_real()[e];
+  for (int i = 0; i < W * E; ++i) {
+    h_seg_[i] = ep_->seg_start()[i];
+    h_seg_[W * E + i] = ep_->seg_rows()[i];
   }
-  TAMOE_CUDA(cudaMemcpyAsync(seg_start_r_, h_seg_, sizeof(int) * E, cudaMemcpyHostToDevice, s));
-  TAMOE_CUDA(cudaMemcpyAsync(seg_rows_r_, h_seg_ + E, sizeof(int) * E, cudaMemcpyHostToDevice, s));
-  TAMOE_CUDA(cudaMemcpyAsync(seg_real_r_, h_seg_ + 2 * E, sizeof(int) * E, cudaMemcpyHostToDevice, s));
+  TAMOE_CUDA(cudaMemcpyAsync(seg_start_r_, h_seg_, sizeof(int) * 2 * W * E, cudaMemcpyHostToDevice, s));
   tm.mark("a2a_counts", s);
-  // dispatch all-to-all straight into the padded expert-major layout
+  const int rows = ep_->recv_rows();
+  // dispatch all-to-all: one contiguous block per peer, straight into the (source, expert) GEMM layout
   ep_->dispatch(x_send_, xp_, c.d, s);
   last_a2a_bytes_[0] = ep_->last_offrank_bytes();
-  zero_pad_rows(seg_start_r_, seg_rows_r_, seg_real_r_, E, xp_, c.d, nullptr, 0, s);
   tm.mark("a2a_dispatch", s);
-  experts_forward(io, E, seg_start_r_, seg_rows_r_, r_max_, s);
+  experts_forward(io, W * E, E, 1, seg_start_r_, seg_rows_r_, std::max(rows, 1), s);
   ep_->combine(O_, o_back_, c.d_out, s);
   last_a2a_bytes_[1] = ep_->last_offrank_bytes();
   tm.mark("a2a_combine", s);
   combine(io, o_back_, do_send_, s);
   ep_->dispatch(do_send_, dO_, c.d_out, s);
   last_a2a_bytes_[2] = ep_->last_offrank_bytes();
-  zero_pad_rows(seg_start_r_, seg_rows_r_, seg_real_r_, E, dO_, c.d_out, nullptr, 0, s);
   tm.mark("a2a_dispatch_grad", s);
-  experts_backward(io, E, seg_start_r_, seg_rows_r_, r_max_, s);
+  experts_backward(io, W * E, E, W, seg_start_r_, seg_rows_r_, std::max(rows, 1), s);
   if (c.need_dx) {
     ep_->combine(dxp_, dx_send_, c.d, s);
     last_a2a_bytes_[3] = ep_->last_offrank_bytes();
@@ -387,8 +388,8 @@ void Layer::gate_backward(const LayerIO& io, const __nv_bfloat16* dx_rows, cudaS
 }
 
 int Layer::launches_per_step() const {
-  // gate, scan, bucket, capacity, permute, combine, dz, dW GEMM + reduce (+ 2 pad-zeroing kernels with EP)
-  int n = 9 + (ep_ ? 2 : 0);
+  // gate, scan, bucket, capacity, permute, combine, dz, dW GEMM + reduce
+  int n = 9;
   n += cfg_.f == 0 ? (1 + 1 + (cfg_.need_dx ? 1 : 0)) : (2 + 3 + (cfg_.need_dx ? 1 : 0));
   if (cfg_.need_dx) n += 1;
   return n;

@@ -126,8 +126,9 @@ class Layer {
  private:
   void step_local(const LayerIO& io, cudaStream_t s);
   void step_ep(const LayerIO& io, cudaStream_t s);
-  void experts_forward(const LayerIO& io, int E, const int* seg_start, const int* seg_rows, int rows, cudaStream_t s);
-  void experts_backward(const LayerIO& io, int E, const int* seg_start, const int* seg_rows, int rows,
+  void experts_forward(const LayerIO& io, int G, int E, int nsub, const int* seg_start, const int* seg_rows, int rows,
+                       cudaStream_t s);
+  void experts_backward(const LayerIO& io, int G, int E, int nsub, const int* seg_start, const int* seg_rows, int rows,
                         cudaStream_t s);
   void gate_backward(const LayerIO& io, const __nv_bfloat16* dx_rows, cudaStream_t s);
   void combine(const LayerIO& io, const __nv_bfloat16* O_rows, __nv_bfloat16* dO_rows, cudaStream_t s);
@@ -139,8 +140,8 @@ class Layer {
   std::unique_ptr<EpComm> ep_;
   // expert-parallel send side (packed, this rank's picks in expert order) and receive-side segments
   __nv_bfloat16 *x_send_ = nullptr, *o_back_ = nullptr, *do_send_ = nullptr, *dx_send_ = nullptr;
-  int *recv_counts_ = nullptr, *seg_start_r_ = nullptr, *seg_rows_r_ = nullptr, *seg_real_r_ = nullptr;
-  int* h_seg_ = nullptr;  // pinned staging of the three receive-side segment arrays
+  int *recv_counts_ = nullptr, *seg_start_r_ = nullptr, *seg_rows_r_ = nullptr;
+  int* h_seg_ = nullptr;  // pinned staging of the receive-side segment arrays
   int r_send_ = 0;
   int n_pad_ = 0, n64_ = 0, r_max_ = 0, dw_splits_ = 1, P_global_ = 1;
   // activations (expert order, padded segments)

@@ -40,41 +40,47 @@ def _worker(rank, world, port, mode, k, errq):
         beta = np.full((world, world), 2.0) + np.eye(world) * -1.5
         c_hat = ops.target_closed_form(beta, N, k, S)
         r = O.topk_route(probs, k, mode, 1.0, c_hat)
-        # this rank's kept picks, packed in (expert, token, slot) order = destination-rank-major
-        mine = [(r["expert"][rank, s, j], s, j) for s in range(S) for j in range(k) if r["kept"][rank, s, j]]
-        mine.sort()
-        send_counts = np.zeros(N, np.int64)
-        for e, _, _ in mine:
-            send_counts[e] += 1
-        assert np.array_equal(send_counts, r["counts"][rank])
-        payload = torch.tensor([rank * 100000 + s * k + j for _, s, j in mine], dtype=torch.int64)
+        # sender layout: this rank's kept picks in (expert, token, slot) order, every expert segment padded
+        # to 16 rows (-1 = pad); the rows for destination j form one contiguous block
+        send_counts = r["counts"][rank].astype(np.int64)
+        blocks = []
+        for j in range(world):
+            blk = []
+            for e in range(j * E, (j + 1) * E):
+                rows = [rank * 100000 + s * k + jj for s in range(S) for jj in range(k)
+                        if r["kept"][rank, s, jj] and r["expert"][rank, s, jj] == e]
+                assert len(rows) == send_counts[e]
+                blk += rows + [-1] * ((-len(rows)) % 16)
+            blocks.append(blk)
+        payload = torch.tensor(sum(blocks, []), dtype=torch.int64)
         # counts all-to-all: E counts to every rank
         recv = torch.zeros(world * E, dtype=torch.int64)
         dist.all_to_all_single(recv, torch.tensor(send_counts, dtype=torch.int64))
         recv = recv.numpy().reshape(world, E)
-        seg_start, seg_rows, recv_off = ep_plan(recv)
-        # payload all-to-all (one block per destination rank), then place per (source, expert)
-        in_split = [int(send_counts[j * E:(j + 1) * E].sum()) for j in range(world)]
-        out_split = [int(recv[i].sum()) for i in range(world)]
+        seg_start, seg_rows, blk_off, blk_rows = ep_plan(recv)
+        # payload all-to-all: one block per peer, landing at the plan's block offsets
+        in_split = [len(b) for b in blocks]
+        out_split = [int(x) for x in blk_rows]
         got = torch.empty(sum(out_split), dtype=torch.int64)
         dist.all_to_all_single(got, payload, output_split_sizes=out_split, input_split_sizes=in_split)
         got = got.numpy()
-        layout = np.full(int(seg_start[-1] + seg_rows[-1]), -1, np.int64)
-        o = 0
-        for i in range(world):
-            for e in range(E):
-                c = recv[i, e]
-                layout[recv_off[i, e]:recv_off[i, e] + c] = got[o:o + c]
-                o += c
-        # expected: reference bucket order of each local expert
+        assert list(blk_off) == list(np.concatenate([[0], np.cumsum(out_split)[:-1]]))
+        # every (source, expert) segment: that process' picks in token order, then zero-padding rows;
+        # reading the segments of expert e in source order gives the reference bucket order
         for e in range(E):
             ge = rank * E + e
-            exp = [i * 100000 + s * k + j for i in range(world) for s in range(S) for j in range(k)
+            order = []
+            for i in range(world):
+                exp_i = [i * 100000 + s * k + j for s in range(S) for j in range(k)
+                         if r["kept"][i, s, j] and r["expert"][i, s, j] == ge]
+                seg = got[seg_start[i, e]:seg_start[i, e] + seg_rows[i, e]]
+                assert seg_rows[i, e] % 16 == 0
+                assert list(seg[:len(exp_i)]) == exp_i, (rank, i, e)
+                assert np.all(seg[len(exp_i):] == -1)
+                order += list(seg[:len(exp_i)])
+            ref = [i * 100000 + s * k + j for i in range(world) for s in range(S) for j in range(k)
                    if r["kept"][i, s, j] and r["expert"][i, s, j] == ge]
-            seg = layout[seg_start[e]:seg_start[e] + seg_rows[e]]
-            assert seg_rows[e] % 16 == 0 and seg_rows[e] >= len(exp)
-            assert list(seg[:len(exp)]) == exp, (rank, e)
-            assert np.all(seg[len(exp):] == -1)
+            assert order == ref
         dist.barrier()
         dist.destroy_process_group()
     except Exception as ex:  # noqa: BLE001
