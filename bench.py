@@ -257,16 +257,20 @@ def main():
     layer.enable_timing(False)
     a2a = None
     if world > 1:
-        nbytes = layer.a2a_bytes()  # off-rank bytes of the last step (dispatch, combine, grad dispatch, grad combine)
-        names = ["a2a_dispatch", "a2a_combine", "a2a_dispatch_grad", "a2a_combine_grad"]
-        a2a_ms = sum(phases.get(n, 0.0) for n in names)
-        tot = float(sum(nbytes))
-        bus = tot / (a2a_ms / 1e3) / 1e9 if a2a_ms > 0 else 0.0
-        a2a = {"offrank_bytes_per_step_rank0": nbytes, "ms_per_step": a2a_ms, "counts_exchange_ms":
-               phases.get("a2a_counts", 0.0), "bus_gbs": bus, "peak_gbs": 900.0, "frac_of_nvlink": bus / 900.0,
-               "measured_peer_peak_gbs": 770.0,
-               "note": "busBW = off-rank bytes sent per rank / time of the 4 payload all-to-alls (NCCL grouped "
-                       "send/recv, CUDA events on the step stream)"}
+        # off-rank payload bytes per step: dispatch stores, combine loads, dO stores, dX loads (all NVLink
+        # peer-memory accesses inside the compute kernels; NCCL only for counts + barriers)
+        nbytes = layer.a2a_bytes()
+        disp_ms = phases.get("a2a_dispatch", 0.0)  # fused permute + dispatch kernel + barrier
+        comb_ms = phases.get("combine_loss", 0.0) + phases.get("a2a_barrier_combine", 0.0)
+        a2a = {"offrank_bytes_per_step": {"dispatch": nbytes[0], "combine_loads": nbytes[1], "dO_stores": nbytes[2],
+                                          "dx_loads": nbytes[3]},
+               "dispatch_ms": disp_ms, "combine_ms": comb_ms,
+               "dispatch_bus_gbs": nbytes[0] / (disp_ms / 1e3) / 1e9 if disp_ms > 0 else 0.0,
+               "combine_bus_gbs": (nbytes[1] + nbytes[2]) / (comb_ms / 1e3) / 1e9 if comb_ms > 0 else 0.0,
+               "peak_gbs": 900.0, "measured_peer_peak_gbs": 770.0,
+               "note": "fused NVLink peer-memory dispatch (permute kernel stores into the owner's layout) and "
+                       "combine (owner loads + dO stores); bus GB/s = off-rank bytes / phase time (CUDA events, "
+                       "incl. the stream-ordered NCCL barrier)"}
     losses = layer.losses.cpu().tolist()
     value = world * S / (ms / 1e3)
 

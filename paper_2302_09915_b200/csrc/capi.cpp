@@ -189,8 +189,10 @@ int tamoe_router_permute(tamoe_router* r, const void* x, int d, void* xp, int r_
   return guarded([&] {
     require(r && x && xp, "permute: null argument");
     RouteWorkspace& rw = r->impl.rw;
-    route_permute(rw.dims, rw.buf, static_cast<const __nv_bfloat16*>(x), d, static_cast<__nv_bfloat16*>(xp), r_max,
-                  nullptr, 0, static_cast<cudaStream_t>(stream));
+    PeerBufs pb{};
+    pb.p[0] = static_cast<__nv_bfloat16*>(xp);
+    route_permute(rw.dims, rw.buf, static_cast<const __nv_bfloat16*>(x), d, pb, r_max, nullptr, 0, RowMap{},
+                  static_cast<cudaStream_t>(stream));
   });
 }
 
@@ -239,7 +241,7 @@ int tamoe_layer_create_ep(const tamoe_layer_config* cfg, const double* c_hat, co
 int tamoe_layer_a2a_bytes(tamoe_layer* l, long long* out4) {
   return guarded([&] {
     require(l && out4, "a2a_bytes: null argument");
-    for (int i = 0; i < 4; ++i) out4[i] = l->impl.a2a_bytes()[i];
+    l->impl.a2a_bytes(out4);
   });
 }
 

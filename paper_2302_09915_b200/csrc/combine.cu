@@ -49,11 +49,21 @@ __global__ void __launch_bounds__(kCombWarps * 32) combine_loss_kernel(CombineAr
     const int k = KT > 0 ? KT : a.k;
     int rows[KM];
     float g[KM], dot[KM];
+    const __nv_bfloat16* osrc[KM];
+    __nv_bfloat16* odst[KM];
 #pragma unroll
     for (int j = 0; j < KM; ++j) {
       rows[j] = (j < k) ? a.pos[t * k + j] : -1;
       g[j] = (j < k) ? a.gate[t * k + j] : 0.f;
       dot[j] = 0.f;
+      osrc[j] = nullptr;
+      odst[j] = nullptr;
+      if (rows[j] >= 0) {
+        const int owner = a.map.rank_of(a.idx[t * k + j]);
+        const long long r = a.map.row(rows[j], owner);
+        osrc[j] = a.O.p[owner] + r * a.dout;
+        odst[j] = a.dO.p[owner] + r * a.dout;
+      }
     }
     const int nv = a.dout / 8;
     const uint4* __restrict__ y4 = reinterpret_cast<const uint4*>(a.y + t * a.dout);
@@ -65,9 +75,7 @@ __global__ void __launch_bounds__(kCombWarps * 32) combine_loss_kernel(CombineAr
         yv[u] = v < nv ? y4[v] : make_uint4(0, 0, 0, 0);
 #pragma unroll
         for (int j = 0; j < KM; ++j)
-          ov[j][u] = (rows[j] >= 0 && v < nv)
-                         ? reinterpret_cast<const uint4*>(a.O + static_cast<long long>(rows[j]) * a.dout)[v]
-                         : make_uint4(0, 0, 0, 0);
+          ov[j][u] = (rows[j] >= 0 && v < nv) ? reinterpret_cast<const uint4*>(osrc[j])[v] : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
@@ -99,7 +107,7 @@ __global__ void __launch_bounds__(kCombWarps * 32) combine_loss_kernel(CombineAr
               dot[j] += r[i] * o[j][i];
               go[i] = a.mse_scale * g[j] * r[i];
             }
-            reinterpret_cast<uint4*>(a.dO + static_cast<long long>(rows[j]) * a.dout)[v] = pack8(go);
+            reinterpret_cast<uint4*>(odst[j])[v] = pack8(go);
           }
         }
       }

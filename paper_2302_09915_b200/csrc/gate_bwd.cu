@@ -184,8 +184,10 @@ __global__ void dwg_reduce_kernel(const float* __restrict__ part, int splits, in
 struct EpiGateDx {
   struct Params {
     __nv_bfloat16* dx;
-    const __nv_bfloat16* dxp;
+    PeerBufs dxp;      // expert-path input gradients in every owner's receive layout
     const int* pos;
+    const int* idx;
+    RowMap map;
     int k, S, d;
   };
   static __device__ __forceinline__ void finish(const Params&, int) {}
@@ -197,8 +199,16 @@ struct EpiGateDx {
     const bool valid = tok < e.S;  // tcgen05.ld is warp-collective: every lane runs the loop
     const long long gtok = static_cast<long long>(ti.g) * e.S + tok;
     int rows[kMaxTopK];
+    const __nv_bfloat16* srcs[kMaxTopK];
 #pragma unroll
-    for (int j = 0; j < kMaxTopK; ++j) rows[j] = (valid && j < e.k) ? e.pos[gtok * e.k + j] : -1;
+    for (int j = 0; j < kMaxTopK; ++j) {
+      rows[j] = (valid && j < e.k) ? e.pos[gtok * e.k + j] : -1;
+      srcs[j] = nullptr;
+      if (rows[j] >= 0) {
+        const int owner = e.map.rank_of(e.idx[gtok * e.k + j]);
+        srcs[j] = e.dxp.p[owner] + e.map.row(rows[j], owner) * e.d;
+      }
+    }
     for (int c0 = 32 * h; c0 < ti.n; c0 += 64) {
       float v[32];
       load_acc32(tmem_tile, c0, v);
@@ -206,7 +216,7 @@ struct EpiGateDx {
 #pragma unroll
       for (int j = 0; j < kMaxTopK; ++j) {
         if (rows[j] >= 0) {
-          const uint4* src = reinterpret_cast<const uint4*>(e.dxp + static_cast<long long>(rows[j]) * e.d + col);
+          const uint4* src = reinterpret_cast<const uint4*>(srcs[j] + col);
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const uint4 w = src[u];
@@ -283,13 +293,14 @@ void gate_dw(const __nv_bfloat16* x, const __nv_bfloat16* dz, int P, int S, int 
 }
 
 void gate_dx(const __nv_bfloat16* dz, const __nv_bfloat16* wg, int P, int S, int d, int n64, int n_pad,
-             const __nv_bfloat16* dxp, const int* pos, int k, __nv_bfloat16* dx, cudaStream_t s) {
+             const PeerBufs& dxp, const int* pos, const int* idx, const RowMap& map, int k, __nv_bfloat16* dx,
+             cudaStream_t s) {
   require(d % 256 == 0, "gate dX: d must be a multiple of 256");
   const long long T = static_cast<long long>(P) * S;
   CUtensorMap ta = make_tmap_bf16(dz, n64, T, n64, 128);                         // A = dz (K-major)
   CUtensorMap tb = make_tmap_bf16(wg, d, static_cast<uint64_t>(P) * n_pad, d, 64);  // B = Wg (MN-major)
   GemmParams p{1, nullptr, nullptr, 0, d, n_pad, 1, S, n_pad, P, 0, 1};
-  EpiGateDx::Params ep{dx, dxp, pos, k, S, d};
+  EpiGateDx::Params ep{dx, dxp, pos, idx, map, k, S, d};
   launch_gemm<kModeGateDx, 256, false, true, EpiGateDx>(ta, tb, p, ep, 0, s);
 }
 

@@ -2,6 +2,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "route.hpp"
+
 namespace tamoe {
 
 struct GateDzArgs {
@@ -28,7 +30,9 @@ void gate_dz(const GateDzArgs& a, cudaStream_t s);
 int gate_dw_splits(int P, int S, int d, int n64);
 void gate_dw(const __nv_bfloat16* x, const __nv_bfloat16* dz, int P, int S, int d, int n64, int n_pad, int N,
              float* part, int splits, float* dwg, cudaStream_t s);
+// dX = dz Wg + sum over kept slots of the expert-path gradient rows (read from the owners' layouts).
 void gate_dx(const __nv_bfloat16* dz, const __nv_bfloat16* wg, int P, int S, int d, int n64, int n_pad,
-             const __nv_bfloat16* dxp, const int* pos, int k, __nv_bfloat16* dx, cudaStream_t s);
+             const PeerBufs& dxp, const int* pos, const int* idx, const RowMap& map, int k, __nv_bfloat16* dx,
+             cudaStream_t s);
 
 }  // namespace tamoe

@@ -165,14 +165,16 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
     arena_.reserve(dA_, static_cast<long long>(r_max_) * c.f);
   }
   if (c.need_dx) arena_.reserve(dxp_, static_cast<long long>(r_max_) * c.d);
+  r_local_ = static_cast<int>(T * c.k + 16LL * c.N);
   if (ep_) {
-    r_send_ = static_cast<int>(T * c.k + 16LL * c.N);
-    arena_.reserve(x_send_, static_cast<long long>(r_send_) * c.d);
-    arena_.reserve(o_back_, static_cast<long long>(r_send_) * c.d_out);
-    arena_.reserve(do_send_, static_cast<long long>(r_send_) * c.d_out);
-    if (c.need_dx) arena_.reserve(dx_send_, static_cast<long long>(r_send_) * c.d);
-    arena_.reserve(recv_counts_, static_cast<long long>(c.world_size) * E);
-    arena_.reserve(seg_start_r_, 2LL * c.world_size * E);  // seg_start [P*E] then seg_rows [P*E]
+    const int W = c.world_size;
+    arena_.reserve(plan_.all_counts, static_cast<long long>(W) * c.N);
+    arena_.reserve(plan_.seg_start, static_cast<long long>(W) * E);
+    arena_.reserve(plan_.seg_rows, static_cast<long long>(W) * E);
+    arena_.reserve(plan_.dst_base, W);
+    arena_.reserve(plan_.send_off, W);
+    arena_.reserve(plan_.recv_rows, 1);
+    arena_.reserve(plan_.flag, 1);
   }
   arena_.reserve(dz_, T * n64_);
   arena_.reserve(logits_, T * c.N);
@@ -184,8 +186,12 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
   arena_.reserve(loss_part_, n_loss_part_);
   arena_.commit();
   if (ep_) {
-    seg_rows_r_ = seg_start_r_ + c.world_size * E;
-    TAMOE_CUDA(cudaMallocHost(&h_seg_, sizeof(int) * 2 * c.world_size * E));
+    // every rank's arena has the same layout: map them all into this process (CUDA IPC over NVLink)
+    ep_->map_peers(arena_.base(), bases_);
+    map_.P = c.world_size;
+    map_.E = E;
+    map_.send_off = plan_.send_off;
+    map_.dst_base = plan_.dst_base;
   }
 
   // host-side, once per topology: penalties p = Norm(1/c_hat) and capacities (gate.cpp:151-180, 222-246)
@@ -205,8 +211,37 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
   rw_.upload_caps(caps.data() + static_cast<size_t>(c.rank) * c.P * c.N, nullptr);
 }
 
-Layer::~Layer() {
-  if (h_seg_) cudaFreeHost(h_seg_);
+Layer::~Layer() = default;
+
+PeerBufs Layer::peers(__nv_bfloat16* local) const {
+  PeerBufs pb{};
+  if (!ep_) {
+    pb.p[0] = local;
+    return pb;
+  }
+  const long long off = reinterpret_cast<char*>(local) - arena_.base();
+  for (size_t j = 0; j < bases_.size(); ++j) pb.p[j] = reinterpret_cast<__nv_bfloat16*>(bases_[j] + off);
+  return pb;
+}
+
+void Layer::a2a_bytes(long long* out4) {
+  for (int i = 0; i < 4; ++i) out4[i] = 0;
+  if (!ep_) return;
+  const LayerConfig& c = cfg_;
+  const int W = c.world_size, E = c.N / W, me = c.rank;
+  std::vector<int> all(static_cast<size_t>(W) * c.N);
+  TAMOE_CUDA(cudaMemcpy(all.data(), plan_.all_counts, sizeof(int) * all.size(), cudaMemcpyDeviceToHost));
+  long long rows_pad = 0, rows = 0;
+  for (int e = 0; e < c.N; ++e) {
+    if (e / E == me) continue;
+    const long long cnt = all[static_cast<size_t>(me) * c.N + e];
+    rows += cnt;
+    rows_pad += (cnt + 15) / 16 * 16;
+  }
+  out4[0] = rows_pad * c.d * 2;     // dispatch stores (incl. zero pad rows)
+  out4[1] = rows * c.d_out * 2;     // combine loads of expert outputs
+  out4[2] = rows * c.d_out * 2;     // dO stores
+  out4[3] = c.need_dx ? rows * c.d * 2 : 0;  // dX loads
 }
 
 // Segments: G groups; group g uses weight g % E (E = G when nsub == 1).  For wgrad the E experts'
@@ -282,15 +317,18 @@ void Layer::step_local(const LayerIO& io, cudaStream_t s) {
   PhaseTimer& tm = timer_;
   tm.begin(s);
   route_front(*this, rw_, tm, io, n_pad_, c.d, c.cap_mode, logits_, s);
-  route_permute(rw_.dims, b, io.x, c.d, xp_, r_max_, dO_, c.d_out, s);
+  const PeerBufs zb = peers(dO_);
+  route_permute(rw_.dims, b, io.x, c.d, peers(xp_), r_max_, &zb, c.d_out, map_, s);
   tm.mark("permute", s);
   experts_forward(io, c.N, c.N, 1, b.seg_start, b.seg_rows, r_max_, s);
-  combine(io, O_, dO_, s);
+  combine(io, s);
   experts_backward(io, c.N, c.N, 1, b.seg_start, b.seg_rows, r_max_, s);
-  gate_backward(io, dxp_, s);
+  gate_backward(io, s);
   tm.end(s);
 }
 
+// Expert parallel step: NCCL carries only the counts all-gather and barriers; every payload moves over
+// NVLink through peer-mapped memory inside the compute kernels.
 void Layer::step_ep(const LayerIO& io, cudaStream_t s) {
   const LayerConfig& c = cfg_;
   const RouteBuffers& b = rw_.buf;
@@ -298,41 +336,30 @@ void Layer::step_ep(const LayerIO& io, cudaStream_t s) {
   const int W = c.world_size, E = c.N / W;
   tm.begin(s);
   route_front(*this, rw_, tm, io, n_pad_, c.d, c.cap_mode, logits_, s);
-  // send layout = the local padded expert-major layout: destination blocks are contiguous, pad rows zero
-  route_permute(rw_.dims, b, io.x, c.d, x_send_, r_send_, do_send_, c.d_out, s);
-  tm.mark("permute", s);
-  // counts all-to-all + receive plan (host)
-  ep_->exchange_counts(b.counts, recv_counts_, c.N, s);
-  for (int i = 0; i < W * E; ++i) {
-    h_seg_[i] = ep_->seg_start()[i];
-    h_seg_[W * E + i] = ep_->seg_rows()[i];
-  }
-  TAMOE_CUDA(cudaMemcpyAsync(seg_start_r_, h_seg_, sizeof(int) * 2 * W * E, cudaMemcpyHostToDevice, s));
+  ep_->allgather_counts(b.counts, plan_.all_counts, c.N, s);  // also: every rank finished its previous step
+  ep_plan_device(plan_, W, E, c.rank, s);
   tm.mark("a2a_counts", s);
-  const int rows = ep_->recv_rows();
-  // dispatch all-to-all: one contiguous block per peer, straight into the (source, expert) GEMM layout
-  ep_->dispatch(x_send_, xp_, c.d, s);
-  last_a2a_bytes_[0] = ep_->last_offrank_bytes();
+  // fused permute + dispatch: rows (and the owners' zero pad rows of dO) stored straight into the owners
+  const PeerBufs zb = peers(dO_);
+  route_permute(rw_.dims, b, io.x, c.d, peers(xp_), r_local_, &zb, c.d_out, map_, s);
+  ep_->barrier(plan_.flag, s);
   tm.mark("a2a_dispatch", s);
-  experts_forward(io, W * E, E, 1, seg_start_r_, seg_rows_r_, std::max(rows, 1), s);
-  ep_->combine(O_, o_back_, c.d_out, s);
-  last_a2a_bytes_[1] = ep_->last_offrank_bytes();
-  tm.mark("a2a_combine", s);
-  combine(io, o_back_, do_send_, s);
-  ep_->dispatch(do_send_, dO_, c.d_out, s);
-  last_a2a_bytes_[2] = ep_->last_offrank_bytes();
-  tm.mark("a2a_dispatch_grad", s);
-  experts_backward(io, W * E, E, W, seg_start_r_, seg_rows_r_, std::max(rows, 1), s);
+  experts_forward(io, W * E, E, 1, plan_.seg_start, plan_.seg_rows, r_max_, s);
+  ep_->barrier(plan_.flag, s);
+  tm.mark("a2a_barrier_fwd", s);
+  combine(io, s);  // loads expert outputs from the owners, stores dO into the owners
+  ep_->barrier(plan_.flag, s);
+  tm.mark("a2a_barrier_combine", s);
+  experts_backward(io, W * E, E, W, plan_.seg_start, plan_.seg_rows, r_max_, s);
   if (c.need_dx) {
-    ep_->combine(dxp_, dx_send_, c.d, s);
-    last_a2a_bytes_[3] = ep_->last_offrank_bytes();
-    tm.mark("a2a_combine_grad", s);
+    ep_->barrier(plan_.flag, s);
+    tm.mark("a2a_barrier_bwd", s);
   }
-  gate_backward(io, dx_send_, s);
+  gate_backward(io, s);  // the dX epilogue loads the expert-path gradients from the owners
   tm.end(s);
 }
 
-void Layer::combine(const LayerIO& io, const __nv_bfloat16* O_rows, __nv_bfloat16* dO_rows, cudaStream_t s) {
+void Layer::combine(const LayerIO& io, cudaStream_t s) {
   const LayerConfig& c = cfg_;
   const RouteBuffers& b = rw_.buf;
   CombineArgs ca{};
@@ -341,18 +368,20 @@ void Layer::combine(const LayerIO& io, const __nv_bfloat16* O_rows, __nv_bfloat1
   ca.dout = c.d_out;
   ca.mse_scale = static_cast<float>(2.0 / (static_cast<double>(P_global_) * c.S * c.d_out));
   ca.pos = b.pos;
+  ca.idx = b.idx;
   ca.gate = b.gate;
-  ca.O = O_rows;
+  ca.O = peers(O_);
   ca.y = io.y;
   ca.y_hat = io.y_hat;
-  ca.dO = dO_rows;
+  ca.dO = peers(dO_);
+  ca.map = map_;
   ca.dldg = dldg_;
   ca.loss_part = loss_part_;
   combine_loss(ca, s);
   timer_.mark("combine_loss", s);
 }
 
-void Layer::gate_backward(const LayerIO& io, const __nv_bfloat16* dx_rows, cudaStream_t s) {
+void Layer::gate_backward(const LayerIO& io, cudaStream_t s) {
   const LayerConfig& c = cfg_;
   const RouteBuffers& b = rw_.buf;
   PhaseTimer& tm = timer_;
@@ -382,14 +411,14 @@ void Layer::gate_backward(const LayerIO& io, const __nv_bfloat16* dx_rows, cudaS
   gate_dw(io.x, dz_, c.P, c.S, c.d, n64_, n_pad_, c.N, dw_part_, dw_splits_, io.dwg, s);
   tm.mark("gate_dw", s);
   if (c.need_dx) {
-    gate_dx(dz_, io.wg, c.P, c.S, c.d, n64_, n_pad_, dx_rows, b.pos, c.k, io.dx, s);
+    gate_dx(dz_, io.wg, c.P, c.S, c.d, n64_, n_pad_, peers(dxp_), b.pos, b.idx, map_, c.k, io.dx, s);
     tm.mark("gate_dx", s);
   }
 }
 
 int Layer::launches_per_step() const {
   // gate, scan, bucket, capacity, permute, combine, dz, dW GEMM + reduce
-  int n = 9;
+  int n = 9 + (ep_ ? 1 : 0);  // + the device plan kernel
   n += cfg_.f == 0 ? (1 + 1 + (cfg_.need_dx ? 1 : 0)) : (2 + 3 + (cfg_.need_dx ? 1 : 0));
   if (cfg_.need_dx) n += 1;
   return n;

@@ -27,6 +27,7 @@ class Arena {
   }
   void commit();
   long long bytes() const { return size_; }
+  char* base() const { return base_; }
 
  private:
   struct Slot {
@@ -111,8 +112,8 @@ class Layer {
   // this rank owns experts [rank*E, (rank+1)*E), E = N / world_size, one logical process per rank.
   Layer(const LayerConfig& cfg, const double* c_hat, std::unique_ptr<EpComm> ep = nullptr);
   ~Layer();
-  // off-rank bytes of the last step's four payload all-to-alls (dispatch, combine, grad dispatch, grad combine)
-  const long long* a2a_bytes() const { return last_a2a_bytes_; }
+  // off-rank payload bytes of the last step: dispatch stores, combine loads, dO stores, dX loads
+  void a2a_bytes(long long* out4);
   void step(const LayerIO& io, cudaStream_t s);
   EpComm* ep() { return ep_.get(); }
   const LayerConfig& cfg() const { return cfg_; }
@@ -130,19 +131,19 @@ class Layer {
                        cudaStream_t s);
   void experts_backward(const LayerIO& io, int G, int E, int nsub, const int* seg_start, const int* seg_rows, int rows,
                         cudaStream_t s);
-  void gate_backward(const LayerIO& io, const __nv_bfloat16* dx_rows, cudaStream_t s);
-  void combine(const LayerIO& io, const __nv_bfloat16* O_rows, __nv_bfloat16* dO_rows, cudaStream_t s);
-  long long last_a2a_bytes_[4] = {0, 0, 0, 0};
+  void gate_backward(const LayerIO& io, cudaStream_t s);
+  void combine(const LayerIO& io, cudaStream_t s);
+  PeerBufs peers(__nv_bfloat16* local) const;
 
   LayerConfig cfg_;
   Arena arena_;
   RouteWorkspace rw_;
   std::unique_ptr<EpComm> ep_;
-  // expert-parallel send side (packed, this rank's picks in expert order) and receive-side segments
-  __nv_bfloat16 *x_send_ = nullptr, *o_back_ = nullptr, *do_send_ = nullptr, *dx_send_ = nullptr;
-  int *recv_counts_ = nullptr, *seg_start_r_ = nullptr, *seg_rows_r_ = nullptr;
-  int* h_seg_ = nullptr;  // pinned staging of the receive-side segment arrays
-  int r_send_ = 0;
+  // expert parallelism: device plan, peer-mapped arena bases, row map
+  EpPlanDev plan_{};
+  std::vector<char*> bases_;
+  RowMap map_{};
+  int r_local_ = 0;  // rows of this rank's own padded layout
   int n_pad_ = 0, n64_ = 0, r_max_ = 0, dw_splits_ = 1, P_global_ = 1;
   // activations (expert order, padded segments)
   __nv_bfloat16 *xp_ = nullptr, *O_ = nullptr, *dO_ = nullptr, *H_ = nullptr, *A_ = nullptr, *dA_ = nullptr,

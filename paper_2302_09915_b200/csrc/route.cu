@@ -301,9 +301,8 @@ constexpr int kPermWarps = 8;
 
 __global__ void __launch_bounds__(kPermWarps * 32) route_permute_kernel(RouteDims d, RouteBuffers b,
                                                                         const __nv_bfloat16* __restrict__ x, int dx,
-                                                                        __nv_bfloat16* __restrict__ xp, int r_max,
-                                                                        __nv_bfloat16* __restrict__ zrows, int zdim,
-                                                                        int pad) {
+                                                                        PeerBufs xp, int r_max, PeerBufs zrows,
+                                                                        int has_z, int zdim, RowMap map) {
   extern __shared__ int sm[];
   const int N = d.N;
   int* start = sm;          // [N]
@@ -313,14 +312,14 @@ __global__ void __launch_bounds__(kPermWarps * 32) route_permute_kernel(RouteDim
     int c = 0;
     for (int pr = 0; pr < d.P; ++pr) c += b.counts[pr * N + e];
     cnt[e] = c;
-    start[e] = (c + pad - 1) / pad * pad;
+    start[e] = (c + 15) & ~15;
   }
   __syncthreads();
   const int total = block_excl_scan(start, N, wtmp);
   if (blockIdx.x == 0) {
     for (int e = threadIdx.x; e < N; e += blockDim.x) {
       b.seg_start[e] = start[e];
-      b.seg_rows[e] = (cnt[e] + pad - 1) / pad * pad;
+      b.seg_rows[e] = (cnt[e] + 15) & ~15;
     }
     if (threadIdx.x == 0) *b.total_rows = total;
   }
@@ -332,11 +331,11 @@ __global__ void __launch_bounds__(kPermWarps * 32) route_permute_kernel(RouteDim
     const int mid = (lo + hi + 1) >> 1;
     if (start[mid] <= r) lo = mid; else hi = mid - 1;
   }
-  // skip empty experts sharing the same start
-  while (lo + 1 < N && start[lo + 1] <= r) ++lo;
   const int e = lo;
   const int j = r - start[e];
-  uint4* dst = reinterpret_cast<uint4*>(xp + static_cast<long long>(r) * dx);
+  const int dst_rank = map.rank_of(e);
+  const long long drow = map.row(r, dst_rank);
+  uint4* dst = reinterpret_cast<uint4*>(xp.p[dst_rank] + drow * dx);
   const int nv = dx / 8;
   if (j < cnt[e]) {
     const int pick = b.clist[b.list_start[e] + j];
@@ -347,8 +346,8 @@ __global__ void __launch_bounds__(kPermWarps * 32) route_permute_kernel(RouteDim
   } else {
     const uint4 z = make_uint4(0, 0, 0, 0);
     for (int v = lane; v < nv; v += 32) dst[v] = z;
-    if (zrows) {
-      uint4* zd = reinterpret_cast<uint4*>(zrows + static_cast<long long>(r) * zdim);
+    if (has_z) {
+      uint4* zd = reinterpret_cast<uint4*>(zrows.p[dst_rank] + drow * zdim);
       for (int v = lane; v < zdim / 8; v += 32) zd[v] = z;
     }
   }
@@ -392,12 +391,14 @@ void route_capacity(const RouteDims& d, const RouteBuffers& b, int mode, const i
   TAMOE_CUDA(cudaGetLastError());
 }
 
-void route_permute(const RouteDims& d, const RouteBuffers& b, const __nv_bfloat16* x, int dx, __nv_bfloat16* xp,
-                   int r_max, __nv_bfloat16* zero_rows, int zdim, cudaStream_t s, int pad) {
-  require(dx % 8 == 0 && (zero_rows == nullptr || zdim % 8 == 0), "permute: row widths must be multiples of 8");
+void route_permute(const RouteDims& d, const RouteBuffers& b, const __nv_bfloat16* x, int dx, const PeerBufs& xp,
+                   int r_max, const PeerBufs* zrows, int zdim, const RowMap& map, cudaStream_t s) {
+  require(dx % 8 == 0 && (zrows == nullptr || zdim % 8 == 0), "permute: row widths must be multiples of 8");
   const int blocks = (r_max + kPermWarps - 1) / kPermWarps;
   const size_t smem = sizeof(int) * (2 * d.N + 32);
-  route_permute_kernel<<<blocks, kPermWarps * 32, smem, s>>>(d, b, x, dx, xp, r_max, zero_rows, zdim, pad);
+  PeerBufs z{};
+  if (zrows) z = *zrows;
+  route_permute_kernel<<<blocks, kPermWarps * 32, smem, s>>>(d, b, x, dx, xp, r_max, z, zrows ? 1 : 0, zdim, map);
   TAMOE_CUDA(cudaGetLastError());
 }
 

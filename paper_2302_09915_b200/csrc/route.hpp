@@ -9,6 +9,24 @@
 namespace tamoe {
 
 constexpr int kMaxTopK = 8;
+constexpr int kMaxRanks = 16;
+
+// Maps a row of this rank's padded expert-major layout to the row it occupies in the owner rank's receive
+// layout (expert parallelism over peer memory).  P == 1: identity (everything local).
+struct RowMap {
+  int P = 1, E = 1;                // ranks, experts per rank
+  const int* send_off = nullptr;   // [P] start of this rank's block for destination j in its own layout
+  const int* dst_base = nullptr;   // [P] start of this rank's block inside rank j's receive layout
+  __device__ __forceinline__ int rank_of(int expert) const { return P == 1 ? 0 : expert / E; }
+  __device__ __forceinline__ long long row(int local_row, int j) const {
+    return P == 1 ? local_row : static_cast<long long>(local_row) - send_off[j] + dst_base[j];
+  }
+};
+
+// The same buffer in every rank's address space (peer-mapped over NVLink; p[0] only when P == 1).
+struct PeerBufs {
+  __nv_bfloat16* p[kMaxRanks];
+};
 constexpr int kRouteTile = 128;  // tokens per routing tile (= GEMM M tile), 4 warps of 32
 
 struct RouteDims {
@@ -73,9 +91,11 @@ void route_bucket(const RouteDims& d, const RouteBuffers& b, cudaStream_t s);
 void route_capacity(const RouteDims& d, const RouteBuffers& b, int mode, const int* caps, cudaStream_t s);
 // padded expert segments + gather of token rows into the expert-sorted buffer.
 // x: [P*S x dx] bf16; xp: [R_max x dx]; zero_rows (optional): second buffer whose pad rows are zeroed.
-// pad = 16: padded segments for the local expert GEMMs; pad = 1: packed send layout (expert parallelism).
-void route_permute(const RouteDims& d, const RouteBuffers& b, const __nv_bfloat16* x, int dx, __nv_bfloat16* xp,
-                   int r_max, __nv_bfloat16* zero_rows, int zdim, cudaStream_t s, int pad = 16);
+// Gather kept token rows into the padded expert-major layout (16-row segments, pad rows zeroed) and write
+// each row to wherever its owner expects it: `map`/`xp` (and the pad rows of `zrows`) may point into peer
+// ranks' memory, which fuses the dispatch all-to-all into the permute (NVLink stores).
+void route_permute(const RouteDims& d, const RouteBuffers& b, const __nv_bfloat16* x, int dx, const PeerBufs& xp,
+                   int r_max, const PeerBufs* zrows, int zdim, const RowMap& map, cudaStream_t s);
 // Zero rows [seg_start + seg_real, seg_start + seg_rows) of each of G segments in buffers a and b.
 void zero_pad_rows(const int* seg_start, const int* seg_rows, const int* seg_real, int G, __nv_bfloat16* a, int wa,
                    __nv_bfloat16* b, int wb, cudaStream_t s);
