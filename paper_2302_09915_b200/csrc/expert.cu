@@ -13,6 +13,8 @@
 // its token count rounded to 16 (not 128): weights are the M=128 operand.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "common.hpp"
 #include "expert.hpp"
 #include "gemm_sm100.cuh"
@@ -224,6 +226,11 @@ static SwapParams swap_params(__nv_bfloat16* out, __nv_bfloat16* pre_out, const 
   return e;
 }
 
+static int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
 static void check_groups(int G) { require(G >= 1 && G <= kMaxGroups, "group count out of range [1, 1024]"); }
 
 
@@ -237,7 +244,8 @@ void grouped_fwd(const __nv_bfloat16* tokens, const __nv_bfloat16* w, int G, int
   const int Gw = w_mod > 0 ? w_mod : G;  // distinct weight matrices
   CUtensorMap ta = make_tmap_bf16(w, K, static_cast<uint64_t>(Gw) * M, K, kBM);
   CUtensorMap tb = make_tmap_bf16(tokens, K, R, K, pair ? 128 : 256);
-  GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1, w_mod, 1};
+  GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1, w_mod, 1, env_int("TAMOE_PF_DIST", 0),
+               env_int("TAMOE_PF_B", 0)};
   SwapParams ep = swap_params(out, pre_out, nullptr, M, R, act, kActNone);
   if (pre_out) launch_pair_or_single<kModeSwap, 256, false, false, EpiSwap<1>>(pair, ta, tb, p, ep, s);
   else launch_pair_or_single<kModeSwap, 256, false, false, EpiSwap<0>>(pair, ta, tb, p, ep, s);
@@ -254,7 +262,8 @@ void grouped_dgrad(const __nv_bfloat16* grad_tokens, const __nv_bfloat16* w, int
   const int Gw = w_mod > 0 ? w_mod : G;
   CUtensorMap ta = make_tmap_bf16(w, M, static_cast<uint64_t>(Gw) * K, M, 64);
   CUtensorMap tb = make_tmap_bf16(grad_tokens, K, R, K, pair ? 128 : 256);
-  GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1, w_mod, 1};
+  GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1, w_mod, 1, env_int("TAMOE_PF_DIST", 0),
+               env_int("TAMOE_PF_B", 0)};
   SwapParams ep = swap_params(out, nullptr, pre_in, M, R, kActNone, pre_in ? act : kActNone);
   if (pre_in) launch_pair_or_single<kModeSwap, 256, true, false, EpiSwap<2>>(pair, ta, tb, p, ep, s);
   else launch_pair_or_single<kModeSwap, 256, true, false, EpiSwap<0>>(pair, ta, tb, p, ep, s);
@@ -269,7 +278,7 @@ void grouped_wgrad(const __nv_bfloat16* a_tokens, const __nv_bfloat16* b_tokens,
   CUtensorMap ta = make_tmap_bf16(a_tokens, M, R, M, 64);
   CUtensorMap tb = make_tmap_bf16(b_tokens, N, R, N, 64);
   require(nsub >= 1 && G * nsub <= kMaxGroups, "grouped_wgrad: too many sub-segments");
-  GemmParams p{G, seg_start, seg_rows, M, N, 0, 1, 1, 1, 1, 0, nsub};
+  GemmParams p{G, seg_start, seg_rows, M, N, 0, 1, 1, 1, 1, 0, nsub, 0, 0};
   EpiWgrad::Params ep{make_tmap_bf16_box(out, N, static_cast<uint64_t>(G) * M, N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)};
   launch_pair_or_single<kModeWgrad, 256, true, true, EpiWgrad>(M % 256 == 0, ta, tb, p, ep, s);
 }

@@ -271,7 +271,7 @@ void gate_dw(const __nv_bfloat16* x, const __nv_bfloat16* dz, int P, int S, int 
   const long long T = static_cast<long long>(P) * S;
   CUtensorMap ta = make_tmap_bf16(x, d, T, d, 64);     // A = x^T (MN-major)
   CUtensorMap tb = make_tmap_bf16(dz, n64, T, n64, 64);  // B = dz   (MN-major)
-  GemmParams p{1, nullptr, nullptr, d, 64, 0, splits, S, 0, P, 0, 1};
+  GemmParams p{1, nullptr, nullptr, d, 64, 0, splits, S, 0, P, 0, 1, 0, 0};
   // one 64-column N block per launch keeps BN = 64 (n64 > 64 loops over column blocks)
   EpiGateDw::Params ep{part, d, n64, P};
   if (n64 == 64) {
@@ -299,7 +299,7 @@ void gate_dx(const __nv_bfloat16* dz, const __nv_bfloat16* wg, int P, int S, int
   const long long T = static_cast<long long>(P) * S;
   CUtensorMap ta = make_tmap_bf16(dz, n64, T, n64, 128);                         // A = dz (K-major)
   CUtensorMap tb = make_tmap_bf16(wg, d, static_cast<uint64_t>(P) * n_pad, d, 64);  // B = Wg (MN-major)
-  GemmParams p{1, nullptr, nullptr, 0, d, n_pad, 1, S, n_pad, P, 0, 1};
+  GemmParams p{1, nullptr, nullptr, 0, d, n_pad, 1, S, n_pad, P, 0, 1, 0, 0};
   EpiGateDx::Params ep{dx, dxp, pos, idx, map, k, S, d};
   launch_gemm<kModeGateDx, 256, false, true, EpiGateDx>(ta, tb, p, ep, 0, s);
 }

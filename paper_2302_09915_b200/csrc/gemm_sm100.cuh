@@ -46,6 +46,8 @@ struct GemmParams {
   int procs;             // logical processes (gate modes)
   int w_mod;             // kModeSwap: weight of group g is g % w_mod (0: g) -- (source, expert) segments
   int nsub;              // kModeWgrad: K of group g = sub-segments s*num_groups + g, s < nsub
+  int pf_dist;           // kModeSwap: k-blocks of A/B prefetched into L2 ahead of the TMA loads (0: off)
+  int pf_b;              // also prefetch B
 };
 
 struct TileInfo {
@@ -280,9 +282,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (ptx::elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cluster_id; t < total_tiles; t += num_clusters) {
-        TileInfo ti;
-        decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, t, ti);
+      // this CTA's operand coordinates of a decoded tile
+      auto localize = [&](TileInfo& ti) {
         const int my_m0 = ti.m0 + static_cast<int>(rank) * kBM;
         if constexpr (kMode == kModeSwap) {
           if constexpr (A_MN) { ti.ax = my_m0; ti.ay = ti.wg * p.Kw; }
@@ -292,6 +293,38 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           ti.ax = my_m0;
           ti.bx += static_cast<int>(rank) * (BN / kCG);
         }
+      };
+      // Swap mode streams every expert's weights once from HBM: keep kPfDist k-blocks of A (weights) and
+      // B (tokens) prefetched into L2 ahead of the TMA loads, across tile boundaries, so DRAM latency is
+      // not bounded by the shared-memory pipeline depth.
+      const int kPfDist = p.pf_dist;
+      int pf_t = cluster_id, pf_kb = 0;
+      TileInfo pf_ti;
+      bool pf_ok = (kMode == kModeSwap) && kPfDist > 0 && pf_t < total_tiles;
+      if (pf_ok) { decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, pf_t, pf_ti); localize(pf_ti); }
+      auto pf_step = [&]() {
+        if constexpr (kMode == kModeSwap) {
+          if (!pf_ok) return;
+          if constexpr (A_MN) {
+            ptx::tma_prefetch_2d(&tmA, pf_ti.ax, pf_ti.ay + pf_kb * kBK);
+            ptx::tma_prefetch_2d(&tmA, pf_ti.ax + 64, pf_ti.ay + pf_kb * kBK);
+          } else {
+            ptx::tma_prefetch_2d(&tmA, pf_ti.ax + pf_kb * kBK, pf_ti.ay);
+          }
+          if (p.pf_b) ptx::tma_prefetch_2d(&tmB, pf_ti.bx + pf_kb * kBK, pf_ti.by);
+          if (++pf_kb >= ceil_div(pf_ti.k_len, kBK)) {
+            pf_kb = 0;
+            pf_t += num_clusters;
+            pf_ok = pf_t < total_tiles;
+            if (pf_ok) { decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, pf_t, pf_ti); localize(pf_ti); }
+          }
+        }
+      };
+      for (int i = 0; i < kPfDist; ++i) pf_step();
+      for (int t = cluster_id; t < total_tiles; t += num_clusters) {
+        TileInfo ti;
+        decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, t, ti);
+        localize(ti);
         // K ranges: wgrad walks the group's (source) sub-segments; every other mode has one range
         const int nsub = (kMode == kModeWgrad) ? p.nsub : 1;
         for (int sub = 0; sub < nsub; ++sub) {
@@ -339,6 +372,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               }
             }
             if (++stage == L::kStages) { stage = 0; phase ^= 1; }
+            pf_step();
           }
         }
       }

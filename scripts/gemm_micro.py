@@ -1,0 +1,75 @@
+"""Microbenchmark of the tcgen05 grouped GEMM engine vs cuBLAS (torch.matmul) on dense and grouped shapes."""
+import sys
+import os
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2302_09915_b200 import _lib  # noqa: E402
+
+
+def segs(counts):
+    rows = [((c + 15) // 16) * 16 for c in counts]
+    start = np.concatenate([[0], np.cumsum(rows)[:-1]]).astype(np.int32)
+    return (torch.tensor(start, dtype=torch.int32, device="cuda"), torch.tensor(rows, dtype=torch.int32, device="cuda"),
+            int(sum(rows)))
+
+
+def timeit(fn, iters=20):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(iters):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / iters
+
+
+def run(name, counts, M, K, mode="fwd"):
+    G = len(counts)
+    ss, sr, R = segs(counts)
+    x = torch.randn(R, K, device="cuda").bfloat16()
+    st = torch.cuda.current_stream().cuda_stream
+    if mode == "fwd":
+        w = torch.randn(G, M, K, device="cuda").bfloat16()
+        out = torch.empty(R, M, device="cuda", dtype=torch.bfloat16)
+        fn = lambda: _lib.call("tamoe_grouped_fwd", x.data_ptr(), w.data_ptr(), G, M, K, R, ss.data_ptr(),
+                               sr.data_ptr(), out.data_ptr(), None, 0, st)
+        flops = 2.0 * sum(counts) * M * K
+    elif mode == "dgrad":
+        w = torch.randn(G, K, M, device="cuda").bfloat16()
+        out = torch.empty(R, M, device="cuda", dtype=torch.bfloat16)
+        fn = lambda: _lib.call("tamoe_grouped_dgrad", x.data_ptr(), w.data_ptr(), G, M, K, R, ss.data_ptr(),
+                               sr.data_ptr(), out.data_ptr(), None, 0, st)
+        flops = 2.0 * sum(counts) * M * K
+    else:  # wgrad: M x N=K over rows
+        a = torch.randn(R, M, device="cuda").bfloat16()
+        out = torch.empty(G, M, K, device="cuda", dtype=torch.bfloat16)
+        fn = lambda: _lib.call("tamoe_grouped_wgrad", a.data_ptr(), x.data_ptr(), G, M, K, R, ss.data_ptr(),
+                               sr.data_ptr(), out.data_ptr(), st)
+        flops = 2.0 * sum(counts) * M * K
+    ms = timeit(fn)
+    # cuBLAS reference: dense equivalent with the same total rows
+    A = torch.randn(sum(counts), K, device="cuda").bfloat16()
+    B = torch.randn(K, M, device="cuda").bfloat16()
+    ms_cb = timeit(lambda: torch.matmul(A, B))
+    print(f"{name:34s} {mode:5s} G={G:3d} rows={sum(counts):6d} M={M:5d} K={K:5d}: ours {ms*1e3:8.1f} us "
+          f"{flops/ms/1e9:7.1f} TF/s | cuBLAS dense {ms_cb*1e3:8.1f} us {flops/ms_cb/1e9:7.1f} TF/s", flush=True)
+
+
+if __name__ == "__main__":
+    rng = np.random.default_rng(0)
+    bal = list(rng.multinomial(16384, [1 / 64] * 64))
+    run("dense 16384 rows", [16384], 4096, 1024)
+    run("dense 16384 rows", [16384], 1024, 4096)
+    run("dense 65536 rows", [65536], 4096, 4096)
+    run("64 experts x ~256 (C2 fwd1)", bal, 4096, 1024)
+    run("64 experts x ~256 (C2 fwd2)", bal, 1024, 4096)
+    run("64 experts x ~256 (C2 dgrad1)", bal, 1024, 4096, "dgrad")
+    run("64 experts x ~256 (C2 wgrad1)", bal, 4096, 1024, "wgrad")
+    run("8 experts x ~2048 (C2 ep8 fwd1)", list(rng.multinomial(16384, [1 / 8] * 8)), 4096, 1024)
+    run("8 experts x ~2048 (C2 ep8 fwd2)", list(rng.multinomial(16384, [1 / 8] * 8)), 1024, 4096)
+    run("8 experts x ~2048 (C2 ep8 wgrad)", list(rng.multinomial(16384, [1 / 8] * 8)), 4096, 1024, "wgrad")
