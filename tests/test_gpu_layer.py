@@ -119,3 +119,12 @@ def test_layer_validation_errors():
         TAMoELayer(LayerConfig(P=1, S=128, d=256, d_out=128, N=8, k=9))
     with pytest.raises(ops.ValidationError):
         TAMoELayer(LayerConfig(P=1, S=128, d=256, d_out=128, N=8, aux_kind=1), None)
+
+
+def test_layer_c4_expert_shape_reduced():
+    """BASELINE config 4 expert shape (d=4096, f=16384, top-2, capacity factor 1.25, local proportional
+    capacities from a 2-level topology) reduced so the fp64 oracle fits and finishes: 4 experts (each
+    2 x 4096 x 16384), P=2 logical processes x S=16 tokens."""
+    P, S, d, dout, N, k, f = 2, 16, 4096, 4096, 4, 2, 16384
+    layer, o, extra = run_case(P, S, d, dout, N, k, f, 3, 1, True, seed=4)
+    check(layer, o, extra, P, S, N, k, f, True)
