@@ -153,23 +153,24 @@ typedef struct {
 /* c_hat: host fp64 [P_global x N] dispatch target (required for topo loss / proportional capacity). */
 int tamoe_layer_create(const tamoe_layer_config* cfg, const double* c_hat, tamoe_layer** out);
 
-/* Expert parallelism across GPUs (one process per GPU, NCCL over NVLink / NVSwitch).
+/* Expert parallelism across GPUs (one process per GPU, NVLink / NVSwitch).
  * Rank r owns experts [r*E, (r+1)*E), E = N / world_size (dispatch.hpp:31); gate replicas are per rank with
- * no all-reduce (trainer.cpp:207-216).  Every step runs a counts all-to-all and four payload all-to-alls
- * (dispatch, combine, gradient dispatch, gradient combine) sized by the rank-local capacities
- * (local / proportional, gate.cpp:165-180).  tamoe_nccl_unique_id fills 128 bytes on one rank; broadcast them
- * to all ranks, then every rank calls tamoe_layer_create_ep with its cfg.rank / cfg.world_size. */
+ * no all-reduce (trainer.cpp:207-216).  Ranks map each other's workspaces (CUDA IPC): the permute kernel
+ * stores token rows straight into the owners (dispatch), the combine kernel loads expert outputs from the
+ * owners and stores dO into them, the gate-dX epilogue loads the owners' input gradients; NCCL carries only
+ * the counts all-gather and stream-ordered barriers.  Capacities are rank-local (local / proportional,
+ * gate.cpp:165-180).  tamoe_nccl_unique_id fills 128 bytes on one rank; broadcast them to all ranks, then
+ * every rank calls tamoe_layer_create_ep with its cfg.rank / cfg.world_size. */
 int tamoe_nccl_unique_id(void* out128);
 int tamoe_layer_create_ep(const tamoe_layer_config* cfg, const double* c_hat, const void* nccl_id128,
                           tamoe_layer** out);
 /* Off-rank payload bytes of the last step's all-to-alls: out[4] = dispatch, combine, grad dispatch, grad combine. */
 int tamoe_layer_a2a_bytes(tamoe_layer* l, long long* out4);
-/* Host-side receive plan (CPU-testable): recv[P x E] rows per (source rank, local expert) ->
- * 16-row padded (source, expert) segments seg_start/seg_rows [P x E] (source-major) and the receive block
- * offset / rows of every source rank [P].  The sender's block for this rank is its own padded expert-major
- * layout restricted to this rank's experts, so one NCCL send/recv pair per peer moves it. */
-int tamoe_ep_plan(int P, int E, const long long* recv, int* seg_start, int* seg_rows, long long* blk_off,
-                  long long* blk_rows);
+/* Host-side receive plan (CPU-testable): recv[P x E] rows per (source rank, local expert) -> the receive
+ * segment of each local expert seg_start/seg_rows [E] (expert-major; inside it one 16-row padded block per
+ * source rank, in rank order = the reference's (process, token) bucket order) and where each source's rows
+ * for it start, src_off [P x E].  The device plan kernel computes the same from the all-gathered counts. */
+int tamoe_ep_plan(int P, int E, const long long* recv, int* seg_start, int* seg_rows, long long* src_off);
 int tamoe_layer_destroy(tamoe_layer* l);
 int tamoe_layer_step(tamoe_layer* l, const tamoe_layer_io* io, void* stream);
 int tamoe_layer_read(tamoe_layer* l, int what, void* dst, long long bytes, void* stream);

@@ -245,11 +245,10 @@ int tamoe_layer_a2a_bytes(tamoe_layer* l, long long* out4) {
   });
 }
 
-int tamoe_ep_plan(int P, int E, const long long* recv, int* seg_start, int* seg_rows, long long* blk_off,
-                  long long* blk_rows) {
+int tamoe_ep_plan(int P, int E, const long long* recv, int* seg_start, int* seg_rows, long long* src_off) {
   return guarded([&] {
-    require(P >= 1 && E >= 1 && recv && seg_start && seg_rows && blk_off && blk_rows, "ep_plan: bad arguments");
-    ep_plan(P, E, recv, seg_start, seg_rows, blk_off, blk_rows);
+    require(P >= 1 && E >= 1 && recv && seg_start && seg_rows && src_off, "ep_plan: bad arguments");
+    ep_plan(P, E, recv, seg_start, seg_rows, src_off);
   });
 }
 

@@ -59,8 +59,9 @@ __global__ void __launch_bounds__(kCombWarps * 32) combine_loss_kernel(CombineAr
       osrc[j] = nullptr;
       odst[j] = nullptr;
       if (rows[j] >= 0) {
-        const int owner = a.map.rank_of(a.idx[t * k + j]);
-        const long long r = a.map.row(rows[j], owner);
+        const int ex = a.idx[t * k + j];
+        const int owner = a.map.rank_of(ex);
+        const long long r = a.map.row(rows[j], ex);
         osrc[j] = a.O.p[owner] + r * a.dout;
         odst[j] = a.dO.p[owner] + r * a.dout;
       }

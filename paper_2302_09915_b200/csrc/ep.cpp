@@ -13,18 +13,15 @@ static void nccl_check(ncclResult_t r, const char* what) {
 }
 #define TAMOE_NCCL(expr) nccl_check((expr), #expr)
 
-void ep_plan(int P, int E, const long long* recv, int* seg_start, int* seg_rows, long long* blk_off,
-             long long* blk_rows) {
+void ep_plan(int P, int E, const long long* recv, int* seg_start, int* seg_rows, long long* src_off) {
   long long row = 0;
-  for (int i = 0; i < P; ++i) {
-    blk_off[i] = row;
-    for (int e = 0; e < E; ++e) {
-      const long long r = (recv[i * E + e] + 15) / 16 * 16;
-      seg_start[i * E + e] = static_cast<int>(row);
-      seg_rows[i * E + e] = static_cast<int>(r);
-      row += r;
+  for (int e = 0; e < E; ++e) {
+    seg_start[e] = static_cast<int>(row);
+    for (int i = 0; i < P; ++i) {
+      src_off[i * E + e] = row;
+      row += (recv[i * E + e] + 15) / 16 * 16;
     }
-    blk_rows[i] = row - blk_off[i];
+    seg_rows[e] = static_cast<int>(row - seg_start[e]);
   }
 }
 

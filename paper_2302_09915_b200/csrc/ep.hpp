@@ -21,13 +21,14 @@
 
 namespace tamoe {
 
-// Per-step device plan, identical on all ranks up to the `me` perspective.
+// Per-step device plan, identical on all ranks up to the `me` perspective.  Receive layout of a rank:
+// expert-major; expert e_l holds one 16-row-padded segment per source rank (in rank order), so every
+// local expert is one contiguous GEMM group whose rows follow the reference order (process, token).
 struct EpPlanDev {
   int* all_counts = nullptr;  // [P x N] kept counts of every rank (all-gather)
-  int* seg_start = nullptr;   // [P*E] receive segments of this rank, source-major (src*E + e)
-  int* seg_rows = nullptr;    // [P*E] 16-row padded
-  int* dst_base = nullptr;    // [P] start of this rank's block inside rank j's receive layout
-  int* send_off = nullptr;    // [P] start of this rank's block for j in its own padded layout
+  int* seg_start = nullptr;   // [E] receive segment of each local expert
+  int* seg_rows = nullptr;    // [E]
+  int* dst_off = nullptr;     // [N] where this rank's rows for global expert e start at the owner
   int* recv_rows = nullptr;   // [1]
   int* flag = nullptr;        // [1] barrier scratch
 };
@@ -53,9 +54,8 @@ class EpComm {
   std::vector<void*> opened_;
 };
 
-// Host reference of the receive plan (CPU-testable): recv[src][e] (P x E) rows -> (source, expert)
-// segments seg_start/seg_rows [P*E] (16-row padded, source-major) and block offsets/rows per source [P].
-void ep_plan(int P, int E, const long long* recv, int* seg_start, int* seg_rows, long long* blk_off,
-             long long* blk_rows);
+// Host reference of the receive plan (CPU-testable): recv[src][e] (P x E) rows -> per local expert the
+// segment seg_start/seg_rows [E] and the row where each source's rows for it start, src_off [P x E].
+void ep_plan(int P, int E, const long long* recv, int* seg_start, int* seg_rows, long long* src_off);
 
 }  // namespace tamoe

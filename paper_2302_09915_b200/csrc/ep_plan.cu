@@ -8,37 +8,27 @@ namespace {
 
 __device__ __forceinline__ int pad16(int c) { return (c + 15) & ~15; }
 
+// expert-major receive layouts: at rank j, local expert e_l owns rows
+//   [ sum_{e' < e_l} sum_src pad16(c[src][jE+e']) , ... ) split into per-source segments in rank order.
 __global__ void ep_plan_kernel(EpPlanDev p, int P, int E, int me) {
-  __shared__ int blk[kMaxRanks * kMaxRanks];  // blk[i*P + j] = padded rows rank i sends to rank j
   const int N = P * E;
-  for (int ij = threadIdx.x; ij < P * P; ij += blockDim.x) {
-    const int i = ij / P, j = ij % P;
-    int r = 0;
-    for (int e = 0; e < E; ++e) r += pad16(p.all_counts[i * N + j * E + e]);
-    blk[ij] = r;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int recv = 0;
-    for (int i = 0; i < P; ++i) {
-      int row = recv;
-      for (int e = 0; e < E; ++e) {
-        const int c = pad16(p.all_counts[i * N + me * E + e]);
-        p.seg_start[i * E + e] = row;
-        p.seg_rows[i * E + e] = c;
-        row += c;
-      }
-      recv += blk[i * P + me];
-    }
-    *p.recv_rows = recv;
+  // one thread per global expert: where do my rows for it start at its owner?
+  for (int ge = threadIdx.x; ge < N; ge += blockDim.x) {
+    const int j = ge / E, el = ge % E;
     int off = 0;
-    for (int j = 0; j < P; ++j) {
-      int base = 0;
-      for (int i = 0; i < me; ++i) base += blk[i * P + j];
-      p.dst_base[j] = base;
-      p.send_off[j] = off;
-      off += blk[me * P + j];
+    for (int e2 = 0; e2 < el; ++e2)
+      for (int i = 0; i < P; ++i) off += pad16(p.all_counts[i * N + j * E + e2]);
+    for (int i = 0; i < me; ++i) off += pad16(p.all_counts[i * N + ge]);
+    p.dst_off[ge] = off;
+  }
+  if (threadIdx.x == 0) {
+    int row = 0;
+    for (int el = 0; el < E; ++el) {
+      p.seg_start[el] = row;
+      for (int i = 0; i < P; ++i) row += pad16(p.all_counts[i * N + me * E + el]);
+      p.seg_rows[el] = row - p.seg_start[el];
     }
+    *p.recv_rows = row;
   }
 }
 

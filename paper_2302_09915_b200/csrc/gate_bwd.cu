@@ -205,8 +205,9 @@ struct EpiGateDx {
       rows[j] = (valid && j < e.k) ? e.pos[gtok * e.k + j] : -1;
       srcs[j] = nullptr;
       if (rows[j] >= 0) {
-        const int owner = e.map.rank_of(e.idx[gtok * e.k + j]);
-        srcs[j] = e.dxp.p[owner] + e.map.row(rows[j], owner) * e.d;
+        const int ex = e.idx[gtok * e.k + j];
+        const int owner = e.map.rank_of(ex);
+        srcs[j] = e.dxp.p[owner] + e.map.row(rows[j], ex) * e.d;
       }
     }
     for (int c0 = 32 * h; c0 < ti.n; c0 += 64) {

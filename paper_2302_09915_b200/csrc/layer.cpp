@@ -169,10 +169,9 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
   if (ep_) {
     const int W = c.world_size;
     arena_.reserve(plan_.all_counts, static_cast<long long>(W) * c.N);
-    arena_.reserve(plan_.seg_start, static_cast<long long>(W) * E);
-    arena_.reserve(plan_.seg_rows, static_cast<long long>(W) * E);
-    arena_.reserve(plan_.dst_base, W);
-    arena_.reserve(plan_.send_off, W);
+    arena_.reserve(plan_.seg_start, E);
+    arena_.reserve(plan_.seg_rows, E);
+    arena_.reserve(plan_.dst_off, c.N);
     arena_.reserve(plan_.recv_rows, 1);
     arena_.reserve(plan_.flag, 1);
   }
@@ -190,8 +189,8 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
     ep_->map_peers(arena_.base(), bases_);
     map_.P = c.world_size;
     map_.E = E;
-    map_.send_off = plan_.send_off;
-    map_.dst_base = plan_.dst_base;
+    map_.local_start = rw_.buf.seg_start;
+    map_.dst_off = plan_.dst_off;
   }
 
   // host-side, once per topology: penalties p = Norm(1/c_hat) and capacities (gate.cpp:151-180, 222-246)
@@ -344,13 +343,13 @@ void Layer::step_ep(const LayerIO& io, cudaStream_t s) {
   route_permute(rw_.dims, b, io.x, c.d, peers(xp_), r_local_, &zb, c.d_out, map_, s);
   ep_->barrier(plan_.flag, s);
   tm.mark("a2a_dispatch", s);
-  experts_forward(io, W * E, E, 1, plan_.seg_start, plan_.seg_rows, r_max_, s);
+  experts_forward(io, E, E, 1, plan_.seg_start, plan_.seg_rows, r_max_, s);
   ep_->barrier(plan_.flag, s);
   tm.mark("a2a_barrier_fwd", s);
   combine(io, s);  // loads expert outputs from the owners, stores dO into the owners
   ep_->barrier(plan_.flag, s);
   tm.mark("a2a_barrier_combine", s);
-  experts_backward(io, W * E, E, W, plan_.seg_start, plan_.seg_rows, r_max_, s);
+  experts_backward(io, E, E, 1, plan_.seg_start, plan_.seg_rows, r_max_, s);
   if (c.need_dx) {
     ep_->barrier(plan_.flag, s);
     tm.mark("a2a_barrier_bwd", s);

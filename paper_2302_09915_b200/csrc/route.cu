@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(kPermWarps * 32) route_permute_kernel(RouteDim
   const int e = lo;
   const int j = r - start[e];
   const int dst_rank = map.rank_of(e);
-  const long long drow = map.row(r, dst_rank);
+  const long long drow = map.P == 1 ? r : static_cast<long long>(r) - start[e] + map.dst_off[e];
   uint4* dst = reinterpret_cast<uint4*>(xp.p[dst_rank] + drow * dx);
   const int nv = dx / 8;
   if (j < cnt[e]) {

@@ -12,14 +12,15 @@ constexpr int kMaxTopK = 8;
 constexpr int kMaxRanks = 16;
 
 // Maps a row of this rank's padded expert-major layout to the row it occupies in the owner rank's receive
-// layout (expert parallelism over peer memory).  P == 1: identity (everything local).
+// layout (expert parallelism over peer memory).  The owner's layout is expert-major too: for each of its
+// experts, one 16-row-padded segment per source rank in rank order.  P == 1: identity (everything local).
 struct RowMap {
-  int P = 1, E = 1;                // ranks, experts per rank
-  const int* send_off = nullptr;   // [P] start of this rank's block for destination j in its own layout
-  const int* dst_base = nullptr;   // [P] start of this rank's block inside rank j's receive layout
+  int P = 1, E = 1;                  // ranks, experts per rank
+  const int* local_start = nullptr;  // [N] segment start of expert e in this rank's padded layout
+  const int* dst_off = nullptr;      // [N] start of this rank's segment for expert e at the owner
   __device__ __forceinline__ int rank_of(int expert) const { return P == 1 ? 0 : expert / E; }
-  __device__ __forceinline__ long long row(int local_row, int j) const {
-    return P == 1 ? local_row : static_cast<long long>(local_row) - send_off[j] + dst_base[j];
+  __device__ __forceinline__ long long row(int local_row, int expert) const {
+    return P == 1 ? local_row : static_cast<long long>(local_row) - local_start[expert] + dst_off[expert];
   }
 };
 

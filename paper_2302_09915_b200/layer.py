@@ -47,7 +47,7 @@ _lib.lib.tamoe_nccl_unique_id.argtypes = [ctypes.c_void_p]
 _lib.lib.tamoe_layer_a2a_bytes.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_longlong)]
 _lib.lib.tamoe_ep_plan.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_longlong),
                                    ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
-                                   ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_longlong)]
+                                   ctypes.POINTER(ctypes.c_longlong)]
 _lib.lib.tamoe_layer_launches_per_step.argtypes = [ctypes.c_void_p]
 _lib.lib.tamoe_layer_enable_timing.argtypes = [ctypes.c_void_p, ctypes.c_int]
 _lib.lib.tamoe_layer_timing.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_char_p),
@@ -100,20 +100,18 @@ def nccl_unique_id() -> bytes:
 
 
 def ep_plan(recv):
-    """Receive plan for recv[P, E] rows per (source rank, local expert): 16-row padded (source, expert)
-    segments seg_start/seg_rows [P, E] and per-source block offsets / rows [P] -- the C++ host logic of
-    the expert-parallel exchange (one NCCL send/recv pair per peer)."""
+    """Receive plan for recv[P, E] rows per (source rank, local expert): the segment of each local expert
+    (seg_start, seg_rows [E]; expert-major, one 16-row padded block per source in rank order) and where each
+    source's rows for it start (src_off [P, E]) -- the host twin of the device plan kernel."""
     r = np.ascontiguousarray(recv, np.int64)
     P, E = r.shape
-    st = np.zeros(P * E, np.int32)
-    rows = np.zeros(P * E, np.int32)
-    off = np.zeros(P, np.int64)
-    blk = np.zeros(P, np.int64)
+    st = np.zeros(E, np.int32)
+    rows = np.zeros(E, np.int32)
+    off = np.zeros(P * E, np.int64)
     LL = ctypes.POINTER(ctypes.c_longlong)
     _lib.check(_lib.lib.tamoe_ep_plan(P, E, r.ctypes.data_as(LL), st.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
-                                      rows.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), off.ctypes.data_as(LL),
-                                      blk.ctypes.data_as(LL)))
-    return st.reshape(P, E), rows.reshape(P, E), off, blk
+                                      rows.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), off.ctypes.data_as(LL)))
+    return st, rows, off.reshape(P, E)
 
 
 class TAMoELayer:

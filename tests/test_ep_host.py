@@ -1,11 +1,11 @@
 """Expert-parallel host logic on the CPU with world_size-2/4 gloo process groups.
 
 Each rank routes its own process' tokens (oracle topk_route over all processes -- the
-reference's multi-process semantics), packs its kept picks in (expert, token) order,
-exchanges counts and payload rows with all_to_all, and lays the received rows out with
-the library's C++ receive plan (tamoe_ep_plan).  The resulting expert-major layout must
-equal the reference bucket order: per expert, ascending (process, token) -- the order
-the device kernels and the NCCL exchange reproduce on the GPU."""
+reference's multi-process semantics), packs its kept picks in (expert, token) order with
+16-row padded expert segments, exchanges counts and payload rows (gloo all_to_all stands in
+for the NVLink peer stores), and places every source's rows at the offsets of the library's
+C++ receive plan (tamoe_ep_plan, the host twin of the device plan kernel).  Each local expert's
+receive segment must hold the reference bucket order: ascending (process, token)."""
 import os
 import socket
 
@@ -57,30 +57,34 @@ def _worker(rank, world, port, mode, k, errq):
         recv = torch.zeros(world * E, dtype=torch.int64)
         dist.all_to_all_single(recv, torch.tensor(send_counts, dtype=torch.int64))
         recv = recv.numpy().reshape(world, E)
-        seg_start, seg_rows, blk_off, blk_rows = ep_plan(recv)
-        # payload all-to-all: one block per peer, landing at the plan's block offsets
+        seg_start, seg_rows, src_off = ep_plan(recv)
+        # payload all-to-all (one block per peer: the sender's padded segments of the peer's experts)
         in_split = [len(b) for b in blocks]
-        out_split = [int(x) for x in blk_rows]
+        out_split = [int(sum((c + 15) // 16 * 16 for c in recv[i])) for i in range(world)]
         got = torch.empty(sum(out_split), dtype=torch.int64)
         dist.all_to_all_single(got, payload, output_split_sizes=out_split, input_split_sizes=in_split)
         got = got.numpy()
-        assert list(blk_off) == list(np.concatenate([[0], np.cumsum(out_split)[:-1]]))
-        # every (source, expert) segment: that process' picks in token order, then zero-padding rows;
-        # reading the segments of expert e in source order gives the reference bucket order
+        layout = np.full(int(seg_start[-1] + seg_rows[-1]), -2, np.int64)
+        o = 0
+        for i in range(world):
+            for e in range(E):
+                rows = (recv[i, e] + 15) // 16 * 16
+                layout[src_off[i, e]:src_off[i, e] + rows] = got[o:o + rows]
+                o += rows
+        assert np.all(layout != -2)  # the plan tiles the receive buffer exactly
+        # each local expert: per source, its picks in token order then padding; in source order this is the
+        # reference bucket order (process, token)
         for e in range(E):
             ge = rank * E + e
-            order = []
-            for i in range(world):
-                exp_i = [i * 100000 + s * k + j for s in range(S) for j in range(k)
-                         if r["kept"][i, s, j] and r["expert"][i, s, j] == ge]
-                seg = got[seg_start[i, e]:seg_start[i, e] + seg_rows[i, e]]
-                assert seg_rows[i, e] % 16 == 0
-                assert list(seg[:len(exp_i)]) == exp_i, (rank, i, e)
-                assert np.all(seg[len(exp_i):] == -1)
-                order += list(seg[:len(exp_i)])
+            seg = layout[seg_start[e]:seg_start[e] + seg_rows[e]]
+            order = [v for v in seg if v >= 0]
             ref = [i * 100000 + s * k + j for i in range(world) for s in range(S) for j in range(k)
                    if r["kept"][i, s, j] and r["expert"][i, s, j] == ge]
-            assert order == ref
+            assert order == ref, (rank, e)
+            for i in range(world):
+                c = recv[i, e]
+                blk = layout[src_off[i, e]:src_off[i, e] + (c + 15) // 16 * 16]
+                assert np.all(blk[c:] == -1) and np.all(blk[:c] >= 0)
         dist.barrier()
         dist.destroy_process_group()
     except Exception as ex:  # noqa: BLE001
