@@ -18,7 +18,6 @@ struct CombineArgs {
   __nv_bfloat16* y_hat;          // optional [T x dout]
   PeerBufs dO;                   // gradient w.r.t. expert outputs, written into the owner's receive layout
   RowMap map;
-  int o_local;                   // 1: expert outputs already in this rank's own layout (row = pos)
   float* dldg;                   // [T*k]
   double* loss_part;             // [combine_blocks(T)] sum of squared residuals per block
 };

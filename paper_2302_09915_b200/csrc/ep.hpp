@@ -29,19 +29,11 @@ struct EpPlanDev {
   int* seg_start = nullptr;   // [E] receive segment of each local expert
   int* seg_rows = nullptr;    // [E]
   int* dst_off = nullptr;     // [N] where this rank's rows for global expert e start at the owner
-  int* src_off = nullptr;     // [P x E] where source i's rows for local expert e start in this rank's layout
-  int* all_lstart = nullptr;  // [P x N] start of expert e in rank i's own padded layout
   int* recv_rows = nullptr;   // [1]
   int* flag = nullptr;        // [1] barrier scratch
 };
 
 void ep_plan_device(const EpPlanDev& plan, int P, int E, int me, cudaStream_t s);
-
-// Owner -> source push of rows of the receive layout (width w) back into every source's own padded
-// layout (dst.p[i] = source i's buffer, peer-mapped): expert outputs after the forward, input
-// gradients after the backward.  Local reads, NVLink stores.
-void ep_push_back(const EpPlanDev& plan, int P, int E, int me, const __nv_bfloat16* src, const PeerBufs& dst, int w,
-                  int r_max, cudaStream_t s);
 
 class EpComm {
  public:

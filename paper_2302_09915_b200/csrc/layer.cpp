@@ -172,10 +172,6 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
     arena_.reserve(plan_.seg_start, E);
     arena_.reserve(plan_.seg_rows, E);
     arena_.reserve(plan_.dst_off, c.N);
-    arena_.reserve(plan_.src_off, static_cast<long long>(W) * E);
-    arena_.reserve(plan_.all_lstart, static_cast<long long>(W) * c.N);
-    arena_.reserve(o_back_, static_cast<long long>(r_local_) * c.d_out);
-    if (c.need_dx) arena_.reserve(dx_back_, static_cast<long long>(r_local_) * c.d);
     arena_.reserve(plan_.recv_rows, 1);
     arena_.reserve(plan_.flag, 1);
   }
@@ -348,20 +344,17 @@ void Layer::step_ep(const LayerIO& io, cudaStream_t s) {
   ep_->barrier(plan_.flag, s);
   tm.mark("a2a_dispatch", s);
   experts_forward(io, E, E, 1, plan_.seg_start, plan_.seg_rows, r_max_, s);
-  // combine all-to-all: owners push expert outputs back into every source's own layout
-  ep_push_back(plan_, W, E, c.rank, O_, peers(o_back_), c.d_out, r_max_, s);
   ep_->barrier(plan_.flag, s);
-  tm.mark("a2a_combine", s);
-  combine(io, s);  // local expert outputs; dO stored into the owners
+  tm.mark("a2a_barrier_fwd", s);
+  combine(io, s);  // loads expert outputs from the owners, stores dO into the owners
   ep_->barrier(plan_.flag, s);
-  tm.mark("a2a_dispatch_grad", s);
+  tm.mark("a2a_barrier_combine", s);
   experts_backward(io, E, E, 1, plan_.seg_start, plan_.seg_rows, r_max_, s);
   if (c.need_dx) {
-    ep_push_back(plan_, W, E, c.rank, dxp_, peers(dx_back_), c.d, r_max_, s);
     ep_->barrier(plan_.flag, s);
-    tm.mark("a2a_combine_grad", s);
+    tm.mark("a2a_barrier_bwd", s);
   }
-  gate_backward(io, s);
+  gate_backward(io, s);  // the dX epilogue loads the expert-path gradients from the owners
   tm.end(s);
 }
 
@@ -376,13 +369,7 @@ void Layer::combine(const LayerIO& io, cudaStream_t s) {
   ca.pos = b.pos;
   ca.idx = b.idx;
   ca.gate = b.gate;
-  if (ep_) {  // expert outputs were pushed back into this rank's own layout
-    ca.O = PeerBufs{};
-    for (int j = 0; j < c.world_size; ++j) ca.O.p[j] = o_back_;
-    ca.o_local = 1;
-  } else {
-    ca.O = peers(O_);
-  }
+  ca.O = peers(O_);
   ca.y = io.y;
   ca.y_hat = io.y_hat;
   ca.dO = peers(dO_);
@@ -423,16 +410,14 @@ void Layer::gate_backward(const LayerIO& io, cudaStream_t s) {
   gate_dw(io.x, dz_, c.P, c.S, c.d, n64_, n_pad_, c.N, dw_part_, dw_splits_, io.dwg, s);
   tm.mark("gate_dw", s);
   if (c.need_dx) {
-    PeerBufs dxb{};
-    dxb.p[0] = ep_ ? dx_back_ : dxp_;
-    gate_dx(dz_, io.wg, c.P, c.S, c.d, n64_, n_pad_, dxb, b.pos, b.idx, RowMap{}, c.k, io.dx, s);
+    gate_dx(dz_, io.wg, c.P, c.S, c.d, n64_, n_pad_, peers(dxp_), b.pos, b.idx, map_, c.k, io.dx, s);
     tm.mark("gate_dx", s);
   }
 }
 
 int Layer::launches_per_step() const {
   // gate, scan, bucket, capacity, permute, combine, dz, dW GEMM + reduce
-  int n = 9 + (ep_ ? (2 + (cfg_.need_dx ? 1 : 0)) : 0);  // + plan, push O, push dX
+  int n = 9 + (ep_ ? 1 : 0);  // + the device plan kernel
   n += cfg_.f == 0 ? (1 + 1 + (cfg_.need_dx ? 1 : 0)) : (2 + 3 + (cfg_.need_dx ? 1 : 0));
   if (cfg_.need_dx) n += 1;
   return n;

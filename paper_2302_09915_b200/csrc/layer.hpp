@@ -144,7 +144,6 @@ class Layer {
   std::vector<char*> bases_;
   RowMap map_{};
   int r_local_ = 0;  // rows of this rank's own padded layout
-  __nv_bfloat16 *o_back_ = nullptr, *dx_back_ = nullptr;  // pushed back by the owners, local layout
   int n_pad_ = 0, n64_ = 0, r_max_ = 0, dw_splits_ = 1, P_global_ = 1;
   // activations (expert order, padded segments)
   __nv_bfloat16 *xp_ = nullptr, *O_ = nullptr, *dO_ = nullptr, *H_ = nullptr, *A_ = nullptr, *dA_ = nullptr,
