@@ -34,6 +34,22 @@ __device__ __forceinline__ float act_fwd(int act, float x) {
   return x;
 }
 
+// act(x) and act'(x) from one tanh
+__device__ __forceinline__ void act_both(int act, float x, float& y, float& dy) {
+  if (act == kActGelu) {
+    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+    const float t = ptx::tanh_fast(k0 * (x + k1 * x * x * x));
+    y = 0.5f * x * (1.f + t);
+    dy = 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
+  } else if (act == kActRelu) {
+    y = x > 0.f ? x : 0.f;
+    dy = x > 0.f ? 1.f : 0.f;
+  } else {
+    y = x;
+    dy = 1.f;
+  }
+}
+
 __device__ __forceinline__ float act_grad(int act, float x) {
   if (act == kActGelu) {
     const float k0 = 0.7978845608028654f, k1 = 0.044715f;
@@ -59,7 +75,8 @@ struct SwapParams {
   int act_grad;  // activation derivative multiplied in (dgrad)
 };
 
-// V = 0: plain store; 1: also store the pre-activation; 2: multiply act'(pre_in).
+// V = 0: plain store; 1: store act(x) and the activation derivative act'(x) (kept for the backward in
+// place of the pre-activation); 2: multiply by the stored act'(x).
 template <int V>
 struct EpiSwap {
   static constexpr int kChunk = 2048;  // 32 x 32 bf16
@@ -117,10 +134,17 @@ struct EpiSwap {
       __nv_bfloat16* sx = extra + (j & 1) * 1024;
 #pragma unroll
       for (int c = 0; c < 32; ++c) {
-        float x = v[c];
-        if constexpr (V == 2) x *= act_grad(e.act_grad, __bfloat162float(sx[c * 32 + lane]));
-        if constexpr (V == 1) sx[c * 32 + lane] = __float2bfloat16(x);
-        so[c * 32 + lane] = __float2bfloat16(act_fwd(e.act_out, x));
+        const float x = v[c];
+        if constexpr (V == 1) {
+          float y, dy;
+          act_both(e.act_out, x, y, dy);
+          sx[c * 32 + lane] = __float2bfloat16(dy);
+          so[c * 32 + lane] = __float2bfloat16(y);
+        } else if constexpr (V == 2) {
+          so[c * 32 + lane] = __float2bfloat16(x * __bfloat162float(sx[c * 32 + lane]));
+        } else {
+          so[c * 32 + lane] = __float2bfloat16(act_fwd(e.act_out, x));
+        }
       }
       ptx::fence_proxy_async_smem();
       __syncwarp();

@@ -7,12 +7,13 @@ namespace tamoe {
 enum ActKind : int { kActNone = 0, kActGelu = 1, kActRelu = 2 };
 
 // out[R x M] = act(tokens[seg_g] . W_g^T), W_g = w[g] stored M x K. pre_out (optional) keeps the
-// pre-activation for the backward pass.
+// activation derivative act'(pre-activation) for the backward pass.
 void grouped_fwd(const __nv_bfloat16* tokens, const __nv_bfloat16* w, int G, int M, int K, int R,
                  const int* seg_start, const int* seg_rows, __nv_bfloat16* out, __nv_bfloat16* pre_out, int act,
                  cudaStream_t s, int w_mod = 0);
 
-// out[R x M] = (grad_tokens[seg_g] . W_g) * act'(pre_in), W_g = w[g] stored K x M.
+// out[R x M] = (grad_tokens[seg_g] . W_g) * pre_in, W_g = w[g] stored K x M, pre_in = the act'(pre-activation)
+// stored by grouped_fwd (or null).
 void grouped_dgrad(const __nv_bfloat16* grad_tokens, const __nv_bfloat16* w, int G, int M, int K, int R,
                    const int* seg_start, const int* seg_rows, __nv_bfloat16* out, const __nv_bfloat16* pre_in,
                    int act, cudaStream_t s, int w_mod = 0);

@@ -146,6 +146,7 @@ class Layer {
   int r_local_ = 0;  // rows of this rank's own padded layout
   int n_pad_ = 0, n64_ = 0, r_max_ = 0, dw_splits_ = 1, P_global_ = 1;
   // activations (expert order, padded segments)
+  // A_ keeps act'(pre-activation) from the forward (all the backward needs of the pre-activation)
   __nv_bfloat16 *xp_ = nullptr, *O_ = nullptr, *dO_ = nullptr, *H_ = nullptr, *A_ = nullptr, *dA_ = nullptr,
                 *dxp_ = nullptr, *dz_ = nullptr;
   float *logits_ = nullptr, *dldg_ = nullptr, *dw_part_ = nullptr;

@@ -42,7 +42,9 @@ def test_grouped_fwd(dev, counts, M, K):
     for g in range(G):
         s, r = start[g], rows[g]
         ref = x[s:s + r].float() @ w[g].float().t()
-        assert _rel(pre[s:s + r], ref) < 1e-2, g
+        refd = ref.clone().requires_grad_(True)
+        torch.nn.functional.gelu(refd, approximate="tanh").sum().backward()
+        assert _rel(pre[s:s + r], refd.grad) < 1e-2, g   # stored gelu'(pre-activation)
         assert _rel(out[s:s + r], torch.nn.functional.gelu(ref, approximate="tanh")) < 1e-2, g
 
 
@@ -54,14 +56,14 @@ def test_grouped_dgrad(dev, counts, M, K):
     ss, sr, start, rows, R = _segments(counts, dev)
     dy = _tokens(counts, start, R, K, dev, 2)
     w = (torch.randn(G, K, M, device=dev) / K ** 0.5).to(torch.bfloat16)  # stored K x M
-    pre = torch.randn(R, M, device=dev).to(torch.bfloat16)
+    deriv = torch.randn(R, M, device=dev).to(torch.bfloat16)  # act'(pre-activation) as grouped_fwd stores it
     out = torch.full((R, M), float("nan"), dtype=torch.bfloat16, device=dev)
     _lib.call("tamoe_grouped_dgrad", dy.data_ptr(), w.data_ptr(), G, M, K, R, ss.data_ptr(), sr.data_ptr(),
-              out.data_ptr(), pre.data_ptr(), 2, torch.cuda.current_stream().cuda_stream)
+              out.data_ptr(), deriv.data_ptr(), 2, torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     for g in range(G):
         s, r = start[g], rows[g]
-        ref = (dy[s:s + r].float() @ w[g].float()) * (pre[s:s + r].float() > 0).float()
+        ref = (dy[s:s + r].float() @ w[g].float()) * deriv[s:s + r].float()
         assert _rel(out[s:s + r], ref) < 1e-2, g
 
 
