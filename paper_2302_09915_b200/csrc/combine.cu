@@ -38,7 +38,7 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
 // KT = compile-time top-k (0: runtime k <= kMaxTopK).  Each lane keeps kU 16-byte vectors of every
 // slot in flight before computing, so the warp has (k + 1) * kU * 512 B of loads outstanding.
 template <int KT>
-__global__ void __launch_bounds__(kCombWarps * 32) combine_loss_kernel(CombineArgs a) {
+__global__ void __launch_bounds__(kCombWarps * 32) combine_loss_kernel(const __grid_constant__ CombineArgs a) {
   constexpr int KM = KT > 0 ? KT : kMaxTopK;
   constexpr int kU = 4;
   __shared__ double wsum[kCombWarps];

@@ -82,6 +82,8 @@ struct EpiSwap {
   static constexpr int kChunk = 2048;  // 32 x 32 bf16
   static constexpr int kPf = 2;        // own chunks of pre_in in flight
   static constexpr int kWarpBytes = V == 0 ? 2 * kChunk : 4 * kChunk;
+  static constexpr bool kEarlyRelease = true;
+  static constexpr int kMaxCh = 4;  // a warp's chunks per tile: every other 32-column chunk of N <= 256
   using Params = SwapParams;
   static __device__ __forceinline__ void load_chunk(const Params& e, const TileInfo& ti, int row0, int mcol, int ch,
                                                     __nv_bfloat16* slot, int lane) {
@@ -108,9 +110,24 @@ struct EpiSwap {
       for (int j = 0; j < kPf; ++j) load_chunk(e, ti, row0, mcol, h + 2 * j, ring + j * 1024, lane);
     }
   }
+  template <class Release>
   static __device__ __forceinline__ void run(const Params& e, const GemmParams&, const TileInfo& ti,
                                              uint32_t tmem_tile, int q, int h, int lane, uint8_t* wsm,
-                                             const int* s_start) {
+                                             const int* s_start, Release&& release) {
+    // copy this warp's share of the accumulator to registers and hand TMEM back to the MMA at once
+    const int nch_all = (ti.n + 31) / 32;
+    float acc[kMaxCh][32];
+#pragma unroll
+    for (int j = 0; j < kMaxCh; ++j) {
+      if (h + 2 * j < nch_all) {
+        uint32_t r[32];
+        ptx::tmem_ld_32x32b_x32(tmem_tile + (h + 2 * j) * 32, r);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[j][i] = __uint_as_float(r[i]);
+      }
+    }
+    ptx::tmem_ld_wait();
+    release();
     __nv_bfloat16* st_out = reinterpret_cast<__nv_bfloat16*>(wsm);
     __nv_bfloat16* extra = reinterpret_cast<__nv_bfloat16*>(wsm + 2 * kChunk);  // pre_out staging | pre_in ring
     const int mcol = ti.m0 + q * 32;
@@ -118,14 +135,15 @@ struct EpiSwap {
     const int nch = (ti.n + 31) / 32;
     if (lane == 0) ptx::bulk_wait_read<0>();  // staging tiles free again
     __syncwarp();
-    int j = 0;
-    for (int ch = h; ch < nch; ch += 2, ++j) {
+#pragma unroll
+    for (int j = 0; j < kMaxCh; ++j) {
+      const int ch = h + 2 * j;
+      if (ch >= nch) break;
       if constexpr (V == 2) {
         ptx::cp_async_wait<kPf - 1>();
         __syncwarp();
       }
-      float v[32];
-      load_acc32(tmem_tile, ch * 32, v);
+      const float* v = acc[j];
       if (j >= 2) {
         if (lane == 0) ptx::bulk_wait_read<1>();
         __syncwarp();
@@ -172,26 +190,42 @@ struct EpiSwap {
 // one bulk store.
 struct EpiWgrad {
   static constexpr int kWarpBytes = 2 * 2048;
+  static constexpr bool kEarlyRelease = true;
   struct Params {
     CUtensorMap out;  // [G*Mw x Nw], box {32, 32}, 64B swizzle
   };
   static __device__ __forceinline__ void prefetch(const Params&, const GemmParams&, const TileInfo&, int, int, int,
                                                   uint8_t*, const int*) {}
+  template <class Release>
   static __device__ __forceinline__ void run(const Params& e, const GemmParams& p, const TileInfo& ti,
-                                             uint32_t tmem_tile, int q, int h, int lane, uint8_t* wsm, const int*) {
+                                             uint32_t tmem_tile, int q, int h, int lane, uint8_t* wsm, const int*,
+                                             Release&& release) {
+    // BN = 256: four 32-column chunks per warp, copied out of TMEM before any math / store
+    float acc[4][32];
+    if (ti.k_len > 0) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t r[32];
+        ptx::tmem_ld_32x32b_x32(tmem_tile + 32 * h + 64 * j, r);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[j][i] = __uint_as_float(r[i]);
+      }
+      ptx::tmem_ld_wait();
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[j][i] = 0.f;
+    }
+    release();
     if (lane == 0) ptx::bulk_wait_read<0>();
     __syncwarp();
     const int row = ti.g * p.Mw + ti.m0 + q * 32;
     const int sw = (lane >> 1) & 3;
-    int j = 0;
-    for (int c0 = 32 * h; c0 < ti.n; c0 += 64, ++j) {
-      float v[32];
-      if (ti.k_len > 0) {
-        load_acc32(tmem_tile, c0, v);
-      } else {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = 0.f;
-      }
+    for (int j = 0; j < 4; ++j) {
+      const int c0 = 32 * h + 64 * j;
+      const float* v = acc[j];
       if (j >= 2) {
         if (lane == 0) ptx::bulk_wait_read<1>();
         __syncwarp();

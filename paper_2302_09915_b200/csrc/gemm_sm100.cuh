@@ -62,6 +62,17 @@ struct TileInfo {
 };
 
 // Epilogues may declare `static constexpr int kWarpBytes` of scratch shared memory per epilogue warp.
+// Epilogues that declare `static constexpr bool kEarlyRelease = true` free the TMEM accumulator
+// themselves (right after copying it to registers) through the `release` callback.
+template <class Epi, class = void>
+struct EpiEarly {
+  static constexpr bool value = false;
+};
+template <class Epi>
+struct EpiEarly<Epi, decltype(void(Epi::kEarlyRelease))> {
+  static constexpr bool value = Epi::kEarlyRelease;
+};
+
 template <class Epi, class = void>
 struct EpiSmem {
   static constexpr int warp = 0;
@@ -455,12 +466,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       ptx::mbar_wait(&tfull_bar[buf], use & 1);
       ptx::tc_fence_after();
       const uint32_t tmem_tile = tmem_base + buf * BN + (static_cast<uint32_t>(q * 32) << 16);
-      Epi::run(ep, p, ti, tmem_tile, q, h, lane, wsm, s_start);
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (kCG == 2) ptx::mbar_arrive_remote(ptx::mapa(&tempty_bar[buf], 0));
-        else ptx::mbar_arrive(&tempty_bar[buf]);
+      auto release = [&]() {
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (kCG == 2) ptx::mbar_arrive_remote(ptx::mapa(&tempty_bar[buf], 0));
+          else ptx::mbar_arrive(&tempty_bar[buf]);
+        }
+      };
+      if constexpr (EpiEarly<Epi>::value) {
+        Epi::run(ep, p, ti, tmem_tile, q, h, lane, wsm, s_start, release);
+      } else {
+        Epi::run(ep, p, ti, tmem_tile, q, h, lane, wsm, s_start);
+        release();
       }
     }
     Epi::finish(ep, lane);

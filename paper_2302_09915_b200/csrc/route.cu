@@ -301,7 +301,8 @@ constexpr int kPermWarps = 8;
 
 __global__ void __launch_bounds__(kPermWarps * 32) route_permute_kernel(RouteDims d, RouteBuffers b,
                                                                         const __nv_bfloat16* __restrict__ x, int dx,
-                                                                        PeerBufs xp, int r_max, PeerBufs zrows,
+                                                                        const __grid_constant__ PeerBufs xp, int r_max,
+                                                                        const __grid_constant__ PeerBufs zrows,
                                                                         int has_z, int zdim, RowMap map) {
   extern __shared__ int sm[];
   const int N = d.N;
