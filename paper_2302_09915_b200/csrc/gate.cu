@@ -22,25 +22,42 @@ struct GateEpiParams {
   int N, k, S, TB;
 };
 
+// The two epilogue warps of a TMEM lane quarter (h = 0, 1) split each token row's experts: warp h owns
+// 32-column chunks [h*C0, min(C, (h+1)*C0)).  Row max, the softmax denominator (sum of the two halves'
+// sequential partial sums) and the top-k lists are exchanged through shared memory under a named barrier
+// per lane quarter; warp h = 0 merges the lists (its experts have the lower indices, so ties keep it).
 template <int KM>
 struct EpiGate {
   using Params = GateEpiParams;
+  struct Xchg {
+    float mx[2][32];
+    int fin[2][32];
+    double sum[2][32];
+    double tp[32][KM];
+    int te[32][KM];
+  };
+  static constexpr int kWarpBytes = ((static_cast<int>(sizeof(Xchg)) + 127) / 128) * 128;
   static __device__ __forceinline__ void finish(const Params&, int) {}
   static __device__ __forceinline__ void prefetch(const Params&, const GemmParams&, const TileInfo&, int, int, int,
                                                   uint8_t*, const int*) {}
   static __device__ __forceinline__ void run(const Params& e, const GemmParams& p, const TileInfo& ti,
-                                             uint32_t tmem_tile, int q, int h, int lane, uint8_t*, const int*) {
-    if (h != 0) return;  // the softmax needs whole rows: one warp per lane quarter
+                                             uint32_t tmem_tile, int q, int h, int lane, uint8_t* wsm, const int*) {
+    // the lane quarter's exchange area lives in warp q's (h = 0) scratch
+    Xchg& X = *reinterpret_cast<Xchg*>(h == 0 ? wsm : wsm - 4 * kWarpBytes);
+    const uint32_t bar_id = 1 + q;
     const int row = q * 32 + lane;
     const int tok = ti.m0 + row;
     const bool valid = tok < e.S;
     const long long gtok = static_cast<long long>(ti.g) * e.S + tok;
     const int tile_warp = (ti.g * e.TB + ti.m0 / kBM) * 4 + q;
     const int N = e.N;
-    // pass 1: max (and the non-finite check of gate.cpp:16)
+    const int C = (N + 31) / 32, C0 = (C + 1) / 2;
+    const int cb = h == 0 ? 0 : C0, ce = h == 0 ? C0 : C;
+    // pass 1: max over my columns (and the non-finite check of gate.cpp:16); logits out
     float mx = -INFINITY;
     bool finite = true;
-    for (int c0 = 0; c0 < N; c0 += 32) {
+    for (int ch = cb; ch < ce; ++ch) {
+      const int c0 = ch * 32;
       float v[32];
       load_acc32(tmem_tile, c0, v);
 #pragma unroll
@@ -48,26 +65,46 @@ struct EpiGate {
         if (c0 + c < N) {
           finite &= isfinite(v[c]);
           mx = fmaxf(mx, v[c]);
-          if (valid && e.o.logits) e.o.logits[gtok * N + c0 + c] = v[c];
+        }
+      }
+      if (valid && e.o.logits) {
+        float* dst = e.o.logits + gtok * N + c0;
+        if (c0 + 32 <= N && (N % 4) == 0) {
+#pragma unroll
+          for (int c = 0; c < 32; c += 4) *reinterpret_cast<float4*>(dst + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if (c0 + c < N) dst[c] = v[c];
         }
       }
     }
-    if (valid && !finite) atomicOr(e.o.bad, 1);
+    X.mx[h][lane] = mx;
+    X.fin[h][lane] = finite ? 1 : 0;
+    ptx::named_bar_sync(bar_id, 64);
+    mx = fmaxf(X.mx[0][lane], X.mx[1][lane]);
+    finite = X.fin[0][lane] && X.fin[1][lane];
+    if (h == 0 && valid && !finite) atomicOr(e.o.bad, 1);
     const double dmx = valid ? static_cast<double>(mx) : 0.0;
-    // pass 2: denominator, sequential in expert order
-    double denom = 0.0;
-    for (int c0 = 0; c0 < N; c0 += 32) {
+    // pass 2: my half of the denominator, sequential in expert order
+    double part = 0.0;
+    for (int ch = cb; ch < ce; ++ch) {
+      const int c0 = ch * 32;
       float v[32];
       load_acc32(tmem_tile, c0, v);
 #pragma unroll
       for (int c = 0; c < 32; ++c)
-        if (c0 + c < N) denom += valid ? exp(static_cast<double>(v[c]) - dmx) : 0.0;
+        if (c0 + c < N) part += valid ? exp(static_cast<double>(v[c]) - dmx) : 0.0;
     }
-    // pass 3: probabilities, top-k, probability sums
+    X.sum[h][lane] = part;
+    ptx::named_bar_sync(bar_id, 64);
+    const double denom = X.sum[0][lane] + X.sum[1][lane];
+    // pass 3: probabilities, my top-k, probability sums of my columns
     TopK<KM> tk;
     tk.init();
     double* msum = e.o.msum4 + static_cast<long long>(tile_warp) * N;
-    for (int c0 = 0; c0 < N; c0 += 32) {
+    for (int ch = cb; ch < ce; ++ch) {
+      const int c0 = ch * 32;
       float v[32];
       double pr[32];
       load_acc32(tmem_tile, c0, v);
@@ -82,7 +119,21 @@ struct EpiGate {
       const double colsum = warp_transpose_sum32(pr, lane);
       if (c0 + lane < N) msum[c0 + lane] = colsum;
     }
-    finish_row(tk, valid, gtok, e.k, N, tile_warp, e.o, lane);
+    if (h == 1) {
+#pragma unroll
+      for (int j = 0; j < KM; ++j) {
+        X.tp[lane][j] = tk.p[j];
+        X.te[lane][j] = tk.e[j];
+      }
+    }
+    ptx::named_bar_sync(bar_id, 64);
+    if (h == 0) {
+#pragma unroll
+      for (int j = 0; j < KM; ++j)
+        if (X.te[lane][j] >= 0) tk.insert(X.tp[lane][j], X.te[lane][j], e.k);
+      finish_row(tk, valid, gtok, e.k, N, tile_warp, e.o, lane);
+    }
+    ptx::named_bar_sync(bar_id, 64);  // exchange area free for the next tile
   }
 };
 

@@ -24,7 +24,10 @@ namespace {
 constexpr int kDzWarps = 8;
 constexpr int kMaxNPerLane = 8;  // N <= 256
 
-__global__ void __launch_bounds__(kDzWarps * 32) gate_dz_kernel(GateDzArgs a) {
+// KT: compile-time top-k (0 = runtime k <= 8); NPL: experts per lane (N <= 32 * NPL).
+template <int KT, int NPL>
+__global__ void __launch_bounds__(kDzWarps * 32) gate_dz_kernel(const __grid_constant__ GateDzArgs a) {
+  constexpr int KM = KT > 0 ? KT : kMaxTopK;
   extern __shared__ double coeff[];  // [P*N]
   const int N = a.N;
   const double s2 = static_cast<double>(a.S) * a.S;
@@ -60,12 +63,12 @@ __global__ void __launch_bounds__(kDzWarps * 32) gate_dz_kernel(GateDzArgs a) {
   const long long t = static_cast<long long>(blockIdx.x) * kDzWarps + warp;
   if (t >= static_cast<long long>(a.P) * a.S) return;
   const int proc = static_cast<int>(t / a.S);
-  const int k = a.k;
+  const int k = KT > 0 ? KT : a.k;
   // softmax of the stored fp32 logits (fp32 math, max-subtracted)
-  float l[kMaxNPerLane], p[kMaxNPerLane], dpi[kMaxNPerLane];
+  float l[NPL], p[NPL], dpi[NPL];
   float mx = -INFINITY;
 #pragma unroll
-  for (int i = 0; i < kMaxNPerLane; ++i) {
+  for (int i = 0; i < NPL; ++i) {
     const int e = lane + 32 * i;
     l[i] = e < N ? a.logits[t * N + e] : -INFINITY;
     mx = fmaxf(mx, l[i]);
@@ -74,7 +77,7 @@ __global__ void __launch_bounds__(kDzWarps * 32) gate_dz_kernel(GateDzArgs a) {
   for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   float den = 0.f;
 #pragma unroll
-  for (int i = 0; i < kMaxNPerLane; ++i) {
+  for (int i = 0; i < NPL; ++i) {
     p[i] = (lane + 32 * i < N) ? expf(l[i] - mx) : 0.f;
     den += p[i];
   }
@@ -83,57 +86,70 @@ __global__ void __launch_bounds__(kDzWarps * 32) gate_dz_kernel(GateDzArgs a) {
   const float inv = 1.f / den;
   const float aux_scale = static_cast<float>(a.aux_weight / a.P_global);
 #pragma unroll
-  for (int i = 0; i < kMaxNPerLane; ++i) {
+  for (int i = 0; i < NPL; ++i) {
     const int e = lane + 32 * i;
     p[i] *= inv;
     dpi[i] = e < N ? aux_scale * static_cast<float>(coeff[proc * N + e]) : 0.f;
   }
   // combine-weight Jacobian (trainer.cpp:318-331)
-  int ex[kMaxTopK];
-  float add[kMaxTopK];
-  double mass = 0.0;
-#pragma unroll
-  for (int j = 0; j < kMaxTopK; ++j) {
-    ex[j] = j < k ? a.idx[t * k + j] : -1;
-    if (j < k) mass += a.score[t * k + j];
-  }
+  int ex[KM];
+  float add[KM];
   if (k == 1) {
+    ex[0] = a.idx[t];
     add[0] = a.dldg[t];
 #pragma unroll
-    for (int j = 1; j < kMaxTopK; ++j) add[j] = 0.f;
+    for (int j = 1; j < KM; ++j) {
+      ex[j] = -1;
+      add[j] = 0.f;
+    }
   } else {
+    double sc[KM], dg[KM];
+    double mass = 0.0;
 #pragma unroll
-    for (int l2 = 0; l2 < kMaxTopK; ++l2) {
+    for (int j = 0; j < KM; ++j) {
+      ex[j] = j < k ? a.idx[t * k + j] : -1;
+      sc[j] = j < k ? a.score[t * k + j] : 0.0;
+      dg[j] = j < k ? static_cast<double>(a.dldg[t * k + j]) : 0.0;
+      mass += sc[j];
+    }
+    const double inv2 = 1.0 / (mass * mass);
+#pragma unroll
+    for (int l2 = 0; l2 < KM; ++l2) {
       double acc = 0.0;
-      if (l2 < k) {
 #pragma unroll
-        for (int j = 0; j < kMaxTopK; ++j) {
-          if (j < k) {
-            const double dg = a.dldg[t * k + j];
-            if (dg != 0.0) acc += dg * ((j == l2 ? mass : 0.0) - a.score[t * k + j]) / (mass * mass);
-          }
-        }
-      }
+      for (int j = 0; j < KM; ++j)
+        if (dg[j] != 0.0) acc += dg[j] * ((j == l2 ? mass : 0.0) - sc[j]) * inv2;
       add[l2] = static_cast<float>(acc);
     }
   }
 #pragma unroll
-  for (int i = 0; i < kMaxNPerLane; ++i) {
+  for (int i = 0; i < NPL; ++i) {
     const int e = lane + 32 * i;
 #pragma unroll
-    for (int j = 0; j < kMaxTopK; ++j) dpi[i] += (ex[j] == e) ? add[j] : 0.f;
+    for (int j = 0; j < KM; ++j) dpi[i] += (ex[j] == e) ? add[j] : 0.f;
   }
   float dot = 0.f;
 #pragma unroll
-  for (int i = 0; i < kMaxNPerLane; ++i) dot += dpi[i] * p[i];
+  for (int i = 0; i < NPL; ++i) dot += dpi[i] * p[i];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
   __nv_bfloat16* dz = a.dz + t * a.n64;
 #pragma unroll
-  for (int i = 0; i < kMaxNPerLane; ++i) {
+  for (int i = 0; i < NPL; ++i) {
     const int e = lane + 32 * i;
     if (e < a.n64) dz[e] = __float2bfloat16(e < N ? p[i] * (dpi[i] - dot) : 0.f);
   }
+  // experts beyond 32 * NPL (n64 padding) are zero
+  for (int e = 32 * NPL + lane; e < a.n64; e += 32) dz[e] = __float2bfloat16(0.f);
+}
+
+template <int KT>
+void launch_dz(const GateDzArgs& a, int blocks, cudaStream_t s) {
+  const size_t smem = sizeof(double) * a.P * a.N;
+  if (a.N <= 32) gate_dz_kernel<KT, 1><<<blocks, kDzWarps * 32, smem, s>>>(a);
+  else if (a.N <= 64) gate_dz_kernel<KT, 2><<<blocks, kDzWarps * 32, smem, s>>>(a);
+  else if (a.N <= 128) gate_dz_kernel<KT, 4><<<blocks, kDzWarps * 32, smem, s>>>(a);
+  else gate_dz_kernel<KT, 8><<<blocks, kDzWarps * 32, smem, s>>>(a);
 }
 
 // dWg partials: acc[m = d index][n = expert] -> part[((ks * P + proc) * n64 + n) * d + m]
@@ -181,66 +197,96 @@ __global__ void dwg_reduce_kernel(const float* __restrict__ part, int splits, in
 }
 
 // dX: acc[token][d col] + gathered expert-path input gradients
+struct GateDxParams {
+  __nv_bfloat16* dx;
+  PeerBufs dxp;      // expert-path input gradients in every owner's receive layout
+  const int* pos;
+  const int* idx;
+  RowMap map;
+  int k, S, d;
+};
+
+// KT = compile-time top-k (0: runtime k).  The expert-path rows of every chunk this warp stores are
+// gathered into registers before the first accumulator load, so their latency overlaps.
+template <int KT>
 struct EpiGateDx {
-  struct Params {
-    __nv_bfloat16* dx;
-    PeerBufs dxp;      // expert-path input gradients in every owner's receive layout
-    const int* pos;
-    const int* idx;
-    RowMap map;
-    int k, S, d;
-  };
+  using Params = GateDxParams;
+  static constexpr int KM = KT > 0 ? KT : kMaxTopK;
   static __device__ __forceinline__ void finish(const Params&, int) {}
   static __device__ __forceinline__ void prefetch(const Params&, const GemmParams&, const TileInfo&, int, int, int,
                                                   uint8_t*, const int*) {}
+  static __device__ __forceinline__ void add8(float* v, const uint4& w) {
+    const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(hh[i]);
+      v[2 * i] += f.x;
+      v[2 * i + 1] += f.y;
+    }
+  }
   static __device__ __forceinline__ void run(const Params& e, const GemmParams& p, const TileInfo& ti,
                                              uint32_t tmem_tile, int q, int h, int lane, uint8_t*, const int*) {
     const int tok = ti.m0 + q * 32 + lane;
-    const bool valid = tok < e.S;  // tcgen05.ld is warp-collective: every lane runs the loop
+    const bool valid = tok < e.S;  // tcgen05.ld is warp-collective: every lane runs the loops
     const long long gtok = static_cast<long long>(ti.g) * e.S + tok;
-    int rows[kMaxTopK];
-    const __nv_bfloat16* srcs[kMaxTopK];
+    const int k = KT > 0 ? KT : e.k;
+    const __nv_bfloat16* srcs[KM];
 #pragma unroll
-    for (int j = 0; j < kMaxTopK; ++j) {
-      rows[j] = (valid && j < e.k) ? e.pos[gtok * e.k + j] : -1;
+    for (int j = 0; j < KM; ++j) {
       srcs[j] = nullptr;
-      if (rows[j] >= 0) {
-        const int ex = e.idx[gtok * e.k + j];
+      const int r = (valid && j < k) ? e.pos[gtok * k + j] : -1;
+      if (r >= 0) {
+        const int ex = e.idx[gtok * k + j];
         const int owner = e.map.rank_of(ex);
-        srcs[j] = e.dxp.p[owner] + e.map.row(rows[j], ex) * e.d;
+        srcs[j] = e.dxp.p[owner] + e.map.row(r, ex) * e.d;
       }
     }
-    for (int c0 = 32 * h; c0 < ti.n; c0 += 64) {
-      float v[32];
-      load_acc32(tmem_tile, c0, v);
-      const int col = ti.n0 + c0;
+    constexpr int kCh = 4;  // BN = 256: four 32-column chunks per warp (every other chunk)
+    if constexpr (KT > 0) {
+      uint4 g[KM][kCh][4];
 #pragma unroll
-      for (int j = 0; j < kMaxTopK; ++j) {
-        if (rows[j] >= 0) {
-          const uint4* src = reinterpret_cast<const uint4*>(srcs[j] + col);
+      for (int j = 0; j < KM; ++j)
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const uint4 w = src[u];
-            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+        for (int c = 0; c < kCh; ++c)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float2 f = __bfloat1622float2(h[i]);
-              v[8 * u + 2 * i] += f.x;
-              v[8 * u + 2 * i + 1] += f.y;
-            }
-          }
-        }
+          for (int u = 0; u < 4; ++u)
+            g[j][c][u] = srcs[j] ? reinterpret_cast<const uint4*>(srcs[j] + ti.n0 + 32 * h + 64 * c)[u]
+                                 : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int c = 0; c < kCh; ++c) {
+        const int c0 = 32 * h + 64 * c;
+        float v[32];
+        load_acc32(tmem_tile, c0, v);
+#pragma unroll
+        for (int j = 0; j < KM; ++j)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) add8(v + 8 * u, g[j][c][u]);
+        if (!valid) continue;
+        store32(e, gtok, ti.n0 + c0, v);
       }
-      if (!valid) continue;
-      uint4* dst = reinterpret_cast<uint4*>(e.dx + gtok * e.d + col);
+    } else {
+      for (int c0 = 32 * h; c0 < ti.n; c0 += 64) {
+        float v[32];
+        load_acc32(tmem_tile, c0, v);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        uint4 w;
-        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&w);
+        for (int j = 0; j < KM; ++j)
+          if (srcs[j])
 #pragma unroll
-        for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[8 * u + 2 * i], v[8 * u + 2 * i + 1]);
-        dst[u] = w;
+            for (int u = 0; u < 4; ++u) add8(v + 8 * u, reinterpret_cast<const uint4*>(srcs[j] + ti.n0 + c0)[u]);
+        if (!valid) continue;
+        store32(e, gtok, ti.n0 + c0, v);
       }
+    }
+  }
+  static __device__ __forceinline__ void store32(const Params& e, long long gtok, int col, const float* v) {
+    uint4* dst = reinterpret_cast<uint4*>(e.dx + gtok * e.d + col);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      uint4 w;
+      __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&w);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) hh[i] = __floats2bfloat162_rn(v[8 * u + 2 * i], v[8 * u + 2 * i + 1]);
+      dst[u] = w;
     }
   }
 };
@@ -252,7 +298,9 @@ void gate_dz(const GateDzArgs& a, cudaStream_t s) {
   require(a.k >= 1 && a.k <= kMaxTopK, "gate backward: k out of range");
   const long long T = static_cast<long long>(a.P) * a.S;
   const int blocks = static_cast<int>((T + kDzWarps - 1) / kDzWarps);
-  gate_dz_kernel<<<blocks, kDzWarps * 32, sizeof(double) * a.P * a.N, s>>>(a);
+  if (a.k == 1) launch_dz<1>(a, blocks, s);
+  else if (a.k == 2) launch_dz<2>(a, blocks, s);
+  else launch_dz<0>(a, blocks, s);
   TAMOE_CUDA(cudaGetLastError());
 }
 
@@ -301,8 +349,10 @@ void gate_dx(const __nv_bfloat16* dz, const __nv_bfloat16* wg, int P, int S, int
   CUtensorMap ta = make_tmap_bf16(dz, n64, T, n64, 128);                         // A = dz (K-major)
   CUtensorMap tb = make_tmap_bf16(wg, d, static_cast<uint64_t>(P) * n_pad, d, 64);  // B = Wg (MN-major)
   GemmParams p{1, nullptr, nullptr, 0, d, n_pad, 1, S, n_pad, P, 0, 1, 0, 0};
-  EpiGateDx::Params ep{dx, dxp, pos, idx, map, k, S, d};
-  launch_gemm<kModeGateDx, 256, false, true, EpiGateDx>(ta, tb, p, ep, 0, s);
+  GateDxParams ep{dx, dxp, pos, idx, map, k, S, d};
+  if (k == 1) launch_gemm<kModeGateDx, 256, false, true, EpiGateDx<1>>(ta, tb, p, ep, 0, s);
+  else if (k == 2) launch_gemm<kModeGateDx, 256, false, true, EpiGateDx<2>>(ta, tb, p, ep, 0, s);
+  else launch_gemm<kModeGateDx, 256, false, true, EpiGateDx<0>>(ta, tb, p, ep, 0, s);
 }
 
 }  // namespace tamoe
