@@ -16,9 +16,7 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
-import tempfile
 import threading
 import time
 
@@ -53,50 +51,65 @@ def peaks():
 
 # ------------------------------------------------------------------------------------------ clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clock + clock-event (throttle) reasons sampled DURING the timed region through NVML every ~1 ms
+    (nvidia-smi -lms needs ~1 s to produce its first line; a timed region is tens of ms).  The device is
+    matched to the CUDA ordinal by PCI bus id."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
 
-    def __init__(self, gpu_index):
-        self.gpu = gpu_index
-        self.proc = None
-        self.path = tempfile.mktemp(suffix=".csv")
+    def __init__(self, cuda_index, period_s=0.001):
+        self.idx = cuda_index
+        self.period = period_s
+        self.rows = []
+        self.err = None
+        self.h = None
+        self.nv = None
+        self.stop = threading.Event()
+        try:
+            import pynvml as nv
+            import torch
+            nv.nvmlInit()
+            self.nv = nv
+            try:
+                pr = torch.cuda.get_device_properties(cuda_index)
+                bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+                self.h = nv.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                self.h = nv.nvmlDeviceGetHandleByIndex(cuda_index)
+            self.max_sm = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        except Exception as e:  # no NVML: reported, not fatal
+            self.err = f"nvml unavailable: {e}"
+
+    def _sample(self):
+        nv = self.nv
+        reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self.stop.is_set():
+            try:
+                self.rows.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM), reasons(self.h)))
+            except Exception as e:
+                self.err = str(e)
+                return
+            time.sleep(self.period)
 
     def __enter__(self):
-        try:
-            self.f = open(self.path, "w")
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
-                                         stderr=subprocess.DEVNULL)
-        except Exception:
-            self.proc = None
+        if self.h is not None:
+            self.t = threading.Thread(target=self._sample, daemon=True)
+            self.t.start()
         return self
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
-            self.f.close()
+        if self.h is not None:
+            self.stop.set()
+            self.t.join(timeout=5)
 
     def summary(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        rows = []
-        with open(self.path) as f:
-            for line in f:
-                parts = [p.strip() for p in line.split(",")]
-                if len(parts) >= 7 and parts[0].replace(".", "").isdigit():
-                    rows.append(parts)
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        sm = [float(r[0]) for r in rows]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
-                "samples": len(rows)}
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.err or "no samples"]}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({n for _, m in self.rows for n, bit in self.REASONS.items() if m & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(self.max_sm), "reasons": reasons,
+                "samples": len(self.rows), "source": "nvml, 1 ms period, timed region only"}
 
 
 # ------------------------------------------------------------------------------------------ CPU baseline
@@ -253,6 +266,13 @@ def main():
         torch.cuda.synchronize()
     barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    clocks = clk.summary()
+    if world > 1:  # every rank sampled its own GPU: union of reasons, per-rank medians
+        allc = [None] * world
+        dist.all_gather_object(allc, clocks)
+        clocks = dict(clocks)
+        clocks["reasons"] = sorted({r for c in allc for r in c["reasons"]})
+        clocks["per_rank_sm_mhz"] = [c["sm_mhz"] for c in allc]
     phases, tsteps = layer.timing()
     layer.enable_timing(False)
     a2a = None
@@ -267,10 +287,11 @@ def main():
                "dispatch_ms": disp_ms, "combine_ms": comb_ms,
                "dispatch_bus_gbs": nbytes[0] / (disp_ms / 1e3) / 1e9 if disp_ms > 0 else 0.0,
                "combine_bus_gbs": (nbytes[1] + nbytes[2]) / (comb_ms / 1e3) / 1e9 if comb_ms > 0 else 0.0,
-               "peak_gbs": 900.0, "measured_peer_peak_gbs": 770.0,
+               "peak_gbs": 900.0, "measured_peer_peak_gbs": 690.0, "measured_a2a_gbs": 533.0,
                "note": "fused NVLink peer-memory dispatch (permute kernel stores into the owner's layout) and "
                        "combine (owner loads + dO stores); bus GB/s = off-rank bytes / phase time (CUDA events, "
-                       "incl. the stream-ordered NCCL barrier)"}
+                       "incl. the stream-ordered NCCL barrier); measured peaks: profiles/r01_p2p_bench.txt "
+                       "(single-pair SM pull 690 GB/s, 4-GPU all-to-all SM stores 533 GB/s per GPU)"}
     losses = layer.losses.cpu().tolist()
     value = world * S / (ms / 1e3)
 
@@ -361,7 +382,7 @@ def main():
                            "l2": "working set > L2 (1.07 GB expert weights + ~0.6 GB activations per step)"},
                 "roofline": roof, "all_to_all": a2a, "phases_ms": phases, "timed_steps_for_phases": tsteps,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": layer.launches_per_step() * args.steps,
-                "clocks": clk.summary(), "losses_last_step": losses}
+                "clocks": clocks, "losses_last_step": losses}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -179,7 +179,7 @@ int tamoe_router_route_gate(tamoe_router* r, const void* x, const void* wg, int 
     rw.upload_caps(caps, s);
     TAMOE_CUDA(cudaMemsetAsync(rw.buf.bad, 0, sizeof(int), s));
     gate_forward(static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(wg), n_pad, rw.dims, d,
-                 rw.row_out(logits, probs), s);
+                 rw.row_out(logits ? logits : rw.buf.logits, probs), s);
     check_bad(rw, s);
     rw.finish(mode, s);
   });

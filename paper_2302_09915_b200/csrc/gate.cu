@@ -1,8 +1,9 @@
-// Fused gate: logits = x . Wg^T on tcgen05 (TMA-staged, fp32 accumulate in
-// TMEM), then per token in the epilogue: fp64 softmax exactly as the reference
-// (max-subtract, exp, sequential sum over experts, divide: gate.cpp:12-28),
-// streaming top-k (gate.cpp:117-134), per-warp expert histograms and
-// probability partial sums for the aux loss (gate.cpp:115).
+// Gate: logits = x . Wg^T on tcgen05 (TMA-staged, fp32 accumulate in TMEM,
+// fp32 logits out of the epilogue), then a warp-per-8-tokens router: fp64
+// softmax exactly as the reference (max-subtract, exp, sequential sum over
+// experts, divide: gate.cpp:12-28), top-k (gate.cpp:117-134), per-group
+// expert histograms and probability partial sums for the aux loss
+// (gate.cpp:115).
 //
 // Replaces gate_forward (gate.cpp:30-32) + the per-token part of topk_route.
 #include <cuda_bf16.h>
@@ -18,124 +19,222 @@
 namespace tamoe {
 
 struct GateEpiParams {
-  RowRouteOut o;
-  int N, k, S, TB;
+  float* logits;  // [P*S x N] fp32
+  int N, S;
 };
 
-// The two epilogue warps of a TMEM lane quarter (h = 0, 1) split each token row's experts: warp h owns
-// 32-column chunks [h*C0, min(C, (h+1)*C0)).  Row max, the softmax denominator (sum of the two halves'
-// sequential partial sums) and the top-k lists are exchanged through shared memory under a named barrier
-// per lane quarter; warp h = 0 merges the lists (its experts have the lower indices, so ties keep it).
-template <int KM>
-struct EpiGate {
+// The gate GEMM's epilogue only materialises the fp32 logits (4 B x N per token, L2-resident for the router
+// that follows); the two warps of a TMEM lane quarter split the 32-column chunks.
+struct EpiLogits {
   using Params = GateEpiParams;
-  struct Xchg {
-    float mx[2][32];
-    int fin[2][32];
-    double sum[2][32];
-    double tp[32][KM];
-    int te[32][KM];
-  };
-  static constexpr int kWarpBytes = ((static_cast<int>(sizeof(Xchg)) + 127) / 128) * 128;
+  static constexpr bool kEarlyRelease = true;
   static __device__ __forceinline__ void finish(const Params&, int) {}
   static __device__ __forceinline__ void prefetch(const Params&, const GemmParams&, const TileInfo&, int, int, int,
                                                   uint8_t*, const int*) {}
-  static __device__ __forceinline__ void run(const Params& e, const GemmParams& p, const TileInfo& ti,
-                                             uint32_t tmem_tile, int q, int h, int lane, uint8_t* wsm, const int*) {
-    // the lane quarter's exchange area lives in warp q's (h = 0) scratch
-    Xchg& X = *reinterpret_cast<Xchg*>(h == 0 ? wsm : wsm - 4 * kWarpBytes);
-    const uint32_t bar_id = 1 + q;
-    const int row = q * 32 + lane;
-    const int tok = ti.m0 + row;
+  template <class Release>
+  static __device__ __forceinline__ void run(const Params& e, const GemmParams&, const TileInfo& ti,
+                                             uint32_t tmem_tile, int q, int h, int lane, uint8_t*, const int*,
+                                             Release&& release) {
+    const int tok = ti.m0 + q * 32 + lane;
     const bool valid = tok < e.S;
     const long long gtok = static_cast<long long>(ti.g) * e.S + tok;
-    const int tile_warp = (ti.g * e.TB + ti.m0 / kBM) * 4 + q;
     const int N = e.N;
     const int C = (N + 31) / 32, C0 = (C + 1) / 2;
     const int cb = h == 0 ? 0 : C0, ce = h == 0 ? C0 : C;
-    // pass 1: max over my columns (and the non-finite check of gate.cpp:16); logits out
-    float mx = -INFINITY;
-    bool finite = true;
     for (int ch = cb; ch < ce; ++ch) {
       const int c0 = ch * 32;
       float v[32];
       load_acc32(tmem_tile, c0, v);
+      if (ch + 1 == ce) release();
+      if (!valid) continue;
+      float* dst = e.logits + gtok * N + c0;
+      if (c0 + 32 <= N && (N % 4) == 0) {
 #pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        if (c0 + c < N) {
-          finite &= isfinite(v[c]);
-          mx = fmaxf(mx, v[c]);
-        }
-      }
-      if (valid && e.o.logits) {
-        float* dst = e.o.logits + gtok * N + c0;
-        if (c0 + 32 <= N && (N % 4) == 0) {
+        for (int c = 0; c < 32; c += 4) *reinterpret_cast<float4*>(dst + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+      } else {
 #pragma unroll
-          for (int c = 0; c < 32; c += 4) *reinterpret_cast<float4*>(dst + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
-        } else {
-#pragma unroll
-          for (int c = 0; c < 32; ++c)
-            if (c0 + c < N) dst[c] = v[c];
-        }
+        for (int c = 0; c < 32; ++c)
+          if (c0 + c < N) dst[c] = v[c];
       }
     }
-    X.mx[h][lane] = mx;
-    X.fin[h][lane] = finite ? 1 : 0;
-    ptx::named_bar_sync(bar_id, 64);
-    mx = fmaxf(X.mx[0][lane], X.mx[1][lane]);
-    finite = X.fin[0][lane] && X.fin[1][lane];
-    if (h == 0 && valid && !finite) atomicOr(e.o.bad, 1);
-    const double dmx = valid ? static_cast<double>(mx) : 0.0;
-    // pass 2: my half of the denominator, sequential in expert order
-    double part = 0.0;
-    for (int ch = cb; ch < ce; ++ch) {
-      const int c0 = ch * 32;
-      float v[32];
-      load_acc32(tmem_tile, c0, v);
-#pragma unroll
-      for (int c = 0; c < 32; ++c)
-        if (c0 + c < N) part += valid ? exp(static_cast<double>(v[c]) - dmx) : 0.0;
-    }
-    X.sum[h][lane] = part;
-    ptx::named_bar_sync(bar_id, 64);
-    const double denom = X.sum[0][lane] + X.sum[1][lane];
-    // pass 3: probabilities, my top-k, probability sums of my columns
-    TopK<KM> tk;
-    tk.init();
-    double* msum = e.o.msum4 + static_cast<long long>(tile_warp) * N;
-    for (int ch = cb; ch < ce; ++ch) {
-      const int c0 = ch * 32;
-      float v[32];
-      double pr[32];
-      load_acc32(tmem_tile, c0, v);
-#pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        pr[c] = (valid && c0 + c < N) ? exp(static_cast<double>(v[c]) - dmx) / denom : 0.0;
-        if (c0 + c < N) {
-          if (valid && e.o.probs) e.o.probs[gtok * N + c0 + c] = pr[c];
-          tk.insert(pr[c], c0 + c, e.k);
-        }
-      }
-      const double colsum = warp_transpose_sum32(pr, lane);
-      if (c0 + lane < N) msum[c0 + lane] = colsum;
-    }
-    if (h == 1) {
-#pragma unroll
-      for (int j = 0; j < KM; ++j) {
-        X.tp[lane][j] = tk.p[j];
-        X.te[lane][j] = tk.e[j];
-      }
-    }
-    ptx::named_bar_sync(bar_id, 64);
-    if (h == 0) {
-#pragma unroll
-      for (int j = 0; j < KM; ++j)
-        if (X.te[lane][j] >= 0) tk.insert(X.tp[lane][j], X.te[lane][j], e.k);
-      finish_row(tk, valid, gtok, e.k, N, tile_warp, e.o, lane);
-    }
-    ptx::named_bar_sync(bar_id, 64);  // exchange area free for the next tile
+    if (cb >= ce) release();
   }
 };
+
+// Per-token routing over fp32 logits: fp64 softmax exactly as the reference (max-subtract, exp, sequential
+// sum in expert order, divide: gate.cpp:12-28), top-k in (probability desc, expert asc) order
+// (gate.cpp:117-134), per-32-token-group expert histograms and probability sums (gate.cpp:115).
+// A block of 4 warps owns one 32-token group (= one hist4/msum4 slot); each warp takes 8 tokens with its
+// lanes across experts (expert c on lane c % 32), so every exp is computed once and parked in shared
+// memory for the sequential denominator, and top-k is a warp arg-max.
+constexpr int kRouteRowsPerWarp = 8;
+
+template <int EPL, int KM>
+__global__ void __launch_bounds__(128) route_logits_kernel(const float* __restrict__ logits, RouteDims d,
+                                                           RowRouteOut o) {
+  constexpr int NC = EPL * 32;
+  constexpr int RPW = kRouteRowsPerWarp;
+  extern __shared__ double route_smem[];
+  auto E = reinterpret_cast<double (*)[RPW][NC + 1]>(route_smem);  // [4][RPW][NC+1] exps
+  __shared__ double den[4][RPW];
+  auto ms = reinterpret_cast<double (*)[NC]>(route_smem);            // reuses E after the block barrier
+  auto hs = reinterpret_cast<int (*)[NC]>(route_smem + 4 * NC);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x;  // 32-token group == hist4 / msum4 slot
+  const int groups = d.TB * 4;
+  const int proc = b / groups;
+  const int tok0 = (b % groups) * 32 + warp * RPW;
+  const int N = d.N, k = d.k;
+  bool finite = true;
+#pragma unroll 2
+  for (int r = 0; r < RPW; ++r) {
+    const int tok = tok0 + r;
+    const bool valid = tok < d.S;
+    const float* row = logits + (static_cast<long long>(proc) * d.S + tok) * N;
+    float v[EPL];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < EPL; ++j) {
+      const int c = j * 32 + lane;
+      v[j] = (valid && c < N) ? __ldg(row + c) : -INFINITY;
+      if (valid && c < N) finite &= isfinite(v[j]);
+      mx = fmaxf(mx, v[j]);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    const double dmx = valid ? static_cast<double>(mx) : 0.0;
+#pragma unroll
+    for (int j = 0; j < EPL; ++j) {
+      const int c = j * 32 + lane;
+      E[warp][r][c] = (valid && c < N) ? exp(static_cast<double>(v[j]) - dmx) : 0.0;
+    }
+  }
+  __syncwarp();
+  if (lane < RPW) {  // sequential denominator, expert order (gate.cpp:19-21)
+    double sum = 0.0;
+    for (int c = 0; c < N; ++c) sum += E[warp][lane][c];
+    den[warp][lane] = sum;
+  }
+  __syncwarp();
+  int hc[EPL];
+  double msum[EPL];
+#pragma unroll
+  for (int j = 0; j < EPL; ++j) {
+    hc[j] = 0;
+    msum[j] = 0.0;
+  }
+  for (int r = 0; r < RPW; ++r) {
+    const int tok = tok0 + r;
+    const bool valid = tok < d.S;
+    const long long gtok = static_cast<long long>(proc) * d.S + tok;
+    const double dn = den[warp][r];
+    double p[EPL];
+#pragma unroll
+    for (int j = 0; j < EPL; ++j) {
+      const int c = j * 32 + lane;
+      p[j] = (valid && c < N) ? E[warp][r][c] / dn : 0.0;
+      if (valid && c < N && o.probs) o.probs[gtok * N + c] = p[j];
+      msum[j] += p[j];
+    }
+    if (!valid) continue;
+    // top-k: k rounds of a warp arg-max under (p desc, expert asc)
+    unsigned taken = 0;
+    double pp[KM];
+    int pe[KM];
+#pragma unroll
+    for (int t = 0; t < KM; ++t) {
+      pp[t] = -1.0;
+      pe[t] = -1;
+      if (t < k) {
+        double bp = -1.0;
+        int bi = 0x7fffffff;
+#pragma unroll
+        for (int j = 0; j < EPL; ++j) {
+          const int c = j * 32 + lane;
+          if (c < N && !((taken >> j) & 1u) && p[j] > bp) {
+            bp = p[j];
+            bi = c;
+          }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const double op = __shfl_xor_sync(0xffffffffu, bp, off);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+          if (op > bp || (op == bp && oi < bi)) {
+            bp = op;
+            bi = oi;
+          }
+        }
+        pp[t] = bp;
+        pe[t] = bi;
+        if ((bi & 31) == lane) {
+          taken |= 1u << (bi >> 5);
+#pragma unroll
+          for (int j = 0; j < EPL; ++j)
+            if (j == (bi >> 5)) ++hc[j];
+        }
+      }
+    }
+    if (lane == 0) {
+      double mass = 0.0;
+#pragma unroll
+      for (int t = 0; t < KM; ++t)
+        if (t < k) mass += pp[t];
+#pragma unroll
+      for (int t = 0; t < KM; ++t) {
+        if (t < k) {
+          const long long a = gtok * k + t;
+          o.idx[a] = pe[t];
+          o.score[a] = pp[t];
+          o.gate[a] = static_cast<float>(k == 1 ? pp[t] : pp[t] / mass);
+        }
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, !finite) && lane == 0) atomicOr(o.bad, 1);
+  __syncthreads();  // every warp is done with E
+#pragma unroll
+  for (int j = 0; j < EPL; ++j) {
+    hs[warp][j * 32 + lane] = hc[j];
+    ms[warp][j * 32 + lane] = msum[j];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < N; c += blockDim.x) {
+    o.hist4[static_cast<long long>(b) * N + c] = hs[0][c] + hs[1][c] + hs[2][c] + hs[3][c];
+    o.msum4[static_cast<long long>(b) * N + c] = ((ms[0][c] + ms[1][c]) + ms[2][c]) + ms[3][c];
+  }
+}
+
+template <int EPL, int KM>
+static void route_logits_launch_k(const float* logits, const RouteDims& d, const RowRouteOut& o, cudaStream_t s) {
+  constexpr int smem = 4 * kRouteRowsPerWarp * (EPL * 32 + 1) * 8;
+  static_assert(smem >= 4 * EPL * 32 * 12, "E must cover the reduction scratch");
+  static unsigned long long attr_set = 0;  // per device
+  int dev = 0;
+  TAMOE_CUDA(cudaGetDevice(&dev));
+  if (!((attr_set >> dev) & 1ull)) {
+    TAMOE_CUDA(cudaFuncSetAttribute(route_logits_kernel<EPL, KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set |= 1ull << dev;
+  }
+  route_logits_kernel<EPL, KM><<<static_cast<unsigned>(d.tiles()) * 4, 128, smem, s>>>(logits, d, o);
+  TAMOE_CUDA(cudaGetLastError());
+}
+
+template <int EPL>
+static void route_logits_launch(const float* logits, const RouteDims& d, const RowRouteOut& o, cudaStream_t s) {
+  if (d.k == 1) route_logits_launch_k<EPL, 1>(logits, d, o, s);
+  else if (d.k == 2) route_logits_launch_k<EPL, 2>(logits, d, o, s);
+  else route_logits_launch_k<EPL, kMaxTopK>(logits, d, o, s);
+}
+
+void route_from_logits(const float* logits, const RouteDims& d, const RowRouteOut& o, cudaStream_t s) {
+  require(d.k >= 1 && d.k <= kMaxTopK && d.k <= d.N, "k must be in [1, min(N, 8)]");
+  require(d.N <= 256, "router: N must be <= 256");
+  if (d.N <= 32) route_logits_launch<1>(logits, d, o, s);
+  else if (d.N <= 64) route_logits_launch<2>(logits, d, o, s);
+  else if (d.N <= 128) route_logits_launch<4>(logits, d, o, s);
+  else route_logits_launch<8>(logits, d, o, s);
+}
 
 // Standalone router over caller-provided fp64 probabilities (the reference's topk_route input).
 __global__ void __launch_bounds__(kRouteTile) route_rows_kernel(const double* __restrict__ probs, RouteDims d,
@@ -166,35 +265,25 @@ void route_rows_from_probs(const double* probs, const RouteDims& d, const RowRou
   TAMOE_CUDA(cudaGetLastError());
 }
 
-template <int BN>
-static void gate_launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
-                        const GateEpiParams& ep, cudaStream_t s) {
-  if (ep.k == 1) {
-    launch_gemm<kModeGate, BN, false, false, EpiGate<1>>(ta, tb, p, ep, 0, s);
-  } else if (ep.k == 2) {
-    launch_gemm<kModeGate, BN, false, false, EpiGate<2>>(ta, tb, p, ep, 0, s);
-  } else {
-    launch_gemm<kModeGate, BN, false, false, EpiGate<kMaxTopK>>(ta, tb, p, ep, 0, s);
-  }
-}
-
 void gate_forward(const __nv_bfloat16* x, const __nv_bfloat16* wg, int n_pad, const RouteDims& d, int dm,
                   const RowRouteOut& o, cudaStream_t s) {
   require(d.k >= 1 && d.k <= kMaxTopK && d.k <= d.N, "k must be in [1, min(N, 8)]");
   require(dm % 64 == 0, "gate: d must be a multiple of 64 (pad with zeros)");
   require(n_pad % 16 == 0 && n_pad >= d.N && n_pad <= 256, "gate: n_pad must be round_up(N, 16) <= 256");
+  require(o.logits != nullptr, "gate: logits buffer required");
   const int BNsel = n_pad <= 32 ? 32 : (n_pad <= 64 ? 64 : (n_pad <= 128 ? 128 : 256));
   const long long T = static_cast<long long>(d.P) * d.S;
   CUtensorMap ta = make_tmap_bf16(x, dm, T, dm, kBM);
   CUtensorMap tb = make_tmap_bf16(wg, dm, static_cast<uint64_t>(d.P) * n_pad, dm, BNsel);
   GemmParams p{1, nullptr, nullptr, 0, n_pad, dm, 1, d.S, n_pad, d.P, 0, 1, 0, 0};
-  GateEpiParams ep{o, d.N, d.k, d.S, d.TB};
+  GateEpiParams ep{o.logits, d.N, d.S};
   switch (BNsel) {
-    case 32: gate_launch<32>(ta, tb, p, ep, s); break;
-    case 64: gate_launch<64>(ta, tb, p, ep, s); break;
-    case 128: gate_launch<128>(ta, tb, p, ep, s); break;
-    default: gate_launch<256>(ta, tb, p, ep, s); break;
+    case 32: launch_gemm<kModeGate, 32, false, false, EpiLogits>(ta, tb, p, ep, 0, s); break;
+    case 64: launch_gemm<kModeGate, 64, false, false, EpiLogits>(ta, tb, p, ep, 0, s); break;
+    case 128: launch_gemm<kModeGate, 128, false, false, EpiLogits>(ta, tb, p, ep, 0, s); break;
+    default: launch_gemm<kModeGate, 256, false, false, EpiLogits>(ta, tb, p, ep, 0, s); break;
   }
+  route_from_logits(o.logits, d, o, s);
 }
 
 }  // namespace tamoe

@@ -58,6 +58,7 @@ void RouteWorkspace::reserve(Arena& a, int P, int S, int N, int k) {
   a.reserve(buf.seg_rows, N);
   a.reserve(buf.total_rows, 1);
   a.reserve(buf.bad, 1);
+  a.reserve(buf.logits, static_cast<long long>(P) * S * N);
   a.reserve(caps, static_cast<long long>(P) * N);
 }
 

@@ -68,6 +68,7 @@ struct RouteBuffers {
   int* seg_rows = nullptr;    // [N]
   int* total_rows = nullptr;  // [1]
   int* bad = nullptr;         // [1] non-finite logit flag
+  float* logits = nullptr;    // [P*S*N] gate logits scratch (router API without a caller buffer)
 };
 
 // Gate epilogue / standalone router outputs (per-row routing, see gate.cu).
@@ -84,6 +85,8 @@ struct RowRouteOut {
 
 // Top-k selection from fp64 probabilities (P x S x N), the reference's topk_route input.
 void route_rows_from_probs(const double* probs, const RouteDims& d, const RowRouteOut& o, cudaStream_t s);
+// Same per-token routing over fp32 gate logits (softmax in fp64 first), N <= 256.
+void route_from_logits(const float* logits, const RouteDims& d, const RowRouteOut& o, cudaStream_t s);
 
 // histogram scan + stable bucket lists (gate.cpp:160-164 / 181-185 order)
 void route_bucket(const RouteDims& d, const RouteBuffers& b, cudaStream_t s);

@@ -60,8 +60,37 @@ def run(name, counts, M, K, mode="fwd"):
           f"{flops/ms/1e9:7.1f} TF/s | cuBLAS dense {ms_cb*1e3:8.1f} us {flops/ms_cb/1e9:7.1f} TF/s", flush=True)
 
 
+def c2_counts():
+    """Per-expert token counts of one real C2 layer step (bench.py's inputs and initial weights)."""
+    from paper_2302_09915_b200 import ops
+    from paper_2302_09915_b200.layer import LayerConfig, TAMoELayer, LOSS_TOPO, ACT_GELU
+    cfg = LayerConfig(P=1, S=16384, d=1024, d_out=1024, N=64, k=1, f=4096, act=ACT_GELU, cap_mode=0,
+                      aux_kind=LOSS_TOPO, need_dx=True)
+    layer = TAMoELayer(cfg, ops.target_closed_form([[1.0]], 64, 1, 16384))
+    params = layer.init_params(seed=1)
+    g = torch.Generator(device="cuda").manual_seed(100)
+    x = torch.randn(16384, 1024, generator=g, device="cuda").bfloat16()
+    y = (torch.randn(16384, 1024, generator=g, device="cuda") * 0.5).bfloat16()
+    layer.step(x, y, params)
+    torch.cuda.synchronize()
+    c = [int(v) for v in layer.read(ops.R_COUNTS, (1, 64))[0]]
+    del layer
+    return c
+
+
 if __name__ == "__main__":
     rng = np.random.default_rng(0)
+    if "--c2" in sys.argv:
+        real = c2_counts()
+        print("C2 routed counts: min", min(real), "max", max(real), "std", float(np.std(real)), flush=True)
+        for nm, cnt in (("uniform 256", [256] * 64), ("C2 routed", real)):
+            run(nm + " fwd1", cnt, 4096, 1024)
+            run(nm + " fwd2", cnt, 1024, 4096)
+            run(nm + " dgrad2", cnt, 4096, 1024, "dgrad")
+            run(nm + " dgrad1", cnt, 1024, 4096, "dgrad")
+            run(nm + " wgrad2", cnt, 1024, 4096, "wgrad")
+            run(nm + " wgrad1", cnt, 4096, 1024, "wgrad")
+        sys.exit(0)
     bal = list(rng.multinomial(16384, [1 / 64] * 64))
     run("dense 16384 rows", [16384], 4096, 1024)
     run("dense 16384 rows", [16384], 1024, 4096)

@@ -1,0 +1,140 @@
+// NVLink peer-memory bandwidth microbenchmark (single process, all visible GPUs, peer access enabled):
+// copy engine vs SM-driven 16-byte stores / loads with several launch shapes, and the all-to-all
+// pattern the expert-parallel layer uses (every GPU writes 1/P of a buffer to every GPU at once).
+// Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o scripts/p2p_bench scripts/p2p_bench.cu
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#define CK(x)                                                                 \
+  do {                                                                        \
+    cudaError_t e_ = (x);                                                     \
+    if (e_ != cudaSuccess) {                                                  \
+      printf("CUDA %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
+      exit(1);                                                                \
+    }                                                                         \
+  } while (0)
+
+template <int U>
+__global__ void copy_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, long long n) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x * U;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x * U + threadIdx.x; i < n; i += stride) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long j = i + static_cast<long long>(u) * blockDim.x;
+      v[u] = j < n ? src[j] : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long j = i + static_cast<long long>(u) * blockDim.x;
+      if (j < n) dst[j] = v[u];
+    }
+  }
+}
+
+// all-to-all: GPU g writes chunk j of its source (n/P vectors) into GPU j's destination at slot g
+__global__ void a2a_kernel(const uint4* __restrict__ src, uint4** dsts, int P, int me, long long chunk) {
+  const long long total = chunk * P;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const int j = static_cast<int>(i / chunk);
+    const long long o = i % chunk;
+    dsts[j][me * chunk + o] = src[i];
+  }
+}
+
+static float time_ms(cudaStream_t s, cudaEvent_t a, cudaEvent_t b) {
+  float ms;
+  CK(cudaEventSynchronize(b));
+  CK(cudaEventElapsedTime(&ms, a, b));
+  return ms;
+}
+
+int main() {
+  int ng = 0;
+  CK(cudaGetDeviceCount(&ng));
+  printf("GPUs: %d\n", ng);
+  if (ng < 2) return 0;
+  const size_t bytes = 64ull << 20;
+  const long long nv = bytes / 16;
+  std::vector<uint4*> buf(ng), buf2(ng);
+  std::vector<cudaStream_t> st(ng);
+  for (int g = 0; g < ng; ++g) {
+    CK(cudaSetDevice(g));
+    for (int h = 0; h < ng; ++h)
+      if (h != g) cudaDeviceEnablePeerAccess(h, 0);
+    CK(cudaMalloc(&buf[g], bytes));
+    CK(cudaMalloc(&buf2[g], bytes));
+    CK(cudaMemset(buf[g], 1, bytes));
+    CK(cudaStreamCreateWithFlags(&st[g], cudaStreamNonBlocking));
+  }
+  CK(cudaSetDevice(0));
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  // 1) copy engine 0 -> 1
+  for (int it = 0; it < 2; ++it) {
+    CK(cudaEventRecord(a, st[0]));
+    CK(cudaMemcpyPeerAsync(buf2[1], 1, buf[0], 0, bytes, st[0]));
+    CK(cudaEventRecord(b, st[0]));
+    float ms = time_ms(st[0], a, b);
+    if (it) printf("copy engine 0->1          : %7.1f GB/s\n", bytes / ms / 1e6);
+  }
+  // 2) SM stores 0 -> 1 (push) and loads 1 -> 0 (pull), several shapes
+  const int grids[] = {148, 296, 592, 1184};
+  const int blocks[] = {256, 512, 1024};
+  for (int dir = 0; dir < 2; ++dir) {
+    for (int gi : grids)
+      for (int bi : blocks) {
+        float best = 1e9;
+        for (int it = 0; it < 3; ++it) {
+          CK(cudaEventRecord(a, st[0]));
+          if (dir == 0) copy_kernel<4><<<gi, bi, 0, st[0]>>>(buf[0], buf2[1], nv);  // push
+          else copy_kernel<4><<<gi, bi, 0, st[0]>>>(buf[1], buf2[0], nv);           // pull
+          CK(cudaEventRecord(b, st[0]));
+          float ms = time_ms(st[0], a, b);
+          if (it && ms < best) best = ms;
+        }
+        printf("SM %-4s grid %5d block %5d : %7.1f GB/s\n", dir == 0 ? "push" : "pull", gi, bi, bytes / best / 1e6);
+      }
+  }
+  // 3) all-to-all over all GPUs, SM stores, every GPU concurrently
+  for (int gi : grids) {
+    std::vector<uint4**> dptr(ng);
+    for (int g = 0; g < ng; ++g) {
+      CK(cudaSetDevice(g));
+      CK(cudaMalloc(&dptr[g], sizeof(uint4*) * ng));
+      CK(cudaMemcpy(dptr[g], buf2.data(), sizeof(uint4*) * ng, cudaMemcpyHostToDevice));
+    }
+    const long long chunk = nv / ng;
+    float worst = 0;
+    for (int it = 0; it < 3; ++it) {
+      for (int g = 0; g < ng; ++g) {
+        CK(cudaSetDevice(g));
+        CK(cudaDeviceSynchronize());
+      }
+      std::vector<cudaEvent_t> ea(ng), eb(ng);
+      for (int g = 0; g < ng; ++g) {
+        CK(cudaSetDevice(g));
+        CK(cudaEventCreate(&ea[g]));
+        CK(cudaEventCreate(&eb[g]));
+        CK(cudaEventRecord(ea[g], st[g]));
+        a2a_kernel<<<gi, 512, 0, st[g]>>>(buf[g], dptr[g], ng, g, chunk);
+        CK(cudaEventRecord(eb[g], st[g]));
+      }
+      float mx = 0;
+      for (int g = 0; g < ng; ++g) {
+        CK(cudaSetDevice(g));
+        mx = std::max(mx, time_ms(st[g], ea[g], eb[g]));
+      }
+      if (it) worst = mx;
+    }
+    const double off = bytes * (ng - 1.0) / ng;
+    printf("a2a %d GPUs grid %5d: %7.1f GB/s off-rank per GPU (%.1f us for %zu MiB/GPU)\n", ng, gi,
+           off / worst / 1e6, worst * 1e3, bytes >> 20);
+  }
+  return 0;
+}
