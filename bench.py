@@ -254,7 +254,6 @@ def main():
     for _ in range(args.warmup):
         layer.step(x, y, params)
     torch.cuda.synchronize()
-    layer.enable_timing(True)
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
@@ -273,6 +272,11 @@ def main():
         clocks = dict(clocks)
         clocks["reasons"] = sorted({r for c in allc for r in c["reasons"]})
         clocks["per_rank_sm_mhz"] = [c["sm_mhz"] for c in allc]
+    # phase breakdown: separate eager steps with CUDA events between launches (not part of `value`)
+    layer.enable_timing(True)
+    for _ in range(max(3, min(args.steps, 10))):
+        layer.step(x, y, params)
+    torch.cuda.synchronize()
     phases, tsteps = layer.timing()
     layer.enable_timing(False)
     a2a = None

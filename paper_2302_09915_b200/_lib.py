@@ -11,7 +11,8 @@ import os
 from ctypes import c_double, c_int, c_longlong, c_void_p, POINTER
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libtamoe.so")
+# TAMOE_LIB: alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("TAMOE_LIB") or os.path.join(_HERE, "lib", "libtamoe.so")
 
 
 class TamoeError(RuntimeError):

@@ -11,10 +11,12 @@ void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams&
                  int grid_limit, cudaStream_t s) {
   auto kern = gemm_sm100_kernel<kMode, BN, A_MN, B_MN, Epi, kCG>;
   const int smem = GemmSmem<BN, EpiSmem<Epi>::value, kCG>::kTotal;
-  static bool configured = false;
-  if (!configured) {
+  static unsigned long long configured = 0;  // per device
+  int dev = 0;
+  TAMOE_CUDA(cudaGetDevice(&dev));
+  if (!((configured >> dev) & 1ull)) {
     TAMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = true;
+    configured |= 1ull << dev;
   }
   int grid = num_sms();
   if (grid_limit > 0 && grid_limit < grid) grid = grid_limit;

@@ -92,7 +92,11 @@ struct GemmSmem {
   // barriers: full[S], empty[S], tfull[2], tempty[2]; tmem addr; tile prefix; group starts / rows
   static constexpr int kMiscBytes = (2 * 8 + 4) * 8 + 16 + (3 * kMaxGroups + 1) * 4;
   static constexpr int kBudget = 227 * 1024 - ((kEpiBytes + 1023) / 1024) * 1024 - kMiscBytes - 2048;
+#ifdef TAMOE_MAX_STAGES
+  static constexpr int kMaxStages = TAMOE_MAX_STAGES;  // A/B experiments only
+#else
   static constexpr int kMaxStages = 8;
+#endif
   static constexpr int kStages = (kBudget / kStageBytes < kMaxStages) ? kBudget / kStageBytes : kMaxStages;
   static_assert(kStages >= 2, "not enough shared memory for the pipeline");
   static constexpr int kEpiOffset = kStages * kStageBytes;

@@ -288,13 +288,77 @@ void Layer::experts_backward(const LayerIO& io, int G, int E, int nsub, const in
   }
 }
 
+Layer::StepGraph::~StepGraph() {
+  for (auto e : exec)
+    if (e) cudaGraphExecDestroy(e);
+  if (in) cudaEventDestroy(in);
+  if (out) cudaEventDestroy(out);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+static bool graphs_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("TAMOE_GRAPHS");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+void Layer::run_step(const LayerIO& io, cudaStream_t s) {
+  if (ep_) step_ep(io, s);
+  else step_local(io, s);
+}
+
+// The first step runs eagerly (one-time kernel attribute setup); later steps replay a captured graph
+// of the whole step (17-19 launches, tensor maps baked in), re-captured whenever a buffer pointer changes.
 void Layer::step(const LayerIO& io, cudaStream_t s) {
   const LayerConfig& c = cfg_;
   require(io.x && io.y && io.wg && io.w1 && io.dwg && io.dw1 && io.losses, "layer step: missing buffer");
   require(c.f == 0 || (io.w2 && io.dw2), "layer step: FFN experts need w2 / dw2");
   require(!c.need_dx || io.dx, "layer step: need_dx set but dx is null");
-  if (ep_) step_ep(io, s);
-  else step_local(io, s);
+  StepGraph& g = graph_;
+  if (timer_.enabled || !graphs_enabled() || !g.warm) {
+    run_step(io, s);
+    g.warm = true;
+    return;
+  }
+  if (!g.stream) {
+    TAMOE_CUDA(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
+    TAMOE_CUDA(cudaEventCreateWithFlags(&g.in, cudaEventDisableTiming));
+    TAMOE_CUDA(cudaEventCreateWithFlags(&g.out, cudaEventDisableTiming));
+  }
+  TAMOE_CUDA(cudaEventRecord(g.in, s));
+  TAMOE_CUDA(cudaStreamWaitEvent(g.stream, g.in, 0));
+  int slot = -1;
+  for (int i = 0; i < StepGraph::kCache; ++i)
+    if (g.exec[i] && std::memcmp(&g.io[i], &io, sizeof(LayerIO)) == 0) slot = i;
+  if (slot < 0) {
+    slot = 0;  // least recently used
+    for (int i = 1; i < StepGraph::kCache; ++i)
+      if (g.used[i] < g.used[slot]) slot = i;
+    if (g.exec[slot]) {
+      TAMOE_CUDA(cudaGraphExecDestroy(g.exec[slot]));
+      g.exec[slot] = nullptr;
+    }
+    cudaGraph_t graph = nullptr;
+    TAMOE_CUDA(cudaStreamBeginCapture(g.stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      run_step(io, g.stream);
+    } catch (...) {
+      cudaStreamEndCapture(g.stream, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    TAMOE_CUDA(cudaStreamEndCapture(g.stream, &graph));
+    const cudaError_t e = cudaGraphInstantiate(&g.exec[slot], graph, 0);
+    cudaGraphDestroy(graph);
+    TAMOE_CUDA(e);
+    g.io[slot] = io;
+  }
+  g.used[slot] = ++g.tick;
+  TAMOE_CUDA(cudaGraphLaunch(g.exec[slot], g.stream));
+  TAMOE_CUDA(cudaEventRecord(g.out, g.stream));
+  TAMOE_CUDA(cudaStreamWaitEvent(s, g.out, 0));
 }
 
 // Shared front: gate + histogram/scan + capacity.

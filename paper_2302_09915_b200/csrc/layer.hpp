@@ -153,6 +153,21 @@ class Layer {
   double *penalties_ = nullptr, *loss_part_ = nullptr;
   int n_loss_part_ = 0;
   PhaseTimer timer_;
+  // CUDA graphs of one step keyed by the step's buffers (LayerIO), a few cached (double-buffered inputs
+  // alternate), captured and launched on a private stream joined to the caller's with two events.
+  // TAMOE_GRAPHS=0 or phase timing: eager.
+  struct StepGraph {
+    static constexpr int kCache = 4;
+    bool warm = false;
+    LayerIO io[kCache]{};
+    cudaGraphExec_t exec[kCache] = {};
+    unsigned long long used[kCache] = {};
+    unsigned long long tick = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t in = nullptr, out = nullptr;
+    ~StepGraph();
+  } graph_;
+  void run_step(const LayerIO& io, cudaStream_t s);
 };
 
 }  // namespace tamoe

@@ -83,6 +83,8 @@ if __name__ == "__main__":
     if "--c2" in sys.argv:
         real = c2_counts()
         print("C2 routed counts: min", min(real), "max", max(real), "std", float(np.std(real)), flush=True)
+        for c in (128, 160, 192, 256, 320, 384, 512):
+            run(f"uniform {c} fwd1", [c] * 64, 4096, 1024)
         for nm, cnt in (("uniform 256", [256] * 64), ("C2 routed", real)):
             run(nm + " fwd1", cnt, 4096, 1024)
             run(nm + " fwd2", cnt, 1024, 4096)

@@ -6,12 +6,12 @@ import sys
 
 def fam(n):
     if "gemm_sm100_kernel<2," in n:
-        return "fused gate (tcgen05 + fp64 softmax/top-k)"
+        return "gate logits GEMM (tcgen05)"
     if "EpiSwap" in n:
         return "expert grouped GEMM fwd/dgrad (tcgen05, swap-AB)"
     if "EpiWgrad" in n:
         return "expert grouped GEMM wgrad (tcgen05)"
-    for k in ["EpiGateDw", "EpiGateDx", "route_scan", "route_bucket", "route_capacity", "route_permute",
+    for k in ["route_logits", "EpiGateDw", "EpiGateDx", "route_scan", "route_bucket", "route_capacity", "route_permute",
               "combine_loss", "gate_dz", "dwg_reduce", "ep_plan"]:
         if k in n:
             return k
@@ -30,7 +30,7 @@ def main(path, out):
             if d.get("Metric Name") == "gpu__time_duration.sum":
                 L.append((d["Kernel Name"], float(d["Metric Value"])))
     ours = [(n, t) for n, t in L if fam(n)]
-    gates = [i for i, (n, t) in enumerate(ours) if fam(n).startswith("fused gate")]
+    gates = [i for i, (n, t) in enumerate(ours) if fam(n).startswith("gate logits")]
     step = ours[gates[-1]:]  # last (warm) step
     tot = sum(t for _, t in step)
     agg = {}

@@ -61,7 +61,7 @@ def run_case(P, S, d, dout, N, k, f, cap, kind, need_dx, seed=0, cf=1.25):
     torch.cuda.synchronize()
     o = O.layer_step(x, y, gates, U=U, W1=W1, W2=W2, k=k, cap_mode=cap, cf=cf, c_hat=c_hat, aux_kind=kind,
                      penalties=pen, act=1, want_dx=need_dx)
-    return layer, o, dict(yh=yh, x=x)
+    return layer, o, dict(yh=yh, x=x, args=(xt, yt, params, yh))
 
 
 def check(layer, o, extra, P, S, N, k, f, need_dx):
@@ -128,3 +128,22 @@ def test_layer_c4_expert_shape_reduced():
     P, S, d, dout, N, k, f = 2, 16, 4096, 4096, 4, 2, 16384
     layer, o, extra = run_case(P, S, d, dout, N, k, f, 3, 1, True, seed=4)
     check(layer, o, extra, P, S, N, k, f, True)
+
+
+def test_layer_graph_replay_bitwise():
+    """Steps after the first replay a captured CUDA graph of the whole step; they must reproduce the eager
+    step bit for bit, also after a buffer pointer changes (re-capture) and when switching back (cache)."""
+    P, S, d, dout, N, k, f = 1, 384, 256, 128, 8, 2, 512
+    layer, o, extra = run_case(P, S, d, dout, N, k, f, 0, 1, True)
+    snap = lambda: [layer.losses.cpu().clone(), layer.dwg.cpu().clone(), layer.dw1.float().cpu().clone(),
+                    layer.dw2.float().cpu().clone(), layer.dx.float().cpu().clone(), extra["yh"].float().cpu().clone()]
+    ref = snap()
+    x, y, params, yh = extra["args"]
+    for it in range(3):
+        yh2 = yh if it != 1 else torch.zeros_like(yh)
+        layer.step(x, y, params, y_hat=yh2)
+        torch.cuda.synchronize()
+        got = snap()
+        got[5] = yh2.float().cpu()
+        for a, b in zip(ref, got):
+            assert torch.equal(a, b)
