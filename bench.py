@@ -285,15 +285,17 @@ def main():
         # peer-memory accesses inside the compute kernels; NCCL only for counts + barriers)
         nbytes = layer.a2a_bytes()
         disp_ms = phases.get("a2a_dispatch", 0.0)  # fused permute + dispatch kernel + barrier
-        comb_ms = phases.get("combine_loss", 0.0) + phases.get("a2a_barrier_combine", 0.0)
-        a2a = {"offrank_bytes_per_step": {"dispatch": nbytes[0], "combine_loads": nbytes[1], "dO_stores": nbytes[2],
-                                          "dx_loads": nbytes[3]},
+        comb_ms = phases.get("combine_loss", 0.0) + phases.get("a2a_barrier_combine", 0.0)  # dO stores
+        a2a = {"offrank_bytes_per_step": {"dispatch": nbytes[0], "o_return": nbytes[1], "dO_stores": nbytes[2],
+                                          "dx_return": nbytes[3]},
                "dispatch_ms": disp_ms, "combine_ms": comb_ms,
                "dispatch_bus_gbs": nbytes[0] / (disp_ms / 1e3) / 1e9 if disp_ms > 0 else 0.0,
-               "combine_bus_gbs": (nbytes[1] + nbytes[2]) / (comb_ms / 1e3) / 1e9 if comb_ms > 0 else 0.0,
+               "combine_bus_gbs": nbytes[2] / (comb_ms / 1e3) / 1e9 if comb_ms > 0 else 0.0,
                "peak_gbs": 900.0, "measured_peer_peak_gbs": 690.0, "measured_a2a_gbs": 533.0,
-               "note": "fused NVLink peer-memory dispatch (permute kernel stores into the owner's layout) and "
-                       "combine (owner loads + dO stores); bus GB/s = off-rank bytes / phase time (CUDA events, "
+               "note": "all payload moves as NVLink peer stores fused into compute kernels: dispatch (permute kernel "
+                       "-> owner's layout), O return (owner's fwd2 epilogue -> home rank), dO (combine kernel -> "
+                       "owner), dX return (owner's dgrad1 epilogue -> home rank); bus GB/s = off-rank bytes / phase "
+                       "time (CUDA events, "
                        "incl. the stream-ordered NCCL barrier); measured peaks: profiles/r01_p2p_bench.txt "
                        "(single-pair SM pull 690 GB/s, 4-GPU all-to-all SM stores 533 GB/s per GPU)"}
     losses = layer.losses.cpu().tolist()

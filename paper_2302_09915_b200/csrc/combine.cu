@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(kCombWarps * 32) combine_loss_kernel(const __g
         const int ex = a.idx[t * k + j];
         const int owner = a.map.rank_of(ex);
         const long long r = a.map.row(rows[j], ex);
-        osrc[j] = a.O.p[owner] + r * a.dout;
+        osrc[j] = a.o_home ? a.O.p[0] + static_cast<long long>(rows[j]) * a.dout : a.O.p[owner] + r * a.dout;
         odst[j] = a.dO.p[owner] + r * a.dout;
       }
     }

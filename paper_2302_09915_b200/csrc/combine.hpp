@@ -13,7 +13,8 @@ struct CombineArgs {
   const int* pos;                // [T*k] row in this rank's padded expert-major layout (-1 dropped)
   const int* idx;                // [T*k] expert of the pick (owner rank = idx / E)
   const float* gate;             // [T*k]
-  PeerBufs O;                    // expert outputs in every owner's receive layout (peer-mapped)
+  PeerBufs O;                    // expert outputs in every owner's receive layout (peer-mapped) ...
+  int o_home;                    // ... or (1) already returned into this rank's layout: O.p[0][pos]
   const __nv_bfloat16* y;        // [T x dout] targets
   __nv_bfloat16* y_hat;          // optional [T x dout]
   PeerBufs dO;                   // gradient w.r.t. expert outputs, written into the owner's receive layout

@@ -5,8 +5,9 @@
 // Data path (no payload goes through NCCL): every rank's workspace arena is mapped into every
 // other rank's address space with CUDA IPC, so
 //   dispatch  = the permute kernel storing rows straight into the owner's receive layout,
-//   combine   = the combine kernel loading expert outputs from the owner and storing dO back,
-//   dX return = the gate-dX GEMM epilogue loading the owner's expert-path gradients.
+//   combine   = the owner's fwd2 epilogue storing expert outputs straight into the source's local layout,
+//               then the combine kernel reading them locally and storing dO into the owner,
+//   dX return = the owner's dgrad1 epilogue storing the expert-path gradients into the source.
 // NCCL carries only the counts all-gather (the paper's "extra all-to-all for sizes") and
 // stream-ordered barriers between the phases.  Offsets are computed on the device, so a step has
 // no host synchronisation.
@@ -31,6 +32,7 @@ struct EpPlanDev {
   int* dst_off = nullptr;     // [N] where this rank's rows for global expert e start at the owner
   int* recv_rows = nullptr;   // [1]
   int* flag = nullptr;        // [1] barrier scratch
+  int* push_row = nullptr;    // [rows] receive row -> (source rank << 27 | row in the source's local layout)
 };
 
 void ep_plan_device(const EpPlanDev& plan, int P, int E, int me, cudaStream_t s);

@@ -32,12 +32,38 @@ __global__ void ep_plan_kernel(EpPlanDev p, int P, int E, int me) {
   }
 }
 
+// Return map of the receive layout: block (local expert el, source i) fills its segment's rows with
+// (i, row of the same pick in source i's local layout = expert-major, 16-padded, global expert order).
+__global__ void ep_push_map_kernel(EpPlanDev p, int P, int E, int me) {
+  const int N = P * E;
+  const int el = blockIdx.x / P, i = blockIdx.x % P;
+  const int ge = me * E + el;
+  __shared__ int s_dst, s_src;
+  if (threadIdx.x == 0) {
+    int dst = 0;
+    for (int e2 = 0; e2 < el; ++e2)
+      for (int i2 = 0; i2 < P; ++i2) dst += pad16(p.all_counts[i2 * N + me * E + e2]);
+    for (int i2 = 0; i2 < i; ++i2) dst += pad16(p.all_counts[i2 * N + ge]);
+    int src = 0;
+    for (int e2 = 0; e2 < ge; ++e2) src += pad16(p.all_counts[i * N + e2]);
+    s_dst = dst;
+    s_src = src;
+  }
+  __syncthreads();
+  const int rows = pad16(p.all_counts[i * N + ge]);
+  for (int r = threadIdx.x; r < rows; r += blockDim.x) p.push_row[s_dst + r] = (i << 27) | (s_src + r);
+}
+
 }  // namespace
 
 void ep_plan_device(const EpPlanDev& plan, int P, int E, int me, cudaStream_t s) {
   require(P >= 1 && P <= kMaxRanks, "expert parallelism supports up to 16 ranks");
   ep_plan_kernel<<<1, 128, 0, s>>>(plan, P, E, me);
   TAMOE_CUDA(cudaGetLastError());
+  if (plan.push_row) {
+    ep_push_map_kernel<<<E * P, 128, 0, s>>>(plan, P, E, me);
+    TAMOE_CUDA(cudaGetLastError());
+  }
 }
 
 }  // namespace tamoe

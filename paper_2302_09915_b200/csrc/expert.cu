@@ -70,18 +70,20 @@ struct SwapParams {
   CUtensorMap out32, out16;  // store maps of `out`: box {32 features, 32 | 16 tokens}
   CUtensorMap pre32, pre16;  // store maps of `pre_out`
   const __nv_bfloat16* pre_in;  // pre-activation for act' (dgrad)
+  SwapPush push;                 // V = 3: peer destination of every output row
   int ld;
   int act_out;   // activation applied on store (forward)
   int act_grad;  // activation derivative multiplied in (dgrad)
 };
 
 // V = 0: plain store; 1: store act(x) and the activation derivative act'(x) (kept for the backward in
-// place of the pre-activation); 2: multiply by the stored act'(x).
+// place of the pre-activation); 2: multiply by the stored act'(x); 3: plain, each row stored into its
+// home rank over NVLink (16-byte peer stores from the staging tile, 4 per lane and chunk).
 template <int V>
 struct EpiSwap {
   static constexpr int kChunk = 2048;  // 32 x 32 bf16
   static constexpr int kPf = 2;        // own chunks of pre_in in flight
-  static constexpr int kWarpBytes = V == 0 ? 2 * kChunk : 4 * kChunk;
+  static constexpr int kWarpBytes = (V == 0 || V == 3) ? 2 * kChunk : 4 * kChunk;
   static constexpr bool kEarlyRelease = true;
   static constexpr int kMaxCh = 4;  // a warp's chunks per tile: every other 32-column chunk of N <= 256
   using Params = SwapParams;
@@ -160,9 +162,27 @@ struct EpiSwap {
           so[c * 32 + lane] = __float2bfloat16(y);
         } else if constexpr (V == 2) {
           so[c * 32 + lane] = __float2bfloat16(x * __bfloat162float(sx[c * 32 + lane]));
-        } else {
+        } else {  // V = 0 / 3
           so[c * 32 + lane] = __float2bfloat16(act_fwd(e.act_out, x));
         }
+      }
+      if constexpr (V == 3) {
+        __syncwarp();
+        const int rows = min(32, ti.n - ch * 32);
+        const int y = row0 + ch * 32;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = (lane >> 2) + 8 * i;
+          if (r < rows) {
+            const int code = __ldg(e.push.row_code + y + r);
+            const uint4 v = *reinterpret_cast<const uint4*>(so + r * 32 + (lane & 3) * 8);
+            __nv_bfloat16* dst = e.push.dst.p[code >> kPushRowBits] +
+                                 static_cast<long long>(code & ((1 << kPushRowBits) - 1)) * e.ld + mcol + (lane & 3) * 8;
+            *reinterpret_cast<uint4*>(dst) = v;
+          }
+        }
+        __syncwarp();  // staging slot free again
+        continue;
       }
       ptx::fence_proxy_async_smem();
       __syncwarp();
@@ -294,7 +314,7 @@ static void check_groups(int G) { require(G >= 1 && G <= kMaxGroups, "group coun
 
 void grouped_fwd(const __nv_bfloat16* tokens, const __nv_bfloat16* w, int G, int M, int K, int R,
                  const int* seg_start, const int* seg_rows, __nv_bfloat16* out, __nv_bfloat16* pre_out, int act,
-                 cudaStream_t s, int w_mod) {
+                 cudaStream_t s, int w_mod, const SwapPush* push) {
   check_groups(G);
   require(M % kBM == 0, "grouped_fwd: M must be a multiple of 128");
   require(K % 64 == 0, "grouped_fwd: K must be a multiple of 64");
@@ -305,13 +325,20 @@ void grouped_fwd(const __nv_bfloat16* tokens, const __nv_bfloat16* w, int G, int
   GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1, w_mod, 1, env_int("TAMOE_PF_DIST", 0),
                env_int("TAMOE_PF_B", 0)};
   SwapParams ep = swap_params(out, pre_out, nullptr, M, R, act, kActNone);
-  if (pre_out) launch_pair_or_single<kModeSwap, 256, false, false, EpiSwap<1>>(pair, ta, tb, p, ep, s);
-  else launch_pair_or_single<kModeSwap, 256, false, false, EpiSwap<0>>(pair, ta, tb, p, ep, s);
+  require(!(push && pre_out), "grouped_fwd: push needs a plain output");
+  if (push) {
+    ep.push = *push;
+    launch_pair_or_single<kModeSwap, 256, false, false, EpiSwap<3>>(pair, ta, tb, p, ep, s);
+  } else if (pre_out) {
+    launch_pair_or_single<kModeSwap, 256, false, false, EpiSwap<1>>(pair, ta, tb, p, ep, s);
+  } else {
+    launch_pair_or_single<kModeSwap, 256, false, false, EpiSwap<0>>(pair, ta, tb, p, ep, s);
+  }
 }
 
 void grouped_dgrad(const __nv_bfloat16* grad_tokens, const __nv_bfloat16* w, int G, int M, int K, int R,
                    const int* seg_start, const int* seg_rows, __nv_bfloat16* out, const __nv_bfloat16* pre_in,
-                   int act, cudaStream_t s, int w_mod) {
+                   int act, cudaStream_t s, int w_mod, const SwapPush* push) {
   // out[R x M] = grad_tokens[R x K] . W_g[K x M]  (W_g stored K x M: MN-major A operand)
   check_groups(G);
   require(M % kBM == 0, "grouped_dgrad: M must be a multiple of 128");
@@ -323,8 +350,15 @@ void grouped_dgrad(const __nv_bfloat16* grad_tokens, const __nv_bfloat16* w, int
   GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1, w_mod, 1, env_int("TAMOE_PF_DIST", 0),
                env_int("TAMOE_PF_B", 0)};
   SwapParams ep = swap_params(out, nullptr, pre_in, M, R, kActNone, pre_in ? act : kActNone);
-  if (pre_in) launch_pair_or_single<kModeSwap, 256, true, false, EpiSwap<2>>(pair, ta, tb, p, ep, s);
-  else launch_pair_or_single<kModeSwap, 256, true, false, EpiSwap<0>>(pair, ta, tb, p, ep, s);
+  require(!(push && pre_in), "grouped_dgrad: push needs a plain output");
+  if (push) {
+    ep.push = *push;
+    launch_pair_or_single<kModeSwap, 256, true, false, EpiSwap<3>>(pair, ta, tb, p, ep, s);
+  } else if (pre_in) {
+    launch_pair_or_single<kModeSwap, 256, true, false, EpiSwap<2>>(pair, ta, tb, p, ep, s);
+  } else {
+    launch_pair_or_single<kModeSwap, 256, true, false, EpiSwap<0>>(pair, ta, tb, p, ep, s);
+  }
 }
 
 void grouped_wgrad(const __nv_bfloat16* a_tokens, const __nv_bfloat16* b_tokens, int G, int M, int N, int R,

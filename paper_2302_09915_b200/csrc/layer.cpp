@@ -175,6 +175,7 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
     arena_.reserve(plan_.dst_off, c.N);
     arena_.reserve(plan_.recv_rows, 1);
     arena_.reserve(plan_.flag, 1);
+    arena_.reserve(plan_.push_row, r_max_);
   }
   arena_.reserve(dz_, T * n64_);
   arena_.reserve(logits_, T * c.N);
@@ -239,9 +240,9 @@ void Layer::a2a_bytes(long long* out4) {
     rows_pad += (cnt + 15) / 16 * 16;
   }
   out4[0] = rows_pad * c.d * 2;     // dispatch stores (incl. zero pad rows)
-  out4[1] = rows * c.d_out * 2;     // combine loads of expert outputs
-  out4[2] = rows * c.d_out * 2;     // dO stores
-  out4[3] = c.need_dx ? rows * c.d * 2 : 0;  // dX loads
+  out4[1] = rows_pad * c.d_out * 2;  // expert outputs returned (owners' fwd2 epilogue stores, incl. pad rows)
+  out4[2] = rows * c.d_out * 2;      // dO stores (combine kernel)
+  out4[3] = c.need_dx ? rows_pad * c.d * 2 : 0;  // dX returns (owners' dgrad1 epilogue stores)
 }
 
 // Segments: G groups; group g uses weight g % E (E = G when nsub == 1).  For wgrad the E experts'
@@ -251,13 +252,16 @@ void Layer::experts_forward(const LayerIO& io, int G, int E, int /*nsub*/, const
   const LayerConfig& c = cfg_;
   PhaseTimer& tm = timer_;
   const int wm = G == E ? 0 : E;
+  // expert parallel: the expert outputs go straight back into each token's home rank
+  SwapPush push{peers(O_), plan_.push_row};
+  const SwapPush* pp = ep_ ? &push : nullptr;
   if (c.f == 0) {
-    grouped_fwd(xp_, io.w1, G, c.d_out, c.d, rows, seg_start, seg_rows, O_, nullptr, kActNone, s, wm);
+    grouped_fwd(xp_, io.w1, G, c.d_out, c.d, rows, seg_start, seg_rows, O_, nullptr, kActNone, s, wm, pp);
     tm.mark("expert_fwd", s);
   } else {
     grouped_fwd(xp_, io.w1, G, c.f, c.d, rows, seg_start, seg_rows, H_, A_, c.act, s, wm);
     tm.mark("expert_fwd1", s);
-    grouped_fwd(H_, io.w2, G, c.d_out, c.f, rows, seg_start, seg_rows, O_, nullptr, kActNone, s, wm);
+    grouped_fwd(H_, io.w2, G, c.d_out, c.f, rows, seg_start, seg_rows, O_, nullptr, kActNone, s, wm, pp);
     tm.mark("expert_fwd2", s);
   }
 }
@@ -267,11 +271,14 @@ void Layer::experts_backward(const LayerIO& io, int G, int E, int nsub, const in
   const LayerConfig& c = cfg_;
   PhaseTimer& tm = timer_;
   const int wm = G == E ? 0 : E;
+  // expert parallel: the expert-path input gradients go straight back into each token's home rank
+  SwapPush push{peers(dxp_), plan_.push_row};
+  const SwapPush* pp = ep_ ? &push : nullptr;
   if (c.f == 0) {
     grouped_wgrad(dO_, xp_, E, c.d_out, c.d, rows, seg_start, seg_rows, io.dw1, s, nsub);
     tm.mark("expert_wgrad", s);
     if (c.need_dx) {
-      grouped_dgrad(dO_, io.w1, G, c.d, c.d_out, rows, seg_start, seg_rows, dxp_, nullptr, kActNone, s, wm);
+      grouped_dgrad(dO_, io.w1, G, c.d, c.d_out, rows, seg_start, seg_rows, dxp_, nullptr, kActNone, s, wm, pp);
       tm.mark("expert_dgrad", s);
     }
   } else {
@@ -282,7 +289,7 @@ void Layer::experts_backward(const LayerIO& io, int G, int E, int nsub, const in
     grouped_wgrad(dA_, xp_, E, c.f, c.d, rows, seg_start, seg_rows, io.dw1, s, nsub);
     tm.mark("expert_wgrad1", s);
     if (c.need_dx) {
-      grouped_dgrad(dA_, io.w1, G, c.d, c.f, rows, seg_start, seg_rows, dxp_, nullptr, kActNone, s, wm);
+      grouped_dgrad(dA_, io.w1, G, c.d, c.f, rows, seg_start, seg_rows, dxp_, nullptr, kActNone, s, wm, pp);
       tm.mark("expert_dgrad1", s);
     }
   }
@@ -435,6 +442,11 @@ void Layer::combine(const LayerIO& io, cudaStream_t s) {
   ca.idx = b.idx;
   ca.gate = b.gate;
   ca.O = peers(O_);
+  ca.o_home = ep_ ? 1 : 0;  // expert parallel: fwd2 already stored O into this rank's layout
+  if (ep_) {
+    ca.O = PeerBufs{};
+    ca.O.p[0] = O_;  // local pointer (peers() maps rank r -> rank r's copy)
+  }
   ca.y = io.y;
   ca.y_hat = io.y_hat;
   ca.dO = peers(dO_);
@@ -475,14 +487,17 @@ void Layer::gate_backward(const LayerIO& io, cudaStream_t s) {
   gate_dw(io.x, dz_, c.P, c.S, c.d, n64_, n_pad_, c.N, dw_part_, dw_splits_, io.dwg, s);
   tm.mark("gate_dw", s);
   if (c.need_dx) {
-    gate_dx(dz_, io.wg, c.P, c.S, c.d, n64_, n_pad_, peers(dxp_), b.pos, b.idx, map_, c.k, io.dx, s);
+    // expert-path gradients are in this rank's layout (pushed back by the owners' dgrad1 in EP)
+    PeerBufs home{};
+    home.p[0] = dxp_;
+    gate_dx(dz_, io.wg, c.P, c.S, c.d, n64_, n_pad_, home, b.pos, b.idx, RowMap{}, c.k, io.dx, s);
     tm.mark("gate_dx", s);
   }
 }
 
 int Layer::launches_per_step() const {
   // gate, scan, bucket, capacity, permute, combine, dz, dW GEMM + reduce
-  int n = 9 + (ep_ ? 1 : 0);  // + the device plan kernel
+  int n = 10 + (ep_ ? 2 : 0);  // gate = logits GEMM + router; EP: + plan and return-map kernels
   n += cfg_.f == 0 ? (1 + 1 + (cfg_.need_dx ? 1 : 0)) : (2 + 3 + (cfg_.need_dx ? 1 : 0));
   if (cfg_.need_dx) n += 1;
   return n;

@@ -46,6 +46,34 @@ __global__ void a2a_kernel(const uint4* __restrict__ src, uint4** dsts, int P, i
   }
 }
 
+// Segmented all-to-all: rows of `row_bytes` (2 KB, like a d=1024 bf16 token row), each warp moves `seg` bytes
+// of 32 consecutive rows per step (lane-quarter groups of 16 B), i.e. what a GEMM epilogue chunk can push or
+// pull.  push = local smem-like source -> peer rows; pull = peer rows -> local.
+__global__ void seg_kernel(const uint4* __restrict__ src, uint4** peers, uint4* __restrict__ local, int P, int me,
+                           long long rows_per_peer, int seg, int pull) {
+  const int lane = threadIdx.x & 31;
+  const int per_row = seg / 16;           // 16-byte pieces per row segment
+  const int rows_per_inst = 32 / per_row; // rows covered by one warp instruction
+  const long long segs_per_row = 2048 / seg;
+  const long long total = rows_per_peer * P * segs_per_row;  // (row, segment) units
+  const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  // a warp unit = 32 rows x one segment column
+  const long long units = total / 32;
+  for (long long u = warp; u < units; u += nwarps) {
+    const long long row0 = (u / segs_per_row) * 32;
+    const int sc = static_cast<int>(u % segs_per_row);
+    const int peer = static_cast<int>((row0 / rows_per_peer) % P);
+    for (int r = 0; r < 32; r += rows_per_inst) {
+      const long long row = row0 + r + lane / per_row;
+      const long long off = (row % rows_per_peer + static_cast<long long>(me) * rows_per_peer) * 128 + sc * per_row + lane % per_row;
+      const long long loc = row * 128 + sc * per_row + lane % per_row;
+      if (pull) local[loc] = peers[peer][off];
+      else peers[peer][off] = src[loc];
+    }
+  }
+}
+
 static float time_ms(cudaStream_t s, cudaEvent_t a, cudaEvent_t b) {
   float ms;
   CK(cudaEventSynchronize(b));
@@ -135,6 +163,46 @@ int main() {
     const double off = bytes * (ng - 1.0) / ng;
     printf("a2a %d GPUs grid %5d: %7.1f GB/s off-rank per GPU (%.1f us for %zu MiB/GPU)\n", ng, gi,
            off / worst / 1e6, worst * 1e3, bytes >> 20);
+  }
+  // 4) segmented all-to-all (push / pull), 64 B .. 2 KB segments
+  {
+    std::vector<uint4**> dptr(ng);
+    for (int g = 0; g < ng; ++g) {
+      CK(cudaSetDevice(g));
+      CK(cudaMalloc(&dptr[g], sizeof(uint4*) * ng));
+      CK(cudaMemcpy(dptr[g], buf2.data(), sizeof(uint4*) * ng, cudaMemcpyHostToDevice));
+    }
+    const long long rows = bytes / 2048;  // rows per GPU buffer
+    const long long rows_per_peer = rows / ng;
+    for (int pull = 0; pull < 2; ++pull)
+      for (int seg : {64, 128, 256, 512, 2048}) {
+        float worst = 0;
+        for (int it = 0; it < 3; ++it) {
+          for (int g = 0; g < ng; ++g) {
+            CK(cudaSetDevice(g));
+            CK(cudaDeviceSynchronize());
+          }
+          std::vector<cudaEvent_t> ea(ng), eb(ng);
+          for (int g = 0; g < ng; ++g) {
+            CK(cudaSetDevice(g));
+            CK(cudaEventCreate(&ea[g]));
+            CK(cudaEventCreate(&eb[g]));
+            CK(cudaEventRecord(ea[g], st[g]));
+            seg_kernel<<<1184, 512, 0, st[g]>>>(buf[g], dptr[g], pull ? buf2[g] : nullptr, ng, g, rows_per_peer,
+                                                seg < 512 ? seg : 512, pull);
+            CK(cudaEventRecord(eb[g], st[g]));
+          }
+          float mx = 0;
+          for (int g = 0; g < ng; ++g) {
+            CK(cudaSetDevice(g));
+            mx = std::max(mx, time_ms(st[g], ea[g], eb[g]));
+          }
+          if (it) worst = mx;
+        }
+        const double off = bytes * (ng - 1.0) / ng;
+        printf("seg a2a %s %4d B segments: %7.1f GB/s off-rank per GPU\n", pull ? "pull" : "push", seg < 512 ? seg : 512,
+               off / worst / 1e6);
+      }
   }
   return 0;
 }
