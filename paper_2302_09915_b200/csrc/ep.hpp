@@ -31,11 +31,25 @@ struct EpPlanDev {
   int* seg_rows = nullptr;    // [E]
   int* dst_off = nullptr;     // [N] where this rank's rows for global expert e start at the owner
   int* recv_rows = nullptr;   // [1]
-  int* flag = nullptr;        // [1] barrier scratch
+  int* flag = nullptr;        // [1] NCCL barrier scratch (TAMOE_NCCL_BARRIER=1)
   int* push_row = nullptr;    // [rows] receive row -> (source rank << 27 | row in the source's local layout)
 };
 
 void ep_plan_device(const EpPlanDev& plan, int P, int E, int me, cudaStream_t s);
+
+// Device-side barrier over the peer-mapped workspaces (no NCCL on the step path): every rank stores a
+// monotonically increasing epoch into every rank's signal slot `me` (st.release.sys) and spins on its own
+// slots (ld.acquire.sys) until all peers reached the same epoch.  With `my_counts` it first stores this
+// rank's kept counts into row `me` of every rank's all_counts -- the counts all-gather folded into the
+// barrier.  A peer that never arrives traps the kernel after 20 s instead of hanging the GPU.
+struct EpSignal {
+  unsigned int* sig[kMaxRanks];  // every rank's signal slots [kMaxRanks]
+  unsigned int* epoch;           // this rank's barrier counter
+  int* counts_dst[kMaxRanks];    // every rank's all_counts [P x N]
+  const int* my_counts;          // null: plain barrier
+  int P, me, N;
+};
+void ep_signal_barrier(const EpSignal& a, cudaStream_t s);
 
 class EpComm {
  public:

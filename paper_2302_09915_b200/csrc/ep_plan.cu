@@ -54,7 +54,54 @@ __global__ void ep_push_map_kernel(EpPlanDev p, int P, int E, int me) {
   for (int r = threadIdx.x; r < rows; r += blockDim.x) p.push_row[s_dst + r] = (i << 27) | (s_src + r);
 }
 
+__device__ __forceinline__ void st_release_sys(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void ep_barrier_kernel(const __grid_constant__ EpSignal a) {
+  if (a.my_counts) {
+    for (int i = threadIdx.x; i < a.P * a.N; i += blockDim.x) {
+      const int r = i / a.N, e = i - r * a.N;
+      a.counts_dst[r][a.me * a.N + e] = a.my_counts[e];
+    }
+  }
+  __threadfence_system();  // this kernel's stores (and, by kernel order, earlier kernels') before the signal
+  __shared__ unsigned int ep;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ep = *a.epoch + 1u;
+    *a.epoch = ep;
+  }
+  __syncthreads();
+  const int r = threadIdx.x;
+  if (r < a.P) {
+    st_release_sys(a.sig[r] + a.me, ep);
+    const unsigned int* mine = a.sig[a.me] + r;
+    const unsigned long long t0 = global_ns();
+    // a peer may already be one barrier ahead (it can only pass `ep` after our signal): compare mod 2^32
+    while (static_cast<int>(ld_acquire_sys(mine) - ep) < 0) {
+      if (global_ns() - t0 > 20000000000ull) __trap();
+    }
+  }
+  __syncthreads();
+}
+
 }  // namespace
+
+void ep_signal_barrier(const EpSignal& a, cudaStream_t s) {
+  ep_barrier_kernel<<<1, 256, 0, s>>>(a);
+  TAMOE_CUDA(cudaGetLastError());
+}
 
 void ep_plan_device(const EpPlanDev& plan, int P, int E, int me, cudaStream_t s) {
   require(P >= 1 && P <= kMaxRanks, "expert parallelism supports up to 16 ranks");

@@ -176,6 +176,8 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
     arena_.reserve(plan_.recv_rows, 1);
     arena_.reserve(plan_.flag, 1);
     arena_.reserve(plan_.push_row, r_max_);
+    arena_.reserve(sig_slots_, kMaxRanks);
+    arena_.reserve(sig_epoch_, 1);
   }
   arena_.reserve(dz_, T * n64_);
   arena_.reserve(logits_, T * c.N);
@@ -187,8 +189,22 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
   arena_.reserve(loss_part_, n_loss_part_);
   arena_.commit();
   if (ep_) {
+    // barrier slots start at zero on every rank before any peer can signal: the memset is stream-ordered
+    // before this rank's contribution to the handle all-gather that every peer waits for
+    TAMOE_CUDA(cudaMemset(sig_slots_, 0, sizeof(unsigned int) * kMaxRanks));
+    TAMOE_CUDA(cudaMemset(sig_epoch_, 0, sizeof(unsigned int)));
     // every rank's arena has the same layout: map them all into this process (CUDA IPC over NVLink)
     ep_->map_peers(arena_.base(), bases_);
+    sig_.P = c.world_size;
+    sig_.me = c.rank;
+    sig_.N = c.N;
+    sig_.epoch = sig_epoch_;
+    const long long soff = reinterpret_cast<char*>(sig_slots_) - arena_.base();
+    const long long coff = reinterpret_cast<char*>(plan_.all_counts) - arena_.base();
+    for (int j = 0; j < c.world_size; ++j) {
+      sig_.sig[j] = reinterpret_cast<unsigned int*>(bases_[j] + soff);
+      sig_.counts_dst[j] = reinterpret_cast<int*>(bases_[j] + coff);
+    }
     map_.P = c.world_size;
     map_.E = E;
     map_.local_start = rw_.buf.seg_start;
@@ -407,27 +423,48 @@ void Layer::step_ep(const LayerIO& io, cudaStream_t s) {
   const int W = c.world_size, E = c.N / W;
   tm.begin(s);
   route_front(*this, rw_, tm, io, n_pad_, c.d, c.cap_mode, logits_, s);
-  ep_->allgather_counts(b.counts, plan_.all_counts, c.N, s);  // also: every rank finished its previous step
+  ep_barrier(s, true);  // counts all-gather; also: every rank finished its previous step
   ep_plan_device(plan_, W, E, c.rank, s);
   tm.mark("a2a_counts", s);
   // fused permute + dispatch: rows (and the owners' zero pad rows of dO) stored straight into the owners
   const PeerBufs zb = peers(dO_);
   route_permute(rw_.dims, b, io.x, c.d, peers(xp_), r_local_, &zb, c.d_out, map_, s);
-  ep_->barrier(plan_.flag, s);
+  ep_barrier(s, false);
   tm.mark("a2a_dispatch", s);
   experts_forward(io, E, E, 1, plan_.seg_start, plan_.seg_rows, r_max_, s);
-  ep_->barrier(plan_.flag, s);
+  ep_barrier(s, false);
   tm.mark("a2a_barrier_fwd", s);
   combine(io, s);  // loads expert outputs from the owners, stores dO into the owners
-  ep_->barrier(plan_.flag, s);
+  ep_barrier(s, false);
   tm.mark("a2a_barrier_combine", s);
   experts_backward(io, E, E, 1, plan_.seg_start, plan_.seg_rows, r_max_, s);
   if (c.need_dx) {
-    ep_->barrier(plan_.flag, s);
+    ep_barrier(s, false);
     tm.mark("a2a_barrier_bwd", s);
   }
   gate_backward(io, s);  // the dX epilogue loads the expert-path gradients from the owners
   tm.end(s);
+}
+
+static bool nccl_barrier() {
+  static const bool on = [] {
+    const char* v = std::getenv("TAMOE_NCCL_BARRIER");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
+// Phase barrier of the expert-parallel step: device signal slots over NVLink by default,
+// NCCL (all-gather of counts / 1-int all-reduce) with TAMOE_NCCL_BARRIER=1.
+void Layer::ep_barrier(cudaStream_t s, bool publish_counts) {
+  if (nccl_barrier()) {
+    if (publish_counts) ep_->allgather_counts(rw_.buf.counts, plan_.all_counts, cfg_.N, s);
+    else ep_->barrier(plan_.flag, s);
+    return;
+  }
+  EpSignal a = sig_;
+  a.my_counts = publish_counts ? rw_.buf.counts : nullptr;
+  ep_signal_barrier(a, s);
 }
 
 void Layer::combine(const LayerIO& io, cudaStream_t s) {
@@ -497,7 +534,9 @@ void Layer::gate_backward(const LayerIO& io, cudaStream_t s) {
 
 int Layer::launches_per_step() const {
   // gate, scan, bucket, capacity, permute, combine, dz, dW GEMM + reduce
-  int n = 10 + (ep_ ? 2 : 0);  // gate = logits GEMM + router; EP: + plan and return-map kernels
+  int n = 10;  // gate = logits GEMM + router
+  // EP: + plan and return-map kernels + the device barriers (counts publish, dispatch, forward, combine, [dX])
+  if (ep_) n += 2 + (nccl_barrier() ? 0 : 4 + (cfg_.need_dx ? 1 : 0));
   n += cfg_.f == 0 ? (1 + 1 + (cfg_.need_dx ? 1 : 0)) : (2 + 3 + (cfg_.need_dx ? 1 : 0));
   if (cfg_.need_dx) n += 1;
   return n;

@@ -141,6 +141,10 @@ class Layer {
   std::unique_ptr<EpComm> ep_;
   // expert parallelism: device plan, peer-mapped arena bases, row map
   EpPlanDev plan_{};
+  EpSignal sig_{};                   // device barrier (counts publish + phase barriers)
+  unsigned int* sig_slots_ = nullptr;  // [kMaxRanks] in the peer-mapped arena
+  unsigned int* sig_epoch_ = nullptr;
+  void ep_barrier(cudaStream_t s, bool publish_counts);
   std::vector<char*> bases_;
   RowMap map_{};
   int r_local_ = 0;  // rows of this rank's own padded layout
