@@ -206,8 +206,9 @@ struct GateDxParams {
   int k, S, d;
 };
 
-// KT = compile-time top-k (0: runtime k).  The expert-path rows of every chunk this warp stores are
-// gathered into registers before the first accumulator load, so their latency overlaps.
+// KT = compile-time top-k (0: runtime k).  Warp h of a lane quarter owns the contiguous column half
+// [128h, 128h + 128) of the tile, so each lane gathers 256 contiguous bytes of every expert-path row it
+// needs -- all of them into registers before the first accumulator load, so their latency overlaps.
 template <int KT>
 struct EpiGateDx {
   using Params = GateDxParams;
@@ -250,11 +251,11 @@ struct EpiGateDx {
         for (int c = 0; c < kCh; ++c)
 #pragma unroll
           for (int u = 0; u < 4; ++u)
-            g[j][c][u] = srcs[j] ? reinterpret_cast<const uint4*>(srcs[j] + ti.n0 + 32 * h + 64 * c)[u]
+            g[j][c][u] = srcs[j] ? reinterpret_cast<const uint4*>(srcs[j] + ti.n0 + 128 * h + 32 * c)[u]
                                  : make_uint4(0, 0, 0, 0);
 #pragma unroll
       for (int c = 0; c < kCh; ++c) {
-        const int c0 = 32 * h + 64 * c;
+        const int c0 = 128 * h + 32 * c;
         float v[32];
         load_acc32(tmem_tile, c0, v);
 #pragma unroll
@@ -265,7 +266,7 @@ struct EpiGateDx {
         store32(e, gtok, ti.n0 + c0, v);
       }
     } else {
-      for (int c0 = 32 * h; c0 < ti.n; c0 += 64) {
+      for (int c0 = 128 * h; c0 < min(ti.n, 128 * h + 128); c0 += 32) {
         float v[32];
         load_acc32(tmem_tile, c0, v);
 #pragma unroll

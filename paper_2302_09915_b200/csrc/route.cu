@@ -343,7 +343,17 @@ __global__ void __launch_bounds__(kPermWarps * 32) route_permute_kernel(RouteDim
     const long long tok = pick / d.k;
     if (lane == 0) b.pos[pick] = r;
     const uint4* src = reinterpret_cast<const uint4*>(x + tok * dx);
-    for (int v = lane; v < nv; v += 32) dst[v] = src[v];
+    // whole row in registers first (up to 8 x 16 B per lane), then the stores back to back
+    constexpr int kU = 8;
+    for (int v0 = lane; v0 < nv; v0 += 32 * kU) {
+      uint4 t[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (v0 + 32 * u < nv) t[u] = __ldg(src + v0 + 32 * u);
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (v0 + 32 * u < nv) dst[v0 + 32 * u] = t[u];
+    }
   } else {
     const uint4 z = make_uint4(0, 0, 0, 0);
     for (int v = lane; v < nv; v += 32) dst[v] = z;
