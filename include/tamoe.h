@@ -67,6 +67,38 @@ int tamoe_capacity_caps(int mode, double capacity_factor, int k, int S, int N, i
 /* device_payload_tokens (dispatch.cpp:21-26): payload[P x P] = sum of counts[i][e] over experts of j. */
 int tamoe_device_payload_tokens(const double* counts, int P, int N, double* payload);
 
+/* ------------------------------------------------------------------ measured-topology pipeline (host)
+ * Symmetric switch trees are passed as their level vector, root first: {8} = one switch, {2,4} = two
+ * groups of four (topology.hpp:28-33).  n_levels = 0 means "no topology".  Matrices are P x P row-major,
+ * alpha in us, beta in us per decimal MB; NaN marks an unmeasured link. */
+
+/* fit_profile (comm_cost.cpp:57-104 / comm_cost.hpp:44-50): per ordered pair least squares
+ * time_us = alpha + beta * message_mb over its samples (TransferSample, profile_io.hpp:8-13). */
+int tamoe_fit_profile(const int* src, const int* dst, const double* message_mb, const double* time_us, int n,
+                      int P, double* alpha, double* beta);
+
+/* fill_partial_profile (profile.cpp:164-233 / profile.hpp:47-52). */
+int tamoe_fill_partial_profile(const double* alpha, const double* beta, int P, const int* levels, int n_levels,
+                               double self_beta_floor, double* alpha_out, double* beta_out);
+
+/* smooth_profile (profile.cpp:46-98 / profile.hpp:33): level means over a symmetric tree -> alpha_hat,
+ * beta_hat (P x P); level_alpha / level_beta (optional, n_levels entries: one per switch-distance group). */
+int tamoe_smooth_profile(const int* levels, int n_levels, const double* alpha, const double* beta, int P,
+                         double self_beta_floor, double* alpha_hat, double* beta_hat, double* level_alpha,
+                         double* level_beta);
+
+/* NVLink point-to-point sweep (device, collective over `world` processes, one GPU each; the caller has
+ * selected its device).  Every ordered pair (src, dst) incl. src == dst and every message size is timed
+ * `reps` times (after `warmup`) as one SM-driven peer copy, CUDA events on the source rank.
+ * time_us[src][dst][size][rep] is filled on every rank -> TransferSample rows for tamoe_fit_profile. */
+int tamoe_p2p_sweep(const void* nccl_id128, int world, int rank, const double* sizes_mb, int nsizes, int reps,
+                    int warmup, double* time_us);
+
+/* exchange_cost (comm_cost.cpp:24-55): c = dispatch matrix [P x N] tokens, payload d * b bytes per token.
+ * pair_cost_us[P x P] (optional); summary[4] = bottleneck_us, total_bytes, size_exchange_us, total_estimate_us. */
+int tamoe_exchange_cost(const double* alpha, const double* beta, const double* c, int P, int N, int d, int b,
+                        int extra_alpha_rounds, double* pair_cost_us, double* summary);
+
 /* ------------------------------------------------------------------ grouped expert GEMMs (device)
  * Building blocks of the expert FFN (trainer.cpp:284-289 / 310-316 generalised).
  * tokens are bf16 [R x K] row-major; group g owns rows [seg_start[g], seg_start[g]+seg_rows[g]),

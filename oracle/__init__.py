@@ -225,6 +225,47 @@ class Reference(_Common):
         self.lib.ref_rng_normal.argtypes = [c_ulonglong, c_int, c_double, _D]
         self.lib.ref_rng_uniform.argtypes = [c_ulonglong, c_int, c_double, c_double, _D]
 
+    # ---- measured-topology pipeline
+    def fit_profile(self, samples, P):
+        arr = np.asarray(list(samples), dtype=np.float64).reshape(-1, 4)
+        src = np.ascontiguousarray(arr[:, 0], np.int32)
+        dst = np.ascontiguousarray(arr[:, 1], np.int32)
+        mb, us = f64(arr[:, 2]), f64(arr[:, 3])
+        a, b = np.zeros((P, P)), np.zeros((P, P))
+        self._chk(self.lib.ref_fit_profile(_ip(src), _ip(dst), _dp(mb), _dp(us), int(arr.shape[0]), P, _dp(a), _dp(b)))
+        return a, b
+
+    def fill_partial_profile(self, alpha, beta, levels=None, floor=0.1):
+        a, b = f64(alpha), f64(beta)
+        P = a.shape[0]
+        lv = np.ascontiguousarray(levels if levels is not None else [0], np.int32)
+        ao, bo = np.zeros((P, P)), np.zeros((P, P))
+        self._chk(self.lib.ref_fill_partial_profile(_dp(a), _dp(b), P, _ip(lv), 0 if levels is None else len(lv),
+                                                      c_double(floor), _dp(ao), _dp(bo)))
+        return ao, bo
+
+    def smooth_profile(self, levels, alpha, beta, floor=0.1):
+        a, b = f64(alpha), f64(beta)
+        P = a.shape[0]
+        lv = np.ascontiguousarray(levels, np.int32)
+        ah, bh = np.zeros((P, P)), np.zeros((P, P))
+        self._chk(self.lib.ref_smooth_profile(_ip(lv), len(lv), _dp(a), _dp(b), P, c_double(floor), _dp(ah), _dp(bh)))
+        return ah, bh
+
+    def device_groups(self, levels, device, P):
+        lv = np.ascontiguousarray(levels, np.int32)
+        g = np.full(P, -1, np.int32)
+        self._chk(self.lib.ref_device_groups(_ip(lv), len(lv), device, _ip(g)))
+        return g
+
+    def exchange_cost(self, alpha, beta, c, d, b=2, rounds=0):
+        a, bb, cc = f64(alpha), f64(beta), f64(c)
+        P, N = cc.shape
+        pc, summ = np.zeros((P, P)), np.zeros(4)
+        self._chk(self.lib.ref_exchange_cost(_dp(a), _dp(bb), _dp(cc), P, N, d, b, rounds, _dp(pc), _dp(summ)))
+        return dict(pair_cost_us=pc, bottleneck_us=summ[0], total_bytes=summ[1], size_exchange_us=summ[2],
+                    total_estimate_us=summ[3])
+
     def rng_normal(self, seed, n, scale=1.0):
         out = np.zeros(n)
         self.lib.ref_rng_normal(seed, n, scale, _dp(out))

@@ -9,8 +9,12 @@
 #include <string>
 #include <vector>
 
+#include "tadispatch/comm_cost.hpp"
 #include "tadispatch/errors.hpp"
 #include "tadispatch/gate.hpp"
+#include "tadispatch/profile.hpp"
+#include "tadispatch/profile_io.hpp"
+#include "tadispatch/topology.hpp"
 #include "tadispatch/rng.hpp"
 #include "tadispatch/solver.hpp"
 #include "tadispatch/trainer.hpp"
@@ -221,6 +225,79 @@ int ref_train(int P, int S, int d, int d_out, int N, int k, const double* x, con
     }
     if (initial_dispatch) from_matrix(rep.initial_dispatch, initial_dispatch);
     if (final_dispatch) from_matrix(rep.final_dispatch, final_dispatch);
+  });
+}
+
+// ---- measured-topology pipeline (comm_cost.cpp, profile.cpp, topology.cpp)
+static Topology tree_from_levels(const int* levels, int n_levels) {
+  std::string t = "[";
+  for (int i = 0; i < n_levels; ++i) t += (i ? "," : "") + std::to_string(levels[i]);
+  return parse_topology(t + "]");
+}
+
+int ref_fit_profile(const int* src, const int* dst, const double* mb, const double* us, int n, int P, double* alpha,
+                    double* beta) {
+  return guard([&] {
+    std::vector<TransferSample> smp;
+    for (int i = 0; i < n; ++i) smp.push_back({src[i], dst[i], mb[i], us[i]});
+    FittedProfile f = fit_profile(smp, P);
+    std::memcpy(alpha, f.alpha.data().data(), sizeof(double) * P * P);
+    std::memcpy(beta, f.beta.data().data(), sizeof(double) * P * P);
+  });
+}
+
+int ref_fill_partial_profile(const double* alpha, const double* beta, int P, const int* levels, int n_levels,
+                             double floor, double* alpha_out, double* beta_out) {
+  return guard([&] {
+    Topology topo;
+    if (n_levels > 0) topo = tree_from_levels(levels, n_levels);
+    LinkProfile lp = fill_partial_profile(to_matrix(alpha, P, P), to_matrix(beta, P, P),
+                                          n_levels > 0 ? &topo : nullptr, floor);
+    std::memcpy(alpha_out, lp.alpha.data().data(), sizeof(double) * P * P);
+    std::memcpy(beta_out, lp.beta.data().data(), sizeof(double) * P * P);
+  });
+}
+
+int ref_smooth_profile(const int* levels, int n_levels, const double* alpha, const double* beta, int P, double floor,
+                       double* alpha_hat, double* beta_hat) {
+  return guard([&] {
+    Topology topo = tree_from_levels(levels, n_levels);
+    LinkProfile raw;
+    raw.alpha = to_matrix(alpha, P, P);
+    raw.beta = to_matrix(beta, P, P);
+    raw.self_beta_floor = floor;
+    HierarchicalProfile h = smooth_profile(topo, raw);
+    std::memcpy(alpha_hat, h.alpha_hat.data().data(), sizeof(double) * P * P);
+    std::memcpy(beta_hat, h.beta_hat.data().data(), sizeof(double) * P * P);
+  });
+}
+
+int ref_device_groups(const int* levels, int n_levels, int device, int* group_of /* [P] */) {
+  return guard([&] {
+    Topology topo = tree_from_levels(levels, n_levels);
+    auto g = device_groups(topo, device);
+    for (size_t l = 0; l < g.size(); ++l)
+      for (int j : g[l]) group_of[j] = static_cast<int>(l);
+  });
+}
+
+int ref_exchange_cost(const double* alpha, const double* beta, const double* c, int P, int N, int d, int b,
+                      int rounds, double* pair_cost, double* summary) {
+  return guard([&] {
+    DispatchMatrix dm;
+    dm.config.P = P;
+    dm.config.N = N;
+    dm.config.d = d;
+    dm.config.b = b;
+    dm.config.k = 1;
+    dm.config.S = 1;
+    dm.c = to_matrix(c, P, N);
+    CostReport r = exchange_cost(to_matrix(alpha, P, P), to_matrix(beta, P, P), dm, rounds);
+    std::memcpy(pair_cost, r.pair_cost_us.data().data(), sizeof(double) * P * P);
+    summary[0] = r.bottleneck_us;
+    summary[1] = r.total_bytes;
+    summary[2] = r.size_exchange_us;
+    summary[3] = r.total_estimate_us;
   });
 }
 

@@ -36,6 +36,7 @@ lib = _load()
 _P = c_void_p
 _D = POINTER(c_double)
 _L = POINTER(c_longlong)
+_I = POINTER(ctypes.c_int)
 
 # name -> argtypes (restype is always int status except where noted)
 SIGNATURES = {
@@ -44,6 +45,11 @@ SIGNATURES = {
     "tamoe_target_closed_form": [_D, c_int, c_int, c_int, c_int, _D],
     "tamoe_capacity_caps": [c_int, c_double, c_int, c_int, c_int, c_int, _D, _L],
     "tamoe_device_payload_tokens": [_D, c_int, c_int, _D],
+    "tamoe_fit_profile": [_I, _I, _D, _D, c_int, c_int, _D, _D],
+    "tamoe_fill_partial_profile": [_D, _D, c_int, _I, c_int, c_double, _D, _D],
+    "tamoe_smooth_profile": [_I, c_int, _D, _D, c_int, c_double, _D, _D, _D, _D],
+    "tamoe_exchange_cost": [_D, _D, _D, c_int, c_int, c_int, c_int, c_int, _D, _D],
+    "tamoe_p2p_sweep": [_P, c_int, c_int, _D, c_int, c_int, c_int, _D],
     "tamoe_grouped_fwd": [_P, _P, c_int, c_int, c_int, c_int, _P, _P, _P, _P, c_int, _P],
     "tamoe_grouped_dgrad": [_P, _P, c_int, c_int, c_int, c_int, _P, _P, _P, _P, c_int, _P],
     "tamoe_grouped_wgrad": [_P, _P, c_int, c_int, c_int, c_int, _P, _P, _P, _P],

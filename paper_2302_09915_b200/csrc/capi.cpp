@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <memory>
 #include <string>
+#include <vector>
 #include <cstring>
 
 #include "capi_util.hpp"
@@ -122,6 +123,47 @@ int tamoe_device_payload_tokens(const double* counts, int P, int N, double* payl
   });
 }
 
+int tamoe_fit_profile(const int* src, const int* dst, const double* message_mb, const double* time_us, int n,
+                      int P, double* alpha, double* beta) {
+  return guarded([&] {
+    require(src && dst && message_mb && time_us && alpha && beta, "fit_profile: null buffer");
+    fit_profile(src, dst, message_mb, time_us, n, P, alpha, beta);
+  });
+}
+
+int tamoe_fill_partial_profile(const double* alpha, const double* beta, int P, const int* levels, int n_levels,
+                               double self_beta_floor, double* alpha_out, double* beta_out) {
+  return guarded([&] {
+    require(alpha && beta && alpha_out && beta_out, "fill_partial_profile: null buffer");
+    fill_partial_profile(alpha, beta, P, levels, n_levels, self_beta_floor, alpha_out, beta_out);
+  });
+}
+
+int tamoe_smooth_profile(const int* levels, int n_levels, const double* alpha, const double* beta, int P,
+                         double self_beta_floor, double* alpha_hat, double* beta_hat, double* level_alpha,
+                         double* level_beta) {
+  return guarded([&] {
+    require(alpha && beta && alpha_hat && beta_hat, "smooth_profile: null buffer");
+    std::vector<double> la, lb;
+    smooth_profile(levels, n_levels, alpha, beta, P, self_beta_floor, alpha_hat, beta_hat, &la, &lb);
+    if (level_alpha) std::copy(la.begin(), la.end(), level_alpha);
+    if (level_beta) std::copy(lb.begin(), lb.end(), level_beta);
+  });
+}
+
+int tamoe_exchange_cost(const double* alpha, const double* beta, const double* c, int P, int N, int d, int b,
+                        int extra_alpha_rounds, double* pair_cost_us, double* summary) {
+  return guarded([&] {
+    require(alpha && beta && c && summary, "exchange_cost: null buffer");
+    const ExchangeCost r = exchange_cost(alpha, beta, c, P, N, d, b, extra_alpha_rounds);
+    if (pair_cost_us) std::copy(r.pair_cost_us.begin(), r.pair_cost_us.end(), pair_cost_us);
+    summary[0] = r.bottleneck_us;
+    summary[1] = r.total_bytes;
+    summary[2] = r.size_exchange_us;
+    summary[3] = r.total_estimate_us;
+  });
+}
+
 int tamoe_grouped_fwd(const void* tokens, const void* w, int G, int M, int K, int R, const int* seg_start,
                       const int* seg_rows, void* out, void* pre_out, int act, void* stream) {
   return guarded([&] {
@@ -210,6 +252,20 @@ int tamoe_layer_create(const tamoe_layer_config* cfg, const double* c_hat, tamoe
                   cfg->capacity_factor, cfg->aux_kind, cfg->aux_weight, cfg->penalty_norm, cfg->temperature,
                   cfg->need_dx, cfg->world_size, cfg->rank};
     *out = new tamoe_layer(c, c_hat);
+  });
+}
+
+int tamoe_p2p_sweep(const void* nccl_id128, int world, int rank, const double* sizes_mb, int nsizes, int reps,
+                    int warmup, double* time_us) {
+  return guarded([&] {
+    require(nccl_id128 && sizes_mb && time_us, "p2p_sweep: null argument");
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id128, sizeof(id));
+    double max_mb = 0.0;
+    for (int i = 0; i < nsizes; ++i) max_mb = std::max(max_mb, sizes_mb[i]);
+    P2PProbe probe(world, rank, id, (static_cast<size_t>(max_mb * 1e6) + 4095) & ~static_cast<size_t>(4095));
+    const std::vector<double> t = probe.sweep(sizes_mb, nsizes, reps, warmup);
+    std::memcpy(time_us, t.data(), sizeof(double) * t.size());
   });
 }
 

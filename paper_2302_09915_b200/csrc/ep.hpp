@@ -61,6 +61,8 @@ class EpComm {
   void allgather_counts(const int* my_counts, int* all_counts, int N, cudaStream_t s);
   // all ranks' streams reach this point before any proceeds (1-int all-reduce)
   void barrier(int* flag, cudaStream_t s);
+  void allreduce_sum(double* buf, size_t n, cudaStream_t s);
+  void close_peers();  // unmap every peer allocation opened by map_peers
   // map every rank's `local_base` allocation (cudaMalloc'd) into this process; bases[j] = rank j's
   void map_peers(void* local_base, std::vector<char*>& bases);
 
@@ -69,6 +71,28 @@ class EpComm {
   ncclComm_t comm_ = nullptr;
   std::vector<void*> opened_;
 };
+
+// NVLink point-to-point sweep feeding the measured-topology pipeline: every ordered
+// pair (src, dst), src == dst included, and every message size is timed `reps` times as one SM-driven peer
+// copy -- the mechanism the dispatch uses -- with CUDA events on the source rank while the other ranks idle
+// between stream barriers.  Result on every rank: time_us[src][dst][size][rep] (the reference's
+// TransferSample rows, profile_io.hpp:8-13; alpha then absorbs the launch latency).
+class P2PProbe {
+ public:
+  P2PProbe(int world, int rank, const ncclUniqueId& id, size_t max_bytes);
+  ~P2PProbe();
+  std::vector<double> sweep(const double* sizes_mb, int nsizes, int reps, int warmup);
+
+ private:
+  EpComm comm_;
+  size_t max_bytes_;
+  char* buf_ = nullptr;  // [src half | dst half]
+  std::vector<char*> bases_;
+  cudaStream_t stream_ = nullptr;
+  int* flag_ = nullptr;
+};
+
+void p2p_copy(void* dst, const void* src, size_t bytes, cudaStream_t s);
 
 // Host reference of the receive plan (CPU-testable): recv[src][e] (P x E) rows -> per local expert the
 // segment seg_start/seg_rows [E] and the row where each source's rows for it start, src_off [P x E].

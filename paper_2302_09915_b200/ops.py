@@ -78,6 +78,108 @@ def target_closed_form(beta_hat, N: int, k: int, S: int) -> np.ndarray:
     return out
 
 
+# ------------------------------------------------------------------ measured-topology pipeline (§8(f) row 1)
+DEFAULT_SELF_BETA_FLOOR = 0.1  # us/MB, profile.hpp:8
+
+
+def _i32(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+def _levels(levels):
+    if levels is None:
+        return None, 0
+    lv = _i32(levels)
+    return lv, int(lv.size)
+
+
+def fit_profile(samples, P: int):
+    """fit_profile (comm_cost.cpp:57-104).  samples: iterable of (src, dst, message_mb, time_us) rows (the
+    reference's TransferSample / samples CSV).  Returns (alpha, beta) P x P, NaN for unmeasured pairs."""
+    arr = np.asarray(list(samples), dtype=np.float64).reshape(-1, 4)
+    src, dst = _i32(arr[:, 0]), _i32(arr[:, 1])
+    mb, us = _f64(arr[:, 2]), _f64(arr[:, 3])
+    alpha, beta = np.zeros((P, P)), np.zeros((P, P))
+    _lib.call("tamoe_fit_profile", src.ctypes.data_as(_lib._I), dst.ctypes.data_as(_lib._I), mb.ctypes.data_as(_D),
+              us.ctypes.data_as(_D), int(arr.shape[0]), P, alpha.ctypes.data_as(_D), beta.ctypes.data_as(_D))
+    return alpha, beta
+
+
+def fill_partial_profile(alpha, beta, levels=None, self_beta_floor=DEFAULT_SELF_BETA_FLOOR):
+    """fill_partial_profile (profile.cpp:164-233); levels = symmetric tree level vector (root first) or None."""
+    a, b = _f64(alpha), _f64(beta)
+    P = a.shape[0]
+    lv, nl = _levels(levels)
+    ao, bo = np.zeros((P, P)), np.zeros((P, P))
+    _lib.call("tamoe_fill_partial_profile", a.ctypes.data_as(_D), b.ctypes.data_as(_D), P,
+              lv.ctypes.data_as(_lib._I) if lv is not None else None, nl, float(self_beta_floor),
+              ao.ctypes.data_as(_D), bo.ctypes.data_as(_D))
+    return ao, bo
+
+
+def smooth_profile(levels, alpha, beta, self_beta_floor=DEFAULT_SELF_BETA_FLOOR):
+    """smooth_profile (profile.cpp:46-98) over a symmetric tree -> (alpha_hat, beta_hat, level_alpha, level_beta)."""
+    a, b = _f64(alpha), _f64(beta)
+    P = a.shape[0]
+    lv, nl = _levels(levels)
+    ah, bh = np.zeros((P, P)), np.zeros((P, P))
+    la, lb = np.full(nl, np.nan), np.full(nl, np.nan)
+    _lib.call("tamoe_smooth_profile", lv.ctypes.data_as(_lib._I), nl, a.ctypes.data_as(_D), b.ctypes.data_as(_D), P,
+              float(self_beta_floor), ah.ctypes.data_as(_D), bh.ctypes.data_as(_D), la.ctypes.data_as(_D),
+              lb.ctypes.data_as(_D))
+    keep = ~np.isnan(la)
+    return ah, bh, la[keep], lb[keep]
+
+
+def exchange_cost(alpha, beta, c, d: int, b: int = 2, extra_alpha_rounds: int = 0) -> dict:
+    """exchange_cost (comm_cost.cpp:24-55): alpha-beta cost of one exchange of dispatch matrix c [P x N]."""
+    a, bb, cc = _f64(alpha), _f64(beta), _f64(c)
+    P, N = cc.shape
+    pc, summ = np.zeros((P, P)), np.zeros(4)
+    _lib.call("tamoe_exchange_cost", a.ctypes.data_as(_D), bb.ctypes.data_as(_D), cc.ctypes.data_as(_D), P, N, d, b,
+              extra_alpha_rounds, pc.ctypes.data_as(_D), summ.ctypes.data_as(_D))
+    return dict(pair_cost_us=pc, bottleneck_us=summ[0], total_bytes=summ[1], size_exchange_us=summ[2],
+                total_estimate_us=summ[3])
+
+
+def p2p_sweep(nccl_id: bytes, world: int, rank: int, sizes_mb=(1.0, 4.0, 16.0, 64.0, 128.0), reps: int = 5,
+              warmup: int = 2):
+    """Measured transfers between every ordered pair of the `world` GPUs (collective; call on every rank with
+    the same arguments after torch.cuda.set_device).  Returns TransferSample rows (src, dst, message_mb,
+    time_us) -- the samples CSV of the reference (profile_io.hpp:8-13)."""
+    sz = _f64(list(sizes_mb))
+    out = np.zeros((world, world, sz.size, reps))
+    idb = ctypes.create_string_buffer(bytes(nccl_id), 128)
+    _lib.call("tamoe_p2p_sweep", idb, world, rank, sz.ctypes.data_as(_D), int(sz.size), reps, warmup,
+              out.ctypes.data_as(_D))
+    return [(i, j, float(sz[s]), float(out[i, j, s, r])) for i in range(world) for j in range(world)
+            for s in range(sz.size) for r in range(reps)]
+
+
+def solve_target_tree(levels, alpha, beta, N: int, k: int, S: int, self_beta_floor=DEFAULT_SELF_BETA_FLOOR):
+    """solve_target for a symmetric tree (solver.cpp:119-150, closed-form branch): smooth, then Eq. 8 on
+    beta_hat.  Returns (c_hat [P x N], alpha_hat, beta_hat)."""
+    ah, bh, _, _ = smooth_profile(levels, alpha, beta, self_beta_floor)
+    return target_closed_form(bh, N, k, S), ah, bh
+
+
+def load_samples_csv(path):
+    """Samples CSV of the reference (profile_io.cpp: header src,dst,message_mb,time_us)."""
+    with open(path) as f:
+        head = f.readline().strip()
+        if head != "src,dst,message_mb,time_us":
+            raise ValidationError(f"expected CSV header 'src,dst,message_mb,time_us', got '{head}'")
+        rows = [tuple(float(v) for v in line.split(",")) for line in f if line.strip()]
+    return rows
+
+
+def save_samples_csv(path, samples):
+    with open(path, "w") as f:
+        f.write("src,dst,message_mb,time_us\n")
+        for s, d, mb, us in samples:
+            f.write(f"{int(s)},{int(d)},{mb:.12g},{us:.12g}\n")
+
+
 def capacity_caps(policy: CapacityPolicy, k: int, S: int, N: int, P: int, c_hat=None) -> np.ndarray:
     ch = _f64(c_hat) if c_hat is not None else None
     caps = np.zeros((P, N), dtype=np.int64)

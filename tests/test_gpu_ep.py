@@ -31,3 +31,16 @@ def test_ep_parity_multi_gpu(case):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "EP_PARITY_OK" in r.stdout, r.stdout[-2000:]
+
+
+def test_p2p_sweep_multi_gpu():
+    """NVLink sweep -> fit_profile -> fill -> closed form on 2 or 4 GPUs (§8(f) row 1)."""
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = 4 if n >= 4 else 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "p2p_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "P2P_SWEEP_OK" in r.stdout, r.stdout[-2000:]
