@@ -189,16 +189,17 @@ int tamoe_layer_create(const tamoe_layer_config* cfg, const double* c_hat, tamoe
 
 /* Expert parallelism across GPUs (one process per GPU, NVLink / NVSwitch).
  * Rank r owns experts [r*E, (r+1)*E), E = N / world_size (dispatch.hpp:31); gate replicas are per rank with
- * no all-reduce (trainer.cpp:207-216).  Ranks map each other's workspaces (CUDA IPC): the permute kernel
- * stores token rows straight into the owners (dispatch), the combine kernel loads expert outputs from the
- * owners and stores dO into them, the gate-dX epilogue loads the owners' input gradients; NCCL carries only
- * the counts all-gather and stream-ordered barriers.  Capacities are rank-local (local / proportional,
- * gate.cpp:165-180).  tamoe_nccl_unique_id fills 128 bytes on one rank; broadcast them to all ranks, then
+ * no all-reduce (trainer.cpp:207-216).  Ranks map each other's workspaces (CUDA IPC) and every payload is a
+ * peer store from the kernel that computes it: the permute kernel stores token rows into the owners
+ * (dispatch), the owners' fwd2 / dgrad1 GEMM epilogues store expert outputs / input gradients back into the
+ * tokens' home ranks, the combine kernel stores dO into the owners; phases are ordered by a device-side
+ * barrier over the mapped workspaces that also carries the counts all-gather (NCCL is used at setup only).
+ * Capacities are rank-local (local / proportional, gate.cpp:165-180).  tamoe_nccl_unique_id fills 128 bytes on one rank; broadcast them to all ranks, then
  * every rank calls tamoe_layer_create_ep with its cfg.rank / cfg.world_size. */
 int tamoe_nccl_unique_id(void* out128);
 int tamoe_layer_create_ep(const tamoe_layer_config* cfg, const double* c_hat, const void* nccl_id128,
                           tamoe_layer** out);
-/* Off-rank payload bytes of the last step's all-to-alls: out[4] = dispatch, combine, grad dispatch, grad combine. */
+/* Off-rank payload bytes of the last step: out[4] = dispatch, expert-output return, dO, dX return. */
 int tamoe_layer_a2a_bytes(tamoe_layer* l, long long* out4);
 /* Host-side receive plan (CPU-testable): recv[P x E] rows per (source rank, local expert) -> the receive
  * segment of each local expert seg_start/seg_rows [E] (expert-major; inside it one 16-row padded block per
@@ -206,6 +207,40 @@ int tamoe_layer_a2a_bytes(tamoe_layer* l, long long* out4);
  * for it start, src_off [P x E].  The device plan kernel computes the same from the all-gathered counts. */
 int tamoe_ep_plan(int P, int E, const long long* recv, int* seg_start, int* seg_rows, long long* src_off);
 int tamoe_layer_destroy(tamoe_layer* l);
+
+/* ------------------------------------------------------------------ GPU-backed train() (§8(f) row 2)
+ * train (trainer.cpp:183-452 / trainer.hpp:100-106): full-batch gradient descent on task MSE + aux_weight *
+ * aux loss over P logical processes on this GPU (cfg.world_size = 1), per-process gate replicas, shared
+ * experts, plain SGD in the reference's order on fp32 master weights.  kind: 0 balance, 1 topo, 2 compulsory
+ * (not on the device path: validation error); cfg.aux_kind is derived from kind; topo switches to balance
+ * after switch_step when has_switch.  x / y / wg / w1 / w2 are device bf16 in the layer layouts; the weights
+ * are updated in place.  Report arrays are optional (null = not returned). */
+typedef struct {
+  int kind, steps;
+  double lr;
+  int has_switch, switch_step;
+  int report_window;
+  double bytes_per_element;
+  const double* alpha_hat;   /* optional [P x P] profile for the per-step exchange estimate */
+  const double* beta_hat;
+  const int* intra_groups;   /* optional [P x P]: row i marks the devices of i's innermost group */
+} tamoe_train_opts;
+
+typedef struct {
+  double* task_loss;         /* [steps] */
+  double* aux_loss;          /* [steps] unweighted */
+  double* comm_us;           /* [steps] bottleneck + size exchange (needs the profile) */
+  double* dropped_rate;      /* [steps] */
+  double* initial_dispatch;  /* [P x N] counts at step 0 */
+  double* final_dispatch;    /* [P x N] averaged over the report window */
+  double* tv_rows;           /* [P] TV(final row, c_hat row) (needs c_hat) */
+  /* tv_initial_mean, tv_final_mean, col_balance_max_dev, min_expert_load, intra_share, final_task_loss,
+   * final_aux_loss, final_comm_us, dropped_total_rate */
+  double summary[9];
+} tamoe_train_report;
+
+int tamoe_train(const tamoe_layer_config* cfg, const double* c_hat, const tamoe_train_opts* opts, const void* x,
+                const void* y, void* wg, void* w1, void* w2, tamoe_train_report* report, void* stream);
 int tamoe_layer_step(tamoe_layer* l, const tamoe_layer_io* io, void* stream);
 int tamoe_layer_read(tamoe_layer* l, int what, void* dst, long long bytes, void* stream);
 int tamoe_layer_n_pad(int N);

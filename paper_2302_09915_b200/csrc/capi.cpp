@@ -3,6 +3,7 @@
 #include "../../include/tamoe.h"
 
 #include <algorithm>
+#include <climits>
 #include <memory>
 #include <string>
 #include <vector>
@@ -15,6 +16,7 @@
 #include "host_topology.hpp"
 #include "layer.hpp"
 #include "route.hpp"
+#include "trainer.hpp"
 
 using namespace tamoe;
 
@@ -252,6 +254,44 @@ int tamoe_layer_create(const tamoe_layer_config* cfg, const double* c_hat, tamoe
                   cfg->capacity_factor, cfg->aux_kind, cfg->aux_weight, cfg->penalty_norm, cfg->temperature,
                   cfg->need_dx, cfg->world_size, cfg->rank};
     *out = new tamoe_layer(c, c_hat);
+  });
+}
+
+int tamoe_train(const tamoe_layer_config* cfg, const double* c_hat, const tamoe_train_opts* opts, const void* x,
+                const void* y, void* wg, void* w1, void* w2, tamoe_train_report* report, void* stream) {
+  return guarded([&] {
+    require(cfg && opts && x && y && wg && w1 && report, "train: null argument");
+    require(cfg->f == 0 || w2, "train: FFN experts need w2");
+    LayerConfig c{cfg->P, cfg->S, cfg->d, cfg->d_out, cfg->N, cfg->k, cfg->f, cfg->act, cfg->cap_mode,
+                  cfg->capacity_factor, cfg->aux_kind, cfg->aux_weight, cfg->penalty_norm, cfg->temperature,
+                  cfg->need_dx, cfg->world_size, cfg->rank};
+    TrainOptions o;
+    o.kind = opts->kind;
+    o.steps = opts->steps;
+    o.lr = opts->lr;
+    o.switch_step = opts->has_switch ? opts->switch_step : INT_MIN;
+    o.report_window = opts->report_window;
+    o.bytes_per_element = opts->bytes_per_element;
+    o.alpha_hat = opts->alpha_hat;
+    o.beta_hat = opts->beta_hat;
+    o.intra_groups = opts->intra_groups;
+    const TrainReport r = train_layer(c, c_hat, o, static_cast<const __nv_bfloat16*>(x),
+                                      static_cast<const __nv_bfloat16*>(y), static_cast<__nv_bfloat16*>(wg),
+                                      static_cast<__nv_bfloat16*>(w1), static_cast<__nv_bfloat16*>(w2),
+                                      static_cast<cudaStream_t>(stream));
+    auto put = [](double* dst, const std::vector<double>& v) {
+      if (dst && !v.empty()) std::memcpy(dst, v.data(), sizeof(double) * v.size());
+    };
+    put(report->task_loss, r.task_loss);
+    put(report->aux_loss, r.aux_loss);
+    put(report->comm_us, r.comm_us);
+    put(report->dropped_rate, r.dropped_rate);
+    put(report->initial_dispatch, r.initial_dispatch);
+    put(report->final_dispatch, r.final_dispatch);
+    put(report->tv_rows, r.tv_rows);
+    const double sm[9] = {r.tv_initial_mean, r.tv_final_mean, r.col_balance_max_dev, r.min_expert_load,
+                          r.intra_share, r.final_task_loss, r.final_aux_loss, r.final_comm_us, r.dropped_total_rate};
+    std::memcpy(report->summary, sm, sizeof(sm));
   });
 }
 

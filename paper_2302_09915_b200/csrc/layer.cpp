@@ -215,6 +215,7 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
   std::vector<double> pen(static_cast<size_t>(c.P) * c.N, 1.0 / c.N);
   if (c.aux_kind == 1) {
     require(c_hat != nullptr, "topo loss requires a target pattern (c_hat)");
+    topo_ready_ = true;
     for (int i = 0; i < c.P; ++i) {
       auto p = penalty_weights(c_hat + static_cast<size_t>(c.rank * c.P + i) * c.N, c.N, c.penalty_norm,
                                c.temperature);
@@ -325,6 +326,18 @@ static bool graphs_enabled() {
     return !(v && v[0] == '0');
   }();
   return on;
+}
+
+void Layer::set_aux_kind(int kind) {
+  require(kind == 0 || kind == 1, "aux kind must be 0 (balance) or 1 (topo)");
+  require(kind == 0 || topo_ready_, "switching to the topo loss needs a layer created with it (penalties)");
+  if (kind == cfg_.aux_kind) return;
+  cfg_.aux_kind = kind;
+  for (auto& e : graph_.exec)
+    if (e) {
+      TAMOE_CUDA(cudaGraphExecDestroy(e));
+      e = nullptr;
+    }
 }
 
 void Layer::run_step(const LayerIO& io, cudaStream_t s) {

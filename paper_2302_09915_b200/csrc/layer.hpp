@@ -115,6 +115,9 @@ class Layer {
   // off-rank payload bytes of the last step: dispatch stores, combine loads, dO stores, dX loads
   void a2a_bytes(long long* out4);
   void step(const LayerIO& io, cudaStream_t s);
+  // Auxiliary-loss kind of the following steps (train()'s topo -> balance switch, trainer.cpp:254-256);
+  // the routing keeps the c_hat it was created with.  Drops the captured step graphs.
+  void set_aux_kind(int kind);
   EpComm* ep() { return ep_.get(); }
   const LayerConfig& cfg() const { return cfg_; }
   RouteWorkspace& route() { return rw_; }
@@ -156,6 +159,7 @@ class Layer {
   float *logits_ = nullptr, *dldg_ = nullptr, *dw_part_ = nullptr;
   double *penalties_ = nullptr, *loss_part_ = nullptr;
   int n_loss_part_ = 0;
+  bool topo_ready_ = false;  // penalties p = Norm(1/c_hat) computed at creation (created with the topo loss)
   PhaseTimer timer_;
   // CUDA graphs of one step keyed by the step's buffers (LayerIO), a few cached (double-buffered inputs
   // alternate), captured and launched on a private stream joined to the caller's with two events.

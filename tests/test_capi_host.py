@@ -30,12 +30,10 @@ def test_library_loads_and_exports_header_symbols():
 
 def test_no_cpu_fallback_without_library(tmp_path, monkeypatch):
     """The product path refuses to run without the CUDA library (no silent fallback)."""
-    import importlib
     import paper_2302_09915_b200._lib as L
     monkeypatch.setattr(L, "LIB_PATH", str(tmp_path / "missing.so"))
     with pytest.raises(ImportError):
-        L._load()
-    importlib.reload(L)
+        L._load()  # (no reload afterwards: it would redefine the exception classes other modules hold)
 
 
 def re1_beta(P=4):
