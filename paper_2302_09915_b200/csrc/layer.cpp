@@ -147,7 +147,8 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
   require(c.f == 0 || (c.f % 256 == 0), "layer: f must be 0 (linear expert) or a multiple of 256");
   require(c.P == 1 || c.S % 16 == 0, "layer: S must be a multiple of 16 when P > 1 processes share a device");
   require(c.cap_mode >= 0 && c.cap_mode <= 3, "unknown capacity mode");
-  require(c.aux_kind == 0 || c.aux_kind == 1, "unknown aux loss kind");
+  require(c.aux_kind >= 0 && c.aux_kind <= 2, "unknown aux loss kind (0 balance, 1 topo, 2 compulsory)");
+  require(c.aux_kind != 2 || c.k == 1, "compulsory routing supports top-1 only");
   require(c.N <= 256, "layer: N must be <= 256");
   P_global_ = c.P * c.world_size;
   n_pad_ = (c.N + 15) & ~15;
@@ -178,6 +179,12 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
     arena_.reserve(plan_.push_row, r_max_);
     arena_.reserve(sig_slots_, kMaxRanks);
     arena_.reserve(sig_epoch_, 1);
+  }
+  if (c.aux_kind == 2) {
+    arena_.reserve(quota_, static_cast<long long>(c.P) * c.N);
+    arena_.reserve(probs_, T * c.N);
+    comp_ws_bytes_ = compulsory_workspace_bytes(c.P, c.S);
+    arena_.reserve(comp_ws_, static_cast<long long>(comp_ws_bytes_));
   }
   arena_.reserve(dz_, T * n64_);
   arena_.reserve(logits_, T * c.N);
@@ -226,6 +233,20 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
   // the reference withholds c_hat from balance routing (trainer.cpp:250): proportional capacity then throws
   const double* ch = (c.aux_kind == 0) ? nullptr : c_hat;
   auto caps = capacity_caps(c.cap_mode, c.cf, c.k, c.S, c.N, P_global_, ch);
+  if (c.aux_kind == 2) {  // quota_i = LRR(c_hat_i / sum(c_hat_i) * S, S)  (trainer.cpp:128-134)
+    require(c_hat != nullptr, "compulsory routing requires a target pattern (c_hat)");
+    std::vector<int> q(static_cast<size_t>(c.P) * c.N);
+    for (int i = 0; i < c.P; ++i) {
+      const double* row = c_hat + static_cast<size_t>(c.rank * c.P + i) * c.N;
+      double sum = 0.0;
+      for (int e = 0; e < c.N; ++e) sum += row[e];
+      std::vector<double> share(static_cast<size_t>(c.N));
+      for (int e = 0; e < c.N; ++e) share[static_cast<size_t>(e)] = row[e] / sum * static_cast<double>(c.S);
+      const auto lrr = largest_remainder_round(share.data(), c.N, c.S);
+      for (int e = 0; e < c.N; ++e) q[static_cast<size_t>(i) * c.N + e] = static_cast<int>(lrr[static_cast<size_t>(e)]);
+    }
+    TAMOE_CUDA(cudaMemcpy(quota_, q.data(), sizeof(int) * q.size(), cudaMemcpyHostToDevice));
+  }
   rw_.upload_caps(caps.data() + static_cast<size_t>(c.rank) * c.P * c.N, nullptr);
 }
 
@@ -398,17 +419,22 @@ void Layer::step(const LayerIO& io, cudaStream_t s) {
 }
 
 // Shared front: gate + histogram/scan + capacity.
-static void route_front(Layer& L, RouteWorkspace& rw, PhaseTimer& tm, const LayerIO& io, int n_pad, int d,
-                        int cap_mode, float* logits, cudaStream_t s) {
+void Layer::route_front(const LayerIO& io, cudaStream_t s) {
+  RouteWorkspace& rw = rw_;
+  PhaseTimer& tm = timer_;
   const RouteBuffers& b = rw.buf;
+  const bool compulsory = cfg_.aux_kind == 2;
   TAMOE_CUDA(cudaMemsetAsync(b.bad, 0, sizeof(int), s));
-  gate_forward(io.x, io.wg, n_pad, rw.dims, d, rw.row_out(logits, nullptr), s);
+  gate_forward(io.x, io.wg, n_pad_, rw.dims, cfg_.d, rw.row_out(logits_, compulsory ? probs_ : nullptr), s);
   tm.mark("gate_fwd", s);
+  if (compulsory) {  // quota claims replace the top-k / capacity outcome; every token is kept
+    route_compulsory(rw.dims, b, probs_, quota_, comp_ws_, comp_ws_bytes_, s);
+    tm.mark("route_compulsory", s);
+  }
   route_bucket(rw.dims, b, s);
   tm.mark("route_bucket", s);
-  route_capacity(rw.dims, b, cap_mode, rw.caps, s);
+  route_capacity(rw.dims, b, compulsory ? 0 : cfg_.cap_mode, rw.caps, s);
   tm.mark("route_capacity", s);
-  (void)L;
 }
 
 void Layer::step_local(const LayerIO& io, cudaStream_t s) {
@@ -416,7 +442,7 @@ void Layer::step_local(const LayerIO& io, cudaStream_t s) {
   const RouteBuffers& b = rw_.buf;
   PhaseTimer& tm = timer_;
   tm.begin(s);
-  route_front(*this, rw_, tm, io, n_pad_, c.d, c.cap_mode, logits_, s);
+  route_front(io, s);
   const PeerBufs zb = peers(dO_);
   route_permute(rw_.dims, b, io.x, c.d, peers(xp_), r_max_, &zb, c.d_out, map_, s);
   tm.mark("permute", s);
@@ -435,7 +461,7 @@ void Layer::step_ep(const LayerIO& io, cudaStream_t s) {
   PhaseTimer& tm = timer_;
   const int W = c.world_size, E = c.N / W;
   tm.begin(s);
-  route_front(*this, rw_, tm, io, n_pad_, c.d, c.cap_mode, logits_, s);
+  route_front(io, s);
   ep_barrier(s, true);  // counts all-gather; also: every rank finished its previous step
   ep_plan_device(plan_, W, E, c.rank, s);
   tm.mark("a2a_counts", s);
@@ -519,7 +545,7 @@ void Layer::gate_backward(const LayerIO& io, cudaStream_t s) {
   ga.n64 = n64_;
   ga.dout = c.d_out;
   ga.P_global = P_global_;
-  ga.aux_kind = c.aux_kind;
+  ga.aux_kind = c.aux_kind == 2 ? 0 : c.aux_kind;  // compulsory trains with the balance loss (trainer.cpp:253)
   ga.aux_weight = c.aux_weight;
   ga.logits = logits_;
   ga.idx = b.idx;

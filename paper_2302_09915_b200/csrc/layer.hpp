@@ -159,7 +159,12 @@ class Layer {
   float *logits_ = nullptr, *dldg_ = nullptr, *dw_part_ = nullptr;
   double *penalties_ = nullptr, *loss_part_ = nullptr;
   int n_loss_part_ = 0;
-  bool topo_ready_ = false;  // penalties p = Norm(1/c_hat) computed at creation (created with the topo loss)
+  bool topo_ready_ = false;
+  // compulsory-quota routing (aux_kind 2): quotas [P x N], fp64 probabilities [P*S x N], sort workspace
+  int* quota_ = nullptr;
+  double* probs_ = nullptr;
+  char* comp_ws_ = nullptr;
+  size_t comp_ws_bytes_ = 0;  // penalties p = Norm(1/c_hat) computed at creation (created with the topo loss)
   PhaseTimer timer_;
   // CUDA graphs of one step keyed by the step's buffers (LayerIO), a few cached (double-buffered inputs
   // alternate), captured and launched on a private stream joined to the caller's with two events.
@@ -176,6 +181,7 @@ class Layer {
     ~StepGraph();
   } graph_;
   void run_step(const LayerIO& io, cudaStream_t s);
+  void route_front(const LayerIO& io, cudaStream_t s);
 };
 
 }  // namespace tamoe

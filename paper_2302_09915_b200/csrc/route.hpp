@@ -88,6 +88,13 @@ void route_rows_from_probs(const double* probs, const RouteDims& d, const RowRou
 // Same per-token routing over fp32 gate logits (softmax in fp64 first), N <= 256.
 void route_from_logits(const float* logits, const RouteDims& d, const RowRouteOut& o, cudaStream_t s);
 
+// Compulsory-quota re-routing of top-1 picks (trainer.cpp:121-169): rewrites idx / score / gate from the
+// fp64 probabilities [P*S x N] and the per-(process, expert) quotas (device int32 [P*N], rows sum to S),
+// rebuilds the 32-token histograms; follow with route_bucket + route_capacity(mode 0).
+size_t compulsory_workspace_bytes(int P, int S);
+void route_compulsory(const RouteDims& d, const RouteBuffers& b, const double* probs, const int* quota, void* ws,
+                      size_t ws_bytes, cudaStream_t s);
+
 // histogram scan + stable bucket lists (gate.cpp:160-164 / 181-185 order)
 void route_bucket(const RouteDims& d, const RouteBuffers& b, cudaStream_t s);
 // capacity enforcement + compaction + counts + mean probs (gate.cpp:115, 138-199)

@@ -57,11 +57,10 @@ TrainReport train_layer(LayerConfig cfg, const double* c_hat, const TrainOptions
   require(o.kind >= 0 && o.kind <= 2, "train: unknown loss kind");
   require(o.steps >= 0, "train: steps must be >= 0");
   require(o.kind == 0 || c_hat != nullptr, "topo and compulsory losses require a target pattern");
-  require(o.kind != 2, "train: the compulsory-quota ablation is not available on the device path");
-  cfg.aux_kind = o.kind == 1 ? 1 : 0;
+  cfg.aux_kind = o.kind;  // 2 = compulsory quota routing + balance loss
   const int P = cfg.P, S = cfg.S, N = cfg.N, k = cfg.k, E = N / P;
   require(N % P == 0, "N must be divisible by P");
-  Layer layer(cfg, cfg.aux_kind == 1 ? c_hat : nullptr);
+  Layer layer(cfg, cfg.aux_kind != 0 ? c_hat : nullptr);
   const int n_pad = layer.n_pad();
   const long long n_wg = static_cast<long long>(P) * n_pad * cfg.d;
   const long long n_w1 = static_cast<long long>(N) * (cfg.f == 0 ? cfg.d_out : cfg.f) * cfg.d;

@@ -147,3 +147,54 @@ def test_layer_graph_replay_bitwise():
         got[5] = yh2.float().cpu()
         for a, b in zip(ref, got):
             assert torch.equal(a, b)
+
+
+def compulsory_restated(probs, score, c_hat, S):
+    """trainer.cpp:121-169 restated (test-only): quotas by LRR of the c_hat row share; tokens by (top-1 score
+    desc, token asc) claim their best expert (probability desc, expert asc) with quota left."""
+    P, _, N = probs.shape
+    O = oracle.orc()
+    out = np.zeros((P, S), np.int64)
+    for i in range(P):
+        share = c_hat[i] / c_hat[i].sum() * S
+        quota = O.largest_remainder_round(share, S).astype(np.int64)
+        order = sorted(range(S), key=lambda s: (-score[i, s], s))
+        for s in order:
+            for e in sorted(range(N), key=lambda e: (-probs[i, s, e], e)):
+                if quota[e] > 0:
+                    quota[e] -= 1
+                    out[i, s] = e
+                    break
+    return out
+
+
+def test_layer_compulsory_quota_routing():
+    """Compulsory-quota ablation (aux kind 2): device claims == the restated greedy on the device's own
+    probabilities (softmax of the stored logits in fp64); every token kept; counts equal the quotas."""
+    from paper_2302_09915_b200 import ops
+    from paper_2302_09915_b200.layer import LayerConfig, TAMoELayer
+    P, S, d, dout, N = 2, 384, 256, 128, 8
+    rng = np.random.default_rng(5)
+    beta = np.array([[0.1, 4.0], [4.0, 0.1]])
+    c_hat = ops.target_closed_form(beta, N, 1, S)
+    cfg = LayerConfig(P=P, S=S, d=d, d_out=dout, N=N, k=1, f=0, act=0, cap_mode=0, aux_kind=2, need_dx=False)
+    layer = TAMoELayer(cfg, c_hat)
+    params = layer.init_params(seed=3, gate_std=0.05)
+    x = torch.tensor(rng.normal(size=(P * S, d)), dtype=torch.float32).bfloat16().cuda()
+    y = torch.tensor(rng.normal(size=(P * S, dout)), dtype=torch.float32).bfloat16().cuda()
+    layer.step(x, y, params)
+    torch.cuda.synchronize()
+    logits = layer.read(ops.R_LOGITS, (P, S, N)).astype(np.float64)
+    z = np.exp(logits - logits.max(-1, keepdims=True))
+    probs = z / z.sum(-1, keepdims=True)
+    score = probs.max(-1)
+    want = compulsory_restated(probs, score, c_hat, S)
+    got = layer.read(ops.R_IDX, (P, S, 1))[..., 0]
+    mism = np.argwhere(got != want)
+    assert len(mism) <= max(2, want.size // 500), f"{len(mism)} claim mismatches"
+    assert np.all(layer.read(ops.R_KEPT, (P, S, 1)) == 1)
+    O = oracle.orc()
+    quotas = np.stack([O.largest_remainder_round(c_hat[i] / c_hat[i].sum() * S, S) for i in range(P)])
+    np.testing.assert_array_equal(layer.read(ops.R_COUNTS, (P, N)), quotas)
+    with pytest.raises(ops.ValidationError):  # top-1 only (trainer.cpp:124)
+        TAMoELayer(LayerConfig(P=P, S=S, d=d, d_out=dout, N=N, k=2, aux_kind=2), c_hat)

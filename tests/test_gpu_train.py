@@ -26,14 +26,14 @@ def setup(P, S, d, dout, N, k, seed=3):
     return R, bf(x), bf(y), gates, experts
 
 
-@pytest.mark.parametrize("kind,cap,switch", [(0, 0, None), (1, 3, None), (1, 2, 3)])
-def test_train_matches_reference_trajectory(kind, cap, switch):
+@pytest.mark.parametrize("kind,cap,switch,k", [(0, 0, None, 2), (1, 3, None, 2), (1, 2, 3, 2), (2, 0, None, 1)])
+def test_train_matches_reference_trajectory(kind, cap, switch, k):
     from paper_2302_09915_b200 import ops
     from paper_2302_09915_b200.train import TrainConfig, LossKind, train
-    P, S, d, dout, N, k, steps, lr = 4, 256, 256, 128, 8, 2, 12, 0.05
+    P, S, d, dout, N, steps, lr = 4, 256, 256, 128, 8, 12, 0.05
     R, x, y, gates, experts = setup(P, S, d, dout, N, k)
     beta = np.array([[0.1 if i == j else (1.0 if i // 2 == j // 2 else 4.0) for j in range(P)] for i in range(P)])
-    c_hat = ops.target_closed_form(beta, N, k, S) if kind == 1 else None
+    c_hat = ops.target_closed_form(beta, N, k, S) if kind in (1, 2) else None
     ref = R.train(x, y, gates, experts, kind=kind, cap_mode=cap, cf=1.25, c_hat=c_hat, lr=lr, steps=steps, k=k,
                   switch_step=switch)
     cfg = TrainConfig(P=P, S=S, d=d, d_out=dout, N=N, k=k, lr=lr, steps=steps, switch_step=switch,
