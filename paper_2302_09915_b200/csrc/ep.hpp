@@ -51,6 +51,14 @@ struct EpSignal {
 };
 void ep_signal_barrier(const EpSignal& a, cudaStream_t s);
 
+// Store `words` 32-bit words from src into every rank's copy at dst[r] + word offset (NVLink peer stores):
+// the expert-parallel global capacity gathers every rank's picks this way.
+struct PeerWords {
+  unsigned int* p[kMaxRanks];
+};
+void peer_broadcast_words(const PeerWords& dst, long long dst_off_words, const void* src, long long words, int P,
+                          cudaStream_t s);
+
 class EpComm {
  public:
   EpComm(int world, int rank, const ncclUniqueId& id);

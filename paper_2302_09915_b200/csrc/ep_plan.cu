@@ -118,7 +118,24 @@ __global__ void __launch_bounds__(512) p2p_copy_kernel(uint4* __restrict__ dst, 
   }
 }
 
+__global__ void peer_broadcast_kernel(const __grid_constant__ PeerWords dst, long long off,
+                                      const unsigned int* __restrict__ src, long long words, int P) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < words; i += stride) {
+    const unsigned int v = src[i];
+    for (int r = 0; r < P; ++r) dst.p[r][off + i] = v;
+  }
+}
+
 }  // namespace
+
+void peer_broadcast_words(const PeerWords& dst, long long dst_off_words, const void* src, long long words, int P,
+                          cudaStream_t s) {
+  if (words <= 0) return;
+  const int grid = static_cast<int>(std::min<long long>((words + 255) / 256, 2LL * num_sms()));
+  peer_broadcast_kernel<<<grid, 256, 0, s>>>(dst, dst_off_words, static_cast<const unsigned int*>(src), words, P);
+  TAMOE_CUDA(cudaGetLastError());
+}
 
 void p2p_copy(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   require(bytes % 16 == 0, "p2p copy: size must be a multiple of 16 bytes");

@@ -140,8 +140,6 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
   require(c.world_size == 1 || ep_ != nullptr, "expert parallelism needs a communicator (tamoe_layer_create_ep)");
   require(c.world_size == 1 || c.P == 1, "expert parallelism runs one logical process per rank (P = 1)");
   require(c.N % c.world_size == 0, "N must be divisible by world_size");
-  require(c.world_size == 1 || c.cap_mode != 1,
-          "global capacity across ranks needs an owner-side selection exchange (not supported yet)");
   require(c.d % 256 == 0, "layer: d must be a multiple of 256");
   require(c.d_out % 128 == 0, "layer: d_out must be a multiple of 128");
   require(c.f == 0 || (c.f % 256 == 0), "layer: f must be 0 (linear expert) or a multiple of 256");
@@ -158,6 +156,8 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
   // receive side: worst case every token of every rank picks this rank's experts
   r_max_ = static_cast<int>(static_cast<long long>(c.world_size) * (T * c.k + 16LL * E));
   rw_.reserve(arena_, c.P, c.S, c.N, c.k);
+  global_ep_ = ep_ != nullptr && c.cap_mode == 1;
+  if (global_ep_) gw_.reserve(arena_, c.world_size, c.S, c.N, c.k);
   arena_.reserve(xp_, static_cast<long long>(r_max_) * c.d);
   arena_.reserve(O_, static_cast<long long>(r_max_) * c.d_out);
   arena_.reserve(dO_, static_cast<long long>(r_max_) * c.d_out);
@@ -212,6 +212,17 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
       sig_.sig[j] = reinterpret_cast<unsigned int*>(bases_[j] + soff);
       sig_.counts_dst[j] = reinterpret_cast<int*>(bases_[j] + coff);
     }
+    if (global_ep_) {
+      auto peer_of = [&](const void* local, int j) {
+        return reinterpret_cast<unsigned int*>(bases_[j] + (static_cast<const char*>(local) - arena_.base()));
+      };
+      for (int j = 0; j < c.world_size; ++j) {
+        gw_idx_.p[j] = peer_of(gw_.buf.idx, j);
+        gw_score_.p[j] = peer_of(gw_.buf.score, j);
+        gw_hist_.p[j] = peer_of(gw_.buf.hist4, j);
+      }
+      TAMOE_CUDA(cudaMemset(gw_.buf.msum4, 0, sizeof(double) * static_cast<size_t>(gw_.dims.tiles()) * 4 * c.N));
+    }
     map_.P = c.world_size;
     map_.E = E;
     map_.local_start = rw_.buf.seg_start;
@@ -248,6 +259,7 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
     TAMOE_CUDA(cudaMemcpy(quota_, q.data(), sizeof(int) * q.size(), cudaMemcpyHostToDevice));
   }
   rw_.upload_caps(caps.data() + static_cast<size_t>(c.rank) * c.P * c.N, nullptr);
+  if (global_ep_) gw_.upload_caps(caps.data(), nullptr);  // one global cap per expert, every rank's row
 }
 
 Layer::~Layer() = default;
@@ -433,6 +445,22 @@ void Layer::route_front(const LayerIO& io, cudaStream_t s) {
   }
   route_bucket(rw.dims, b, s);
   tm.mark("route_bucket", s);
+  if (global_ep_) {
+    // every rank's picks (expert, score) and 32-token histograms -> every rank's global view, then the
+    // global select over (score desc, process asc, token asc) on that view and this rank's flags back
+    const int W = cfg_.world_size, me = cfg_.rank;
+    const long long picks = rw.dims.picks(), hist = static_cast<long long>(rw.dims.tiles()) * 4 * cfg_.N;
+    peer_broadcast_words(gw_idx_, me * picks, b.idx, picks, W, s);
+    peer_broadcast_words(gw_score_, me * picks * 2, b.score, picks * 2, W, s);
+    peer_broadcast_words(gw_hist_, me * hist, b.hist4, hist, W, s);
+    ep_barrier(s, false);
+    route_bucket(gw_.dims, gw_.buf, s);
+    route_capacity(gw_.dims, gw_.buf, 1, gw_.caps, s);
+    TAMOE_CUDA(cudaMemcpyAsync(b.kept, gw_.buf.kept + me * picks, static_cast<size_t>(picks), cudaMemcpyDeviceToDevice, s));
+    route_capacity(rw.dims, b, 4, rw.caps, s);
+    tm.mark("route_capacity_global", s);
+    return;
+  }
   route_capacity(rw.dims, b, compulsory ? 0 : cfg_.cap_mode, rw.caps, s);
   tm.mark("route_capacity", s);
 }
@@ -576,6 +604,7 @@ int Layer::launches_per_step() const {
   int n = 10;  // gate = logits GEMM + router
   // EP: + plan and return-map kernels + the device barriers (counts publish, dispatch, forward, combine, [dX])
   if (ep_) n += 2 + (nccl_barrier() ? 0 : 4 + (cfg_.need_dx ? 1 : 0));
+  if (global_ep_) n += 3 + (nccl_barrier() ? 0 : 1) + 3;  // broadcasts, barrier, global scan/bucket/capacity
   n += cfg_.f == 0 ? (1 + 1 + (cfg_.need_dx ? 1 : 0)) : (2 + 3 + (cfg_.need_dx ? 1 : 0));
   if (cfg_.need_dx) n += 1;
   return n;

@@ -141,6 +141,11 @@ class Layer {
   LayerConfig cfg_;
   Arena arena_;
   RouteWorkspace rw_;
+  // expert-parallel global capacity (gate.cpp:157-164 across ranks): every rank's picks gathered into a
+  // W-process view (peer stores), the global select run on it redundantly, this rank's flags applied locally
+  bool global_ep_ = false;
+  RouteWorkspace gw_;
+  PeerWords gw_idx_{}, gw_score_{}, gw_hist_{};
   std::unique_ptr<EpComm> ep_;
   // expert parallelism: device plan, peer-mapped arena bases, row map
   EpPlanDev plan_{};

@@ -161,7 +161,9 @@ __global__ void __launch_bounds__(kCapThreads) route_capacity_kernel(RouteDims d
   const int e = blockIdx.x;
   const int N = d.N;
   const int ls = b.list_start[e];
-  const int nb = mode == 1 ? 1 : d.P;
+  const int nb = mode == 1 ? 1 : (mode == 4 ? 0 : d.P);
+  if (mode == 4)  // external decision (expert-parallel global capacity): b.kept holds the flags per pick
+    for (int j = threadIdx.x; j < b.list_count[e]; j += blockDim.x) b.list_keep[ls + j] = b.kept[b.list_pick[ls + j]];
   // pass A: per bucket select + keep flags
   for (int bk = 0; bk < nb; ++bk) {
     const int bs = mode == 1 ? 0 : b.bucket_start[bk * N + e];
@@ -262,7 +264,7 @@ __global__ void __launch_bounds__(kCapThreads) route_capacity_kernel(RouteDims d
   for (int pr = 0; pr < d.P; ++pr) {
     const int bs = b.bucket_start[pr * N + e], bc = b.bucket_count[pr * N + e];
     int kc = 0;
-    if (mode == 1) {
+    if (mode == 1 || mode == 4) {
       for (int j = threadIdx.x; j < bc; j += blockDim.x) kc += b.list_keep[ls + bs + j];
     } else if (threadIdx.x == 0) {
       kc = mode == 0 ? bc : min(bc, max(caps[pr * N + e], 0));  // exactly cap picks survive
@@ -397,7 +399,7 @@ void route_bucket(const RouteDims& d, const RouteBuffers& b, cudaStream_t s) {
 }
 
 void route_capacity(const RouteDims& d, const RouteBuffers& b, int mode, const int* caps, cudaStream_t s) {
-  require(mode >= 0 && mode <= 3, "unknown capacity mode");
+  require(mode >= 0 && mode <= 4, "unknown capacity mode");
   route_capacity_kernel<<<d.N, kCapThreads, 0, s>>>(d, b, mode, caps);
   TAMOE_CUDA(cudaGetLastError());
 }

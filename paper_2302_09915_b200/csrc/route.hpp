@@ -98,7 +98,8 @@ void route_compulsory(const RouteDims& d, const RouteBuffers& b, const double* p
 // histogram scan + stable bucket lists (gate.cpp:160-164 / 181-185 order)
 void route_bucket(const RouteDims& d, const RouteBuffers& b, cudaStream_t s);
 // capacity enforcement + compaction + counts + mean probs (gate.cpp:115, 138-199)
-// caps: device int32 [P*N] (INT32_MAX = unlimited); mode: 0 none, 1 global, 2 local, 3 proportional
+// caps: device int32 [P*N] (INT32_MAX = unlimited); mode: 0 none, 1 global, 2 local, 3 proportional,
+// 4 external (b.kept already holds the keep flag of every pick: the expert-parallel global decision)
 void route_capacity(const RouteDims& d, const RouteBuffers& b, int mode, const int* caps, cudaStream_t s);
 // padded expert segments + gather of token rows into the expert-sorted buffer.
 // x: [P*S x dx] bf16; xp: [R_max x dx]; zero_rows (optional): second buffer whose pad rows are zeroed.

@@ -19,6 +19,9 @@ CASES = {
     "ffn_prop": dict(S=512, d=256, dout=256, f=512, k=2, cap=3, kind=1, need_dx=True),
     "linear_none": dict(S=384, d=256, dout=256, f=0, k=1, cap=0, kind=0, need_dx=True),
     "ffn_local": dict(S=1000, d=512, dout=256, f=256, k=1, cap=2, kind=1, need_dx=True),
+    # global capacity across ranks (gate.cpp:157-164): one cap per expert over every rank's picks
+    # (cf 0.5: about half of the picks are dropped, so the cross-rank selection order is exercised)
+    "ffn_global": dict(S=512, d=256, dout=256, f=512, k=2, cap=1, kind=0, need_dx=True, cf=0.5),
 }
 
 
@@ -61,7 +64,7 @@ def main():
 
     obj = [nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
-    cfg = LayerConfig(P=1, S=S, d=d, d_out=dout, N=N, k=k, f=f, act=1, cap_mode=c["cap"], capacity_factor=1.25,
+    cfg = LayerConfig(P=1, S=S, d=d, d_out=dout, N=N, k=k, f=f, act=1, cap_mode=c["cap"], capacity_factor=c.get("cf", 1.25),
                       aux_kind=c["kind"], need_dx=c["need_dx"], world_size=world, rank=rank)
     layer = TAMoELayer(cfg, c_hat, nccl_id=obj[0])
     lo, hi = rank * E, (rank + 1) * E
@@ -92,7 +95,7 @@ def main():
     a2a = layer.a2a_bytes()
     if rank == 0:
         pen = np.stack([ops.penalty_weights(c_hat[i]) for i in range(P)])
-        o = oracle.orc().layer_step(x, y, gates, U=U, W1=W1, W2=W2, k=k, cap_mode=c["cap"], cf=1.25, c_hat=c_hat,
+        o = oracle.orc().layer_step(x, y, gates, U=U, W1=W1, W2=W2, k=k, cap_mode=c["cap"], cf=c.get("cf", 1.25), c_hat=c_hat,
                                     aux_kind=c["kind"], penalties=pen, act=1, want_dx=c["need_dx"])
         gi = np.concatenate([t.numpy() for t in idx])
         mism = int((gi != o["expert"]).sum())
