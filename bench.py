@@ -351,20 +351,42 @@ def main():
                                            "(double-buffered), losses read back D2H every step"}
 
     # ---------------- roofline of the dominant kernel family (expert grouped GEMMs, tcgen05)
+    # Per launch: FLOPs 2*R*d*f and ALGORITHMIC bytes = this GPU's expert weights (E = N/world experts, read for
+    # fwd/dgrad, dW written for wgrad) + the token-row operands / outputs, R = T*k rows (every rank routes T*k
+    # picks, so a rank receives T*k rows on average).  bound = whichever roofline time is larger.
     pk = peaks()
     T = S
+    R = T * cfg.k
+    E_loc = cfg.N // world
+    wb = 2.0 * E_loc * cfg.d * cfg.f
+    rows = {"fwd1": R * (cfg.d + 2 * cfg.f), "fwd2": R * (cfg.f + cfg.d_out), "dgrad2": R * (cfg.d_out + 2 * cfg.f),
+            "wgrad2": R * (cfg.d_out + cfg.f), "wgrad1": R * (cfg.f + cfg.d), "dgrad1": R * (cfg.f + cfg.d)}
+    bytes_per_launch = sum(wb + 2.0 * v for v in rows.values()) / len(rows)
+    flop_per_launch = 2.0 * R * cfg.d * cfg.f
     gemm_names = [n for n in phases if n.startswith("expert_")]
     gemm_ms = sum(phases[n] for n in gemm_names)
-    # every expert GEMM is 2*rows*d*f; with EP the rows a rank receives average T*k (all ranks route T*k picks)
-    flops = len(gemm_names) * 2.0 * T * cfg.k * cfg.d * cfg.f
-    achieved = flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
+    avg_s = gemm_ms / max(len(gemm_names), 1) / 1e3
+    tflops = flop_per_launch / avg_s / 1e12 if avg_s > 0 else 0.0
+    gbs = bytes_per_launch / avg_s / 1e9 if avg_s > 0 else 0.0
+    t_hbm = bytes_per_launch / (pk["hbm"] * 1e9)
+    t_tc = flop_per_launch / (pk["bf16_sus"] * 1e12)
+    hbm_bound = t_hbm > t_tc
     roof = {"kernel": "expert grouped GEMM (tcgen05, 6 launches/step: fwd1, fwd2, dgrad2, wgrad2, wgrad1, dgrad1)",
-            "bound": "tensor", "achieved": achieved, "peak": pk["bf16_sus"], "unit": "TFLOP/s",
-            "frac": achieved / pk["bf16_sus"], "peak_kind": f"{pk['source']} bf16 sustained",
-            "flop_per_launch": 2.0 * T * cfg.k * cfg.d * cfg.f, "avg_launch_ms": gemm_ms / max(len(gemm_names), 1),
-            "traffic": None}
+            "bound": "hbm" if hbm_bound else "tensor",
+            "achieved": gbs if hbm_bound else tflops,
+            "peak": pk["hbm"] if hbm_bound else pk["bf16_sus"],
+            "unit": "GB/s" if hbm_bound else "TFLOP/s",
+            "frac": (gbs / pk["hbm"]) if hbm_bound else (tflops / pk["bf16_sus"]),
+            "peak_kind": f"{pk['source']} " + ("HBM copy bandwidth" if hbm_bound else "bf16 sustained"),
+            "traffic": None,
+            "algorithmic_bytes_per_launch": bytes_per_launch, "flop_per_launch": flop_per_launch,
+            "arithmetic_intensity_flop_per_byte": flop_per_launch / bytes_per_launch,
+            "ridge_flop_per_byte": pk["bf16_sus"] * 1e12 / (pk["hbm"] * 1e9),
+            "avg_launch_ms": avg_s * 1e3, "tensor_tflops": tflops, "tensor_frac_sustained": tflops / pk["bf16_sus"],
+            "hbm_gbs": gbs, "hbm_frac": gbs / pk["hbm"],
+            "note": "launch durations from CUDA events on the step stream around each GEMM (eager phase steps)"}
     prof_traffic = os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")
-    if os.path.exists(prof_traffic):
+    if os.path.exists(prof_traffic) and world == 1:
         with open(prof_traffic) as f:
             roof["traffic"] = json.load(f).get("traffic_bytes_per_launch")
 
@@ -383,7 +405,7 @@ def main():
                                        f"{S} tokens/GPU, GELU FFN experts, topo aux loss, capacity none, dX on",
                            "tokens_per_gpu": S, "global_tokens": world * S,
                            "parallelism": f"ep{world} (expert parallel, {C2['N'] // world} experts per GPU, "
-                                          "NCCL all-to-all over NVLink)" if world > 1
+                                          "all-to-all as NVLink peer stores fused into the kernels)" if world > 1
                            else "single GPU, 64 local experts",
                            "l2": "working set > L2 (1.07 GB expert weights + ~0.6 GB activations per step)"},
                 "roofline": roof, "all_to_all": a2a, "phases_ms": phases, "timed_steps_for_phases": tsteps,

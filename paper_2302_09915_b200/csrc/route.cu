@@ -327,8 +327,9 @@ __global__ void __launch_bounds__(kPermWarps * 32) route_permute_kernel(RouteDim
     if (threadIdx.x == 0) *b.total_rows = total;
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = blockIdx.x * kPermWarps + warp;
-  if (r >= total || r >= r_max) return;
+  const int rows = min(total, r_max);
+  // warps stride over the rows (the block's expert scan above is amortised over many rows)
+  for (int r = blockIdx.x * kPermWarps + warp; r < rows; r += gridDim.x * kPermWarps) {
   int lo = 0, hi = N - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -363,6 +364,7 @@ __global__ void __launch_bounds__(kPermWarps * 32) route_permute_kernel(RouteDim
       uint4* zd = reinterpret_cast<uint4*>(zrows.p[dst_rank] + drow * zdim);
       for (int v = lane; v < zdim / 8; v += 32) zd[v] = z;
     }
+  }
   }
 }
 
@@ -407,7 +409,7 @@ void route_capacity(const RouteDims& d, const RouteBuffers& b, int mode, const i
 void route_permute(const RouteDims& d, const RouteBuffers& b, const __nv_bfloat16* x, int dx, const PeerBufs& xp,
                    int r_max, const PeerBufs* zrows, int zdim, const RowMap& map, cudaStream_t s) {
   require(dx % 8 == 0 && (zrows == nullptr || zdim % 8 == 0), "permute: row widths must be multiples of 8");
-  const int blocks = (r_max + kPermWarps - 1) / kPermWarps;
+  const int blocks = std::max(1, std::min((r_max + kPermWarps - 1) / kPermWarps, 8 * num_sms()));
   const size_t smem = sizeof(int) * (2 * d.N + 32);
   PeerBufs z{};
   if (zrows) z = *zrows;
