@@ -83,7 +83,10 @@ template <int V>
 struct EpiSwap {
   static constexpr int kChunk = 2048;  // 32 x 32 bf16
   static constexpr int kPf = 2;        // own chunks of pre_in in flight
-  static constexpr int kWarpBytes = (V == 0 || V == 3) ? 2 * kChunk : 4 * kChunk;
+  // staging per warp: V0/V3 a 2-slot output ring; V1 2-slot rings for act(x) and act'(x) (4 pipeline stages:
+  // single slots measured slower); V2 one output slot + the 2-slot act' prefetch ring (keeps 5 stages)
+  static constexpr bool kRing = V != 2;
+  static constexpr int kWarpBytes = (V == 1 ? 4 : (V == 2 ? 3 : 2)) * kChunk;
   static constexpr bool kEarlyRelease = true;
   static constexpr int kMaxCh = 4;  // a warp's chunks per tile: every other 32-column chunk of N <= 256
   using Params = SwapParams;
@@ -106,7 +109,7 @@ struct EpiSwap {
   static __device__ __forceinline__ void prefetch(const Params& e, const GemmParams&, const TileInfo& ti, int q, int h,
                                                   int lane, uint8_t* wsm, const int* s_start) {
     if constexpr (V == 2) {
-      __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(wsm + 2 * kChunk);
+      __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(wsm + kChunk);
       const int row0 = s_start[ti.g] + ti.n0;
       const int mcol = ti.m0 + q * 32;
       for (int j = 0; j < kPf; ++j) load_chunk(e, ti, row0, mcol, h + 2 * j, ring + j * 1024, lane);
@@ -131,7 +134,7 @@ struct EpiSwap {
     ptx::tmem_ld_wait();
     release();
     __nv_bfloat16* st_out = reinterpret_cast<__nv_bfloat16*>(wsm);
-    __nv_bfloat16* extra = reinterpret_cast<__nv_bfloat16*>(wsm + 2 * kChunk);  // pre_out staging | pre_in ring
+    __nv_bfloat16* extra = reinterpret_cast<__nv_bfloat16*>(wsm + (V == 1 ? 2 : 1) * kChunk);  // act' ring (V1 / V2)
     const int mcol = ti.m0 + q * 32;
     const int row0 = s_start[ti.g] + ti.n0;
     const int nch = (ti.n + 31) / 32;
@@ -146,11 +149,14 @@ struct EpiSwap {
         __syncwarp();
       }
       const float* v = acc[j];
-      if (j >= 2) {
-        if (lane == 0) ptx::bulk_wait_read<1>();
+      if (kRing ? j >= 2 : j >= 1) {  // the slot's previous TMA store has read it
+        if (lane == 0) {
+          if constexpr (kRing) ptx::bulk_wait_read<1>();
+          else ptx::bulk_wait_read<0>();
+        }
         __syncwarp();
       }
-      __nv_bfloat16* so = st_out + (j & 1) * 1024;
+      __nv_bfloat16* so = st_out + (kRing ? (j & 1) * 1024 : 0);
       __nv_bfloat16* sx = extra + (j & 1) * 1024;
 #pragma unroll
       for (int c = 0; c < 32; ++c) {

@@ -28,7 +28,7 @@ def timeit(fn, iters=20):
     return a.elapsed_time(b) / iters
 
 
-def run(name, counts, M, K, mode="fwd"):
+def run(name, counts, M, K, mode="fwd", act=0, store_deriv=False):
     G = len(counts)
     ss, sr, R = segs(counts)
     x = torch.randn(R, K, device="cuda").bfloat16()
@@ -36,8 +36,9 @@ def run(name, counts, M, K, mode="fwd"):
     if mode == "fwd":
         w = torch.randn(G, M, K, device="cuda").bfloat16()
         out = torch.empty(R, M, device="cuda", dtype=torch.bfloat16)
+        pre = torch.empty(R, M, device="cuda", dtype=torch.bfloat16) if store_deriv else None
         fn = lambda: _lib.call("tamoe_grouped_fwd", x.data_ptr(), w.data_ptr(), G, M, K, R, ss.data_ptr(),
-                               sr.data_ptr(), out.data_ptr(), None, 0, st)
+                               sr.data_ptr(), out.data_ptr(), pre.data_ptr() if pre is not None else None, act, st)
         flops = 2.0 * sum(counts) * M * K
     elif mode == "dgrad":
         w = torch.randn(G, K, M, device="cuda").bfloat16()
@@ -83,8 +84,11 @@ if __name__ == "__main__":
     if "--c2" in sys.argv:
         real = c2_counts()
         print("C2 routed counts: min", min(real), "max", max(real), "std", float(np.std(real)), flush=True)
-        for c in (128, 160, 192, 256, 320, 384, 512):
-            run(f"uniform {c} fwd1", [c] * 64, 4096, 1024)
+        run("C2 routed fwd1 plain", real, 4096, 1024)
+        run("C2 routed fwd1 gelu", real, 4096, 1024, act=1)
+        run("C2 routed fwd1 gelu+deriv", real, 4096, 1024, act=1, store_deriv=True)
+        if "--act-only" in sys.argv:
+            sys.exit(0)
         for nm, cnt in (("uniform 256", [256] * 64), ("C2 routed", real)):
             run(nm + " fwd1", cnt, 4096, 1024)
             run(nm + " fwd2", cnt, 1024, 4096)

@@ -74,6 +74,42 @@ __global__ void seg_kernel(const uint4* __restrict__ src, uint4** peers, uint4* 
   }
 }
 
+// All-to-all of 2 KB rows, one warp per row: (a) SM stores, 4 x 16 B per lane; (b) the row staged in shared
+// memory and written with one TMA bulk store (cp.async.bulk.global.shared::cta) to the peer address.
+template <int MODE>
+__global__ void __launch_bounds__(256) rows_a2a_kernel(const uint4* __restrict__ src, uint4** dsts, int P, int me,
+                                                       long long rows_per_peer) {
+  __shared__ __align__(128) uint4 stage[8][128];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long total = rows_per_peer * P;
+  for (long long r = static_cast<long long>(blockIdx.x) * 8 + warp; r < total; r += static_cast<long long>(gridDim.x) * 8) {
+    const int j = static_cast<int>(r / rows_per_peer);
+    const long long o = r % rows_per_peer;
+    const uint4* s = src + r * 128;
+    uint4* d = dsts[j] + (me * rows_per_peer + o) * 128;
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = s[lane + 32 * u];
+    if (MODE == 0) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) d[lane + 32 * u] = v[u];
+    } else {
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < 4; ++u) stage[warp][lane + 32 * u] = v[u];
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&stage[warp][0]));
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 2048;" ::"l"(d), "r"(sa) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+  }
+  if (MODE == 1 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 static float time_ms(cudaStream_t s, cudaEvent_t a, cudaEvent_t b) {
   float ms;
   CK(cudaEventSynchronize(b));
@@ -163,6 +199,44 @@ int main() {
     const double off = bytes * (ng - 1.0) / ng;
     printf("a2a %d GPUs grid %5d: %7.1f GB/s off-rank per GPU (%.1f us for %zu MiB/GPU)\n", ng, gi,
            off / worst / 1e6, worst * 1e3, bytes >> 20);
+  }
+  // 3b) row all-to-all: SM stores vs TMA bulk stores
+  {
+    std::vector<uint4**> dptr(ng);
+    for (int g = 0; g < ng; ++g) {
+      CK(cudaSetDevice(g));
+      CK(cudaMalloc(&dptr[g], sizeof(uint4*) * ng));
+      CK(cudaMemcpy(dptr[g], buf2.data(), sizeof(uint4*) * ng, cudaMemcpyHostToDevice));
+    }
+    const long long rows_per_peer = (bytes / 2048) / ng;
+    for (int mode = 0; mode < 2; ++mode)
+      for (int gi : {296, 592, 1184}) {
+        float worst = 0;
+        for (int it = 0; it < 3; ++it) {
+          for (int g = 0; g < ng; ++g) {
+            CK(cudaSetDevice(g));
+            CK(cudaDeviceSynchronize());
+          }
+          std::vector<cudaEvent_t> ea(ng), eb(ng);
+          for (int g = 0; g < ng; ++g) {
+            CK(cudaSetDevice(g));
+            CK(cudaEventCreate(&ea[g]));
+            CK(cudaEventCreate(&eb[g]));
+            CK(cudaEventRecord(ea[g], st[g]));
+            if (mode == 0) rows_a2a_kernel<0><<<gi, 256, 0, st[g]>>>(buf[g], dptr[g], ng, g, rows_per_peer);
+            else rows_a2a_kernel<1><<<gi, 256, 0, st[g]>>>(buf[g], dptr[g], ng, g, rows_per_peer);
+            CK(cudaEventRecord(eb[g], st[g]));
+          }
+          float mx = 0;
+          for (int g = 0; g < ng; ++g) {
+            CK(cudaSetDevice(g));
+            mx = std::max(mx, time_ms(st[g], ea[g], eb[g]));
+          }
+          if (it) worst = mx;
+        }
+        const double off = bytes * (ng - 1.0) / ng;
+        printf("rows a2a %s grid %5d: %7.1f GB/s off-rank per GPU\n", mode ? "TMA bulk" : "SM st  ", gi, off / worst / 1e6);
+      }
   }
   // 4) segmented all-to-all (push / pull), 64 B .. 2 KB segments
   {
