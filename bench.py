@@ -181,6 +181,17 @@ def reference_cpu(tokens_per_thread=256, threads=None, steps=1, seed=0):
                        f"train(steps=2) - train(steps=1) per thread, slowest thread, median of {steps}")
 
 
+def workload_config(S, world):
+    """The `config` object of both arms (same workload, metric and unit)."""
+    return {"workload": "C2: GPT-MoE layer d_model=1024 ffn=4096 64 experts top-1 "
+                        f"{S} tokens/GPU, GELU FFN experts, topo aux loss, capacity none, dX on",
+            "tokens_per_gpu": S, "global_tokens": world * S,
+            "parallelism": f"ep{world} (expert parallel, {C2['N'] // world} experts per GPU, "
+                           "all-to-all as NVLink peer stores fused into the kernels)" if world > 1
+            else "single GPU, 64 local experts",
+            "l2": "working set > L2 (1.07 GB expert weights + ~0.6 GB activations per step)"}
+
+
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return
@@ -188,8 +199,7 @@ def run_reference_arm(args, rank, world):
     line = {"metric": METRIC, "value": r["value"], "unit": r["unit"], "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C2 router/expert shape on the reference CPU path", "tokens_per_gpu": C2["S"],
-                       "d_model": C2["d"], "experts": C2["N"], "top_k": C2["k"]},
+            "config": workload_config(args.tokens, world),
             "cpu_baseline": {"value": r["value"], "unit": r["unit"], "cores": r["cores"], "kind": r["kind"],
                              "sample": r["sample"]},
             "e2e": {"value": r["value"], "unit": r["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -401,13 +411,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic (randn tokens/targets, random-init weights)",
-                "config": {"workload": "C2: GPT-MoE layer d_model=1024 ffn=4096 64 experts top-1 "
-                                       f"{S} tokens/GPU, GELU FFN experts, topo aux loss, capacity none, dX on",
-                           "tokens_per_gpu": S, "global_tokens": world * S,
-                           "parallelism": f"ep{world} (expert parallel, {C2['N'] // world} experts per GPU, "
-                                          "all-to-all as NVLink peer stores fused into the kernels)" if world > 1
-                           else "single GPU, 64 local experts",
-                           "l2": "working set > L2 (1.07 GB expert weights + ~0.6 GB activations per step)"},
+                "config": workload_config(S, world),
                 "roofline": roof, "all_to_all": a2a, "phases_ms": phases, "timed_steps_for_phases": tsteps,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": layer.launches_per_step() * args.steps,
                 "clocks": clocks, "losses_last_step": losses}
