@@ -25,6 +25,14 @@ sys.path.insert(0, ROOT)
 
 METRIC = "MoE-layer tokens/sec (fwd+bwd)"
 C2 = dict(S=16384, d=1024, d_out=1024, f=4096, N=64, k=1)
+# BASELINE configs timed by bench.py: c2 (default, the headline) and c4 (large layer, proportional capacity)
+CONFIGS = {
+    "c2": dict(C2, cap=0, cf=1.0, name="C2: GPT-MoE layer d_model=1024 ffn=4096 64 experts top-1",
+               extra="capacity none"),
+    "c4": dict(S=16384, d=4096, d_out=4096, f=16384, N=64, k=2, cap=3, cf=1.25,
+               name="C4: large MoE layer d_model=4096 ffn=16384 64 experts top-2",
+               extra="local proportional capacity cf 1.25"),
+}
 
 
 def parse():
@@ -33,7 +41,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--tokens", type=int, default=C2["S"], help="tokens per GPU")
+    ap.add_argument("--tokens", type=int, default=None, help="tokens per GPU (default: the config's)")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -181,15 +190,16 @@ def reference_cpu(tokens_per_thread=256, threads=None, steps=1, seed=0):
                        f"train(steps=2) - train(steps=1) per thread, slowest thread, median of {steps}")
 
 
-def workload_config(S, world):
+def workload_config(S, world, name="c2"):
     """The `config` object of both arms (same workload, metric and unit)."""
-    return {"workload": "C2: GPT-MoE layer d_model=1024 ffn=4096 64 experts top-1 "
-                        f"{S} tokens/GPU, GELU FFN experts, topo aux loss, capacity none, dX on",
+    c = CONFIGS[name]
+    wgb = 2 * 2 * c["N"] * c["d"] * c["f"] / 1e9
+    return {"workload": f"{c['name']} {S} tokens/GPU, GELU FFN experts, topo aux loss, {c['extra']}, dX on",
             "tokens_per_gpu": S, "global_tokens": world * S,
-            "parallelism": f"ep{world} (expert parallel, {C2['N'] // world} experts per GPU, "
+            "parallelism": f"ep{world} (expert parallel, {c['N'] // world} experts per GPU, "
                            "all-to-all as NVLink peer stores fused into the kernels)" if world > 1
-            else "single GPU, 64 local experts",
-            "l2": "working set > L2 (1.07 GB expert weights + ~0.6 GB activations per step)"}
+            else f"single GPU, {c['N']} local experts",
+            "l2": f"working set > L2 ({wgb:.2f} GB expert weights + activations per step)"}
 
 
 def run_reference_arm(args, rank, world):
@@ -199,7 +209,7 @@ def run_reference_arm(args, rank, world):
     line = {"metric": METRIC, "value": r["value"], "unit": r["unit"], "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(args.tokens, world),
+            "config": workload_config(args.tokens or CONFIGS[args.config]["S"], world, args.config),
             "cpu_baseline": {"value": r["value"], "unit": r["unit"], "cores": r["cores"], "kind": r["kind"],
                              "sample": r["sample"]},
             "e2e": {"value": r["value"], "unit": r["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -231,12 +241,14 @@ def main():
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    S = args.tokens
-    cfg = LayerConfig(P=1, S=S, d=C2["d"], d_out=C2["d_out"], N=C2["N"], k=C2["k"], f=C2["f"], act=ACT_GELU,
-                      cap_mode=0, aux_kind=LOSS_TOPO, need_dx=True, world_size=world, rank=rank)
+    W = CONFIGS[args.config]
+    S = args.tokens or W["S"]
+    cfg = LayerConfig(P=1, S=S, d=W["d"], d_out=W["d_out"], N=W["N"], k=W["k"], f=W["f"], act=ACT_GELU,
+                      cap_mode=W["cap"], capacity_factor=W["cf"], aux_kind=LOSS_TOPO, need_dx=True,
+                      world_size=world, rank=rank)
     # homogeneous NVSwitch profile: every off-diagonal beta equal, so c_hat is the even pattern
     beta = [[1.0] * world for _ in range(world)]
-    c_hat = ops.target_closed_form(beta, C2["N"], C2["k"], S)
+    c_hat = ops.target_closed_form(beta, W["N"], W["k"], S)
     nccl_id = None
     if world > 1:
         obj = [nccl_unique_id() if rank == 0 else None]
@@ -394,14 +406,15 @@ def main():
             "ridge_flop_per_byte": pk["bf16_sus"] * 1e12 / (pk["hbm"] * 1e9),
             "avg_launch_ms": avg_s * 1e3, "tensor_tflops": tflops, "tensor_frac_sustained": tflops / pk["bf16_sus"],
             "hbm_gbs": gbs, "hbm_frac": gbs / pk["hbm"],
-            "note": "launch durations from CUDA events on the step stream around each GEMM (eager phase steps)"}
+            "note": "launch durations from CUDA events on the step stream around each GEMM (eager phase steps); "
+                    "rows = nominal T*k (picks dropped by capacity not subtracted, pad rows not added)"}
     prof_traffic = os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")
     if os.path.exists(prof_traffic) and world == 1:
         with open(prof_traffic) as f:
             roof["traffic"] = json.load(f).get("traffic_bytes_per_launch")
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config == "c2":
         try:
             cpu = reference_cpu(steps=1, tokens_per_thread=128)
         except Exception as e:  # noqa: BLE001
@@ -411,7 +424,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic (randn tokens/targets, random-init weights)",
-                "config": workload_config(S, world),
+                "config": workload_config(S, world, args.config),
                 "roofline": roof, "all_to_all": a2a, "phases_ms": phases, "timed_steps_for_phases": tsteps,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": layer.launches_per_step() * args.steps,
                 "clocks": clocks, "losses_last_step": losses}
