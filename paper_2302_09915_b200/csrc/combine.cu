@@ -56,13 +56,15 @@ __global__ void __launch_bounds__(kCombWarps * 32) combine_loss_kernel(const __g
       rows[j] = (j < k) ? a.pos[t * k + j] : -1;
       g[j] = (j < k) ? a.gate[t * k + j] : 0.f;
       dot[j] = 0.f;
-      osrc[j] = nullptr;
+      // o_home: the expert output of pick t*k+j sits at that row of this rank (its address does not wait
+      // for pos; a dropped pick's row is stale and is zeroed after the load)
+      osrc[j] = (a.o_home && j < k) ? a.O.p[0] + (t * k + j) * a.dout : nullptr;
       odst[j] = nullptr;
       if (rows[j] >= 0) {
         const int ex = a.idx[t * k + j];
         const int owner = a.map.rank_of(ex);
         const long long r = a.map.row(rows[j], ex);
-        osrc[j] = a.o_home ? a.O.p[0] + static_cast<long long>(rows[j]) * a.dout : a.O.p[owner] + r * a.dout;
+        if (!a.o_home) osrc[j] = a.O.p[owner] + r * a.dout;
         odst[j] = a.dO.p[owner] + r * a.dout;
       }
     }
@@ -75,8 +77,10 @@ __global__ void __launch_bounds__(kCombWarps * 32) combine_loss_kernel(const __g
         const int v = v0 + 32 * u;
         yv[u] = v < nv ? y4[v] : make_uint4(0, 0, 0, 0);
 #pragma unroll
-        for (int j = 0; j < KM; ++j)
-          ov[j][u] = (rows[j] >= 0 && v < nv) ? reinterpret_cast<const uint4*>(osrc[j])[v] : make_uint4(0, 0, 0, 0);
+        for (int j = 0; j < KM; ++j) {
+          ov[j][u] = (osrc[j] && v < nv) ? reinterpret_cast<const uint4*>(osrc[j])[v] : make_uint4(0, 0, 0, 0);
+          if (rows[j] < 0) ov[j][u] = make_uint4(0, 0, 0, 0);
+        }
       }
 #pragma unroll
       for (int u = 0; u < kU; ++u) {

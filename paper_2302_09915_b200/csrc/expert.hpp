@@ -14,7 +14,6 @@ struct SwapPush {
   PeerBufs dst;
   const int* row_code = nullptr;
 };
-constexpr int kPushRowBits = 27;
 
 // out[R x M] = act(tokens[seg_g] . W_g^T), W_g = w[g] stored M x K. pre_out (optional) keeps the
 // activation derivative act'(pre-activation) for the backward pass.

@@ -231,16 +231,15 @@ struct EpiGateDx {
     const bool valid = tok < e.S;  // tcgen05.ld is warp-collective: every lane runs the loops
     const long long gtok = static_cast<long long>(ti.g) * e.S + tok;
     const int k = KT > 0 ? KT : e.k;
+    // the expert-path gradient of pick gtok*k+j sits at that row of dxp (pushed back by the expert dgrad
+    // epilogue): addresses are known up front; dropped picks (pos < 0, stale rows) are zeroed after the load
     const __nv_bfloat16* srcs[KM];
+    bool keep[KM];
 #pragma unroll
     for (int j = 0; j < KM; ++j) {
-      srcs[j] = nullptr;
-      const int r = (valid && j < k) ? e.pos[gtok * k + j] : -1;
-      if (r >= 0) {
-        const int ex = e.idx[gtok * k + j];
-        const int owner = e.map.rank_of(ex);
-        srcs[j] = e.dxp.p[owner] + e.map.row(r, ex) * e.d;
-      }
+      const bool in = valid && j < k;
+      srcs[j] = in ? e.dxp.p[0] + (gtok * k + j) * e.d : nullptr;
+      keep[j] = in && e.pos[gtok * k + j] >= 0;
     }
     constexpr int kCh = 4;  // BN = 256: four 32-column chunks per warp (every other chunk)
     if constexpr (KT > 0) {
@@ -253,6 +252,13 @@ struct EpiGateDx {
           for (int u = 0; u < 4; ++u)
             g[j][c][u] = srcs[j] ? reinterpret_cast<const uint4*>(srcs[j] + ti.n0 + 128 * h + 32 * c)[u]
                                  : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int j = 0; j < KM; ++j)
+        if (!keep[j])
+#pragma unroll
+          for (int c = 0; c < kCh; ++c)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) g[j][c][u] = make_uint4(0, 0, 0, 0);
 #pragma unroll
       for (int c = 0; c < kCh; ++c) {
         const int c0 = 128 * h + 32 * c;
@@ -271,7 +277,7 @@ struct EpiGateDx {
         load_acc32(tmem_tile, c0, v);
 #pragma unroll
         for (int j = 0; j < KM; ++j)
-          if (srcs[j])
+          if (keep[j])
 #pragma unroll
             for (int u = 0; u < 4; ++u) add8(v + 8 * u, reinterpret_cast<const uint4*>(srcs[j] + ti.n0 + c0)[u]);
         if (!valid) continue;

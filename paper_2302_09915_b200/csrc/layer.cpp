@@ -186,6 +186,9 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
     comp_ws_bytes_ = compulsory_workspace_bytes(c.P, c.S);
     arena_.reserve(comp_ws_, static_cast<long long>(comp_ws_bytes_));
   }
+  if (!ep_) arena_.reserve(ret_code_, r_max_);
+  trash_row_ = static_cast<int>(T * c.k);  // pick-ordered buffers: T*k rows + one trash row (<= r_max)
+  require(static_cast<long long>(trash_row_) < r_max_, "layer: receive buffers too small for the return rows");
   arena_.reserve(dz_, T * n64_);
   arena_.reserve(logits_, T * c.N);
   arena_.reserve(dldg_, T * c.k);
@@ -195,6 +198,7 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
   n_loss_part_ = combine_blocks(T);
   arena_.reserve(loss_part_, n_loss_part_);
   arena_.commit();
+  if (!ep_) ret_codes_.p[0] = ret_code_;
   if (ep_) {
     // barrier slots start at zero on every rank before any peer can signal: the memset is stream-ordered
     // before this rank's contribution to the handle all-gather that every peer waits for
@@ -211,6 +215,11 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
     for (int j = 0; j < c.world_size; ++j) {
       sig_.sig[j] = reinterpret_cast<unsigned int*>(bases_[j] + soff);
       sig_.counts_dst[j] = reinterpret_cast<int*>(bases_[j] + coff);
+    }
+    ret_code_ = plan_.push_row;
+    {
+      const long long roff = reinterpret_cast<char*>(plan_.push_row) - arena_.base();
+      for (int j = 0; j < c.world_size; ++j) ret_codes_.p[j] = reinterpret_cast<int*>(bases_[j] + roff);
     }
     if (global_ep_) {
       auto peer_of = [&](const void* local, int j) {
@@ -302,9 +311,9 @@ void Layer::experts_forward(const LayerIO& io, int G, int E, int /*nsub*/, const
   const LayerConfig& c = cfg_;
   PhaseTimer& tm = timer_;
   const int wm = G == E ? 0 : E;
-  // expert parallel: the expert outputs go straight back into each token's home rank
-  SwapPush push{peers(O_), plan_.push_row};
-  const SwapPush* pp = ep_ ? &push : nullptr;
+  // expert outputs go straight back to row token * k + slot of their home rank (peer stores under EP)
+  SwapPush push{peers(O_), ret_code_};
+  const SwapPush* pp = &push;
   if (c.f == 0) {
     grouped_fwd(xp_, io.w1, G, c.d_out, c.d, rows, seg_start, seg_rows, O_, nullptr, kActNone, s, wm, pp);
     tm.mark("expert_fwd", s);
@@ -321,9 +330,9 @@ void Layer::experts_backward(const LayerIO& io, int G, int E, int nsub, const in
   const LayerConfig& c = cfg_;
   PhaseTimer& tm = timer_;
   const int wm = G == E ? 0 : E;
-  // expert parallel: the expert-path input gradients go straight back into each token's home rank
-  SwapPush push{peers(dxp_), plan_.push_row};
-  const SwapPush* pp = ep_ ? &push : nullptr;
+  // expert-path input gradients go straight back to row token * k + slot of their home rank
+  SwapPush push{peers(dxp_), ret_code_};
+  const SwapPush* pp = &push;
   if (c.f == 0) {
     grouped_wgrad(dO_, xp_, E, c.d_out, c.d, rows, seg_start, seg_rows, io.dw1, s, nsub);
     tm.mark("expert_wgrad", s);
@@ -472,7 +481,7 @@ void Layer::step_local(const LayerIO& io, cudaStream_t s) {
   tm.begin(s);
   route_front(io, s);
   const PeerBufs zb = peers(dO_);
-  route_permute(rw_.dims, b, io.x, c.d, peers(xp_), r_max_, &zb, c.d_out, map_, s);
+  route_permute(rw_.dims, b, io.x, c.d, peers(xp_), r_max_, &zb, c.d_out, map_, s, &ret_codes_, 0, trash_row_);
   tm.mark("permute", s);
   experts_forward(io, c.N, c.N, 1, b.seg_start, b.seg_rows, r_max_, s);
   combine(io, s);
@@ -491,11 +500,16 @@ void Layer::step_ep(const LayerIO& io, cudaStream_t s) {
   tm.begin(s);
   route_front(io, s);
   ep_barrier(s, true);  // counts all-gather; also: every rank finished its previous step
-  ep_plan_device(plan_, W, E, c.rank, s);
+  {
+    EpPlanDev plan = plan_;
+    plan.push_row = nullptr;  // the return codes come from the sources' permute kernels
+    ep_plan_device(plan, W, E, c.rank, s);
+  }
   tm.mark("a2a_counts", s);
   // fused permute + dispatch: rows (and the owners' zero pad rows of dO) stored straight into the owners
   const PeerBufs zb = peers(dO_);
-  route_permute(rw_.dims, b, io.x, c.d, peers(xp_), r_local_, &zb, c.d_out, map_, s);
+  route_permute(rw_.dims, b, io.x, c.d, peers(xp_), r_local_, &zb, c.d_out, map_, s, &ret_codes_, c.rank,
+                trash_row_);
   ep_barrier(s, false);
   tm.mark("a2a_dispatch", s);
   experts_forward(io, E, E, 1, plan_.seg_start, plan_.seg_rows, r_max_, s);
@@ -545,12 +559,9 @@ void Layer::combine(const LayerIO& io, cudaStream_t s) {
   ca.pos = b.pos;
   ca.idx = b.idx;
   ca.gate = b.gate;
-  ca.O = peers(O_);
-  ca.o_home = ep_ ? 1 : 0;  // expert parallel: fwd2 already stored O into this rank's layout
-  if (ep_) {
-    ca.O = PeerBufs{};
-    ca.O.p[0] = O_;  // local pointer (peers() maps rank r -> rank r's copy)
-  }
+  ca.O = PeerBufs{};
+  ca.O.p[0] = O_;  // fwd2 stored the expert outputs at row token * k + slot of this rank (local pointer)
+  ca.o_home = 1;
   ca.y = io.y;
   ca.y_hat = io.y_hat;
   ca.dO = peers(dO_);
@@ -603,7 +614,7 @@ int Layer::launches_per_step() const {
   // gate, scan, bucket, capacity, permute, combine, dz, dW GEMM + reduce
   int n = 10;  // gate = logits GEMM + router
   // EP: + plan and return-map kernels + the device barriers (counts publish, dispatch, forward, combine, [dX])
-  if (ep_) n += 2 + (nccl_barrier() ? 0 : 4 + (cfg_.need_dx ? 1 : 0));
+  if (ep_) n += 1 + (nccl_barrier() ? 0 : 4 + (cfg_.need_dx ? 1 : 0));  // + the device plan
   if (global_ep_) n += 3 + (nccl_barrier() ? 0 : 1) + 3;  // broadcasts, barrier, global scan/bucket/capacity
   n += cfg_.f == 0 ? (1 + 1 + (cfg_.need_dx ? 1 : 0)) : (2 + 3 + (cfg_.need_dx ? 1 : 0));
   if (cfg_.need_dx) n += 1;

@@ -149,7 +149,12 @@ class Layer {
   std::unique_ptr<EpComm> ep_;
   // expert parallelism: device plan, peer-mapped arena bases, row map
   EpPlanDev plan_{};
-  EpSignal sig_{};                   // device barrier (counts publish + phase barriers)
+  EpSignal sig_{};
+  // return codes of this rank's receive rows (written by the permute of the rows' home ranks) and their
+  // peer views; expert outputs / input gradients are stored back at row token * k + slot of the home
+  int* ret_code_ = nullptr;
+  PeerInts ret_codes_{};
+  int trash_row_ = 0;                   // device barrier (counts publish + phase barriers)
   unsigned int* sig_slots_ = nullptr;  // [kMaxRanks] in the peer-mapped arena
   unsigned int* sig_epoch_ = nullptr;
   void ep_barrier(cudaStream_t s, bool publish_counts);

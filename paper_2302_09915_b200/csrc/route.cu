@@ -305,7 +305,9 @@ __global__ void __launch_bounds__(kPermWarps * 32) route_permute_kernel(RouteDim
                                                                         const __nv_bfloat16* __restrict__ x, int dx,
                                                                         const __grid_constant__ PeerBufs xp, int r_max,
                                                                         const __grid_constant__ PeerBufs zrows,
-                                                                        int has_z, int zdim, RowMap map) {
+                                                                        int has_z, int zdim, RowMap map,
+                                                                        const __grid_constant__ PeerInts codes,
+                                                                        int has_codes, int me, int trash_row) {
   extern __shared__ int sm[];
   const int N = d.N;
   int* start = sm;          // [N]
@@ -344,7 +346,10 @@ __global__ void __launch_bounds__(kPermWarps * 32) route_permute_kernel(RouteDim
   if (j < cnt[e]) {
     const int pick = b.clist[b.list_start[e] + j];
     const long long tok = pick / d.k;
-    if (lane == 0) b.pos[pick] = r;
+    if (lane == 0) {
+      b.pos[pick] = r;
+      if (has_codes) codes.p[dst_rank][drow] = (me << kPushRowBits) | pick;
+    }
     const uint4* src = reinterpret_cast<const uint4*>(x + tok * dx);
     // whole row in registers first (up to 8 x 16 B per lane), then the stores back to back
     constexpr int kU = 8;
@@ -358,6 +363,7 @@ __global__ void __launch_bounds__(kPermWarps * 32) route_permute_kernel(RouteDim
         if (v0 + 32 * u < nv) dst[v0 + 32 * u] = t[u];
     }
   } else {
+    if (lane == 0 && has_codes) codes.p[dst_rank][drow] = (me << kPushRowBits) | trash_row;
     const uint4 z = make_uint4(0, 0, 0, 0);
     for (int v = lane; v < nv; v += 32) dst[v] = z;
     if (has_z) {
@@ -407,13 +413,17 @@ void route_capacity(const RouteDims& d, const RouteBuffers& b, int mode, const i
 }
 
 void route_permute(const RouteDims& d, const RouteBuffers& b, const __nv_bfloat16* x, int dx, const PeerBufs& xp,
-                   int r_max, const PeerBufs* zrows, int zdim, const RowMap& map, cudaStream_t s) {
+                   int r_max, const PeerBufs* zrows, int zdim, const RowMap& map, cudaStream_t s,
+                   const PeerInts* codes, int me, int trash_row) {
   require(dx % 8 == 0 && (zrows == nullptr || zdim % 8 == 0), "permute: row widths must be multiples of 8");
   const int blocks = std::max(1, std::min((r_max + kPermWarps - 1) / kPermWarps, 8 * num_sms()));
   const size_t smem = sizeof(int) * (2 * d.N + 32);
   PeerBufs z{};
   if (zrows) z = *zrows;
-  route_permute_kernel<<<blocks, kPermWarps * 32, smem, s>>>(d, b, x, dx, xp, r_max, z, zrows ? 1 : 0, zdim, map);
+  PeerInts c{};
+  if (codes) c = *codes;
+  route_permute_kernel<<<blocks, kPermWarps * 32, smem, s>>>(d, b, x, dx, xp, r_max, z, zrows ? 1 : 0, zdim, map, c,
+                                                             codes ? 1 : 0, me, trash_row);
   TAMOE_CUDA(cudaGetLastError());
 }
 

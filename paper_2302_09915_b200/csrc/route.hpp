@@ -24,6 +24,13 @@ struct RowMap {
   }
 };
 
+// Return codes: the expert GEMMs store output row y of a rank's receive layout into rank (code >> 27) at row
+// (code & (2^27 - 1)) of its pick-ordered buffers (row = token * k + slot; pad rows go to a trash row).
+constexpr int kPushRowBits = 27;
+struct PeerInts {
+  int* p[kMaxRanks];
+};
+
 // The same buffer in every rank's address space (peer-mapped over NVLink; p[0] only when P == 1).
 struct PeerBufs {
   __nv_bfloat16* p[kMaxRanks];
@@ -106,8 +113,11 @@ void route_capacity(const RouteDims& d, const RouteBuffers& b, int mode, const i
 // Gather kept token rows into the padded expert-major layout (16-row segments, pad rows zeroed) and write
 // each row to wherever its owner expects it: `map`/`xp` (and the pad rows of `zrows`) may point into peer
 // ranks' memory, which fuses the dispatch all-to-all into the permute (NVLink stores).
+// codes (optional): for every row it writes, the permute also stores the row's return code into the owner's
+// code array (me << 27 | pick, pad rows -> me << 27 | trash_row).
 void route_permute(const RouteDims& d, const RouteBuffers& b, const __nv_bfloat16* x, int dx, const PeerBufs& xp,
-                   int r_max, const PeerBufs* zrows, int zdim, const RowMap& map, cudaStream_t s);
+                   int r_max, const PeerBufs* zrows, int zdim, const RowMap& map, cudaStream_t s,
+                   const PeerInts* codes = nullptr, int me = 0, int trash_row = 0);
 // Zero rows [seg_start + seg_real, seg_start + seg_rows) of each of G segments in buffers a and b.
 void zero_pad_rows(const int* seg_start, const int* seg_rows, const int* seg_real, int G, __nv_bfloat16* a, int wa,
                    __nv_bfloat16* b, int wb, cudaStream_t s);
