@@ -125,6 +125,7 @@ __global__ void peer_broadcast_kernel(const __grid_constant__ PeerWords dst, lon
     const unsigned int v = src[i];
     for (int r = 0; r < P; ++r) dst.p[r][off + i] = v;
   }
+  __threadfence_system();
 }
 
 }  // namespace

@@ -206,6 +206,7 @@ struct EpiSwap {
   }
   static __device__ __forceinline__ void finish(const Params&, int lane) {
     if (lane == 0) ptx::bulk_wait<0>();
+    if constexpr (V == 3) __threadfence_system();  // pushed rows visible before the phase barrier signals
     __syncwarp();
   }
 };

@@ -485,8 +485,9 @@ void Layer::step_local(const LayerIO& io, cudaStream_t s) {
   tm.mark("permute", s);
   experts_forward(io, c.N, c.N, 1, b.seg_start, b.seg_rows, r_max_, s);
   combine(io, s);
-  experts_backward(io, c.N, c.N, 1, b.seg_start, b.seg_rows, r_max_, s);
   gate_backward(io, s);
+  experts_backward(io, c.N, c.N, 1, b.seg_start, b.seg_rows, r_max_, s);
+  gate_backward_dx(io, s);
   tm.end(s);
 }
 
@@ -515,7 +516,8 @@ void Layer::step_ep(const LayerIO& io, cudaStream_t s) {
   experts_forward(io, E, E, 1, plan_.seg_start, plan_.seg_rows, r_max_, s);
   ep_barrier(s, false);
   tm.mark("a2a_barrier_fwd", s);
-  combine(io, s);  // loads expert outputs from the owners, stores dO into the owners
+  combine(io, s);  // reads the returned expert outputs, stores dO into the owners
+  gate_backward(io, s);  // dz + dWg need only local data: they overlap the dO stores' NVLink drain
   ep_barrier(s, false);
   tm.mark("a2a_barrier_combine", s);
   experts_backward(io, E, E, 1, plan_.seg_start, plan_.seg_rows, r_max_, s);
@@ -523,7 +525,7 @@ void Layer::step_ep(const LayerIO& io, cudaStream_t s) {
     ep_barrier(s, false);
     tm.mark("a2a_barrier_bwd", s);
   }
-  gate_backward(io, s);  // the dX epilogue loads the expert-path gradients from the owners
+  gate_backward_dx(io, s);  // the expert-path gradients were pushed back by the owners' dgrad1
   tm.end(s);
 }
 
@@ -601,6 +603,12 @@ void Layer::gate_backward(const LayerIO& io, cudaStream_t s) {
   tm.mark("gate_dz", s);
   gate_dw(io.x, dz_, c.P, c.S, c.d, n64_, n_pad_, c.N, dw_part_, dw_splits_, io.dwg, s);
   tm.mark("gate_dw", s);
+}
+
+void Layer::gate_backward_dx(const LayerIO& io, cudaStream_t s) {
+  const LayerConfig& c = cfg_;
+  const RouteBuffers& b = rw_.buf;
+  PhaseTimer& tm = timer_;
   if (c.need_dx) {
     // expert-path gradients are in this rank's layout (pushed back by the owners' dgrad1 in EP)
     PeerBufs home{};

@@ -134,7 +134,8 @@ class Layer {
                        cudaStream_t s);
   void experts_backward(const LayerIO& io, int G, int E, int nsub, const int* seg_start, const int* seg_rows, int rows,
                         cudaStream_t s);
-  void gate_backward(const LayerIO& io, cudaStream_t s);
+  void gate_backward(const LayerIO& io, cudaStream_t s);  // dz + dWg (local inputs only)
+  void gate_backward_dx(const LayerIO& io, cudaStream_t s);  // dX (needs the expert-path gradients)
   void combine(const LayerIO& io, cudaStream_t s);
   PeerBufs peers(__nv_bfloat16* local) const;
 
