@@ -395,7 +395,7 @@ void Layer::step(const LayerIO& io, cudaStream_t s) {
   require(c.f == 0 || (io.w2 && io.dw2), "layer step: FFN experts need w2 / dw2");
   require(!c.need_dx || io.dx, "layer step: need_dx set but dx is null");
   StepGraph& g = graph_;
-  if (timer_.enabled || !graphs_enabled() || !g.warm) {
+  if (timer_.enabled || !graphs_enabled() || !g.warm || g.disabled) {
     run_step(io, s);
     g.warm = true;
     return;
@@ -410,6 +410,13 @@ void Layer::step(const LayerIO& io, cudaStream_t s) {
   int slot = -1;
   for (int i = 0; i < StepGraph::kCache; ++i)
     if (g.exec[i] && std::memcmp(&g.io[i], &io, sizeof(LayerIO)) == 0) slot = i;
+  ++g.calls;
+  if (slot < 0 && ++g.misses > 8 && 2 * g.misses > g.calls) {
+    // the caller hands new buffers nearly every step: capturing costs more than it saves
+    g.disabled = true;
+    run_step(io, s);
+    return;
+  }
   if (slot < 0) {
     slot = 0;  // least recently used
     for (int i = 1; i < StepGraph::kCache; ++i)

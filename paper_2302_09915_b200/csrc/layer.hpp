@@ -187,6 +187,8 @@ class Layer {
     cudaGraphExec_t exec[kCache] = {};
     unsigned long long used[kCache] = {};
     unsigned long long tick = 0;
+    int misses = 0, calls = 0;  // captures vs replays: mostly misses -> buffers change every step -> eager
+    bool disabled = false;
     cudaStream_t stream = nullptr;
     cudaEvent_t in = nullptr, out = nullptr;
     ~StepGraph();

@@ -198,3 +198,18 @@ def test_layer_compulsory_quota_routing():
     np.testing.assert_array_equal(layer.read(ops.R_COUNTS, (P, N)), quotas)
     with pytest.raises(ops.ValidationError):  # top-1 only (trainer.cpp:124)
         TAMoELayer(LayerConfig(P=P, S=S, d=d, d_out=dout, N=N, k=2, aux_kind=2), c_hat)
+
+
+def test_layer_graph_falls_back_when_buffers_change():
+    """A caller handing new buffers every step would make every step a capture: after a few such misses the
+    layer runs eagerly; results stay bit-identical."""
+    P, S, d, dout, N, k, f = 1, 256, 256, 128, 8, 1, 256
+    layer, o, extra = run_case(P, S, d, dout, N, k, f, 0, 1, True)
+    x, y, params, yh = extra["args"]
+    ref = layer.losses.cpu().clone()
+    for _ in range(14):
+        yh2 = torch.zeros_like(yh)  # a fresh y_hat buffer each step
+        layer.step(x, y, params, y_hat=yh2)
+        torch.cuda.synchronize()
+        assert torch.equal(layer.losses.cpu(), ref)
+        assert torch.equal(yh2, yh)
