@@ -96,6 +96,7 @@ def check(layer, o, extra, P, S, N, k, f, need_dx):
     (2, 256, 256, 128, 4, 2, 0, 2, 1, True),    # local capacity
     (1, 384, 256, 128, 8, 2, 512, 0, 0, True),  # FFN expert (GELU), top-2
     (1, 1000, 512, 256, 16, 1, 256, 1, 1, True),  # FFN, global capacity, ragged S
+    (2, 208, 256, 128, 16, 4, 256, 2, 1, True),   # top-4 (runtime-k combine / dX paths), local capacity, ragged
 ])
 def test_layer_step_parity(P, S, d, dout, N, k, f, cap, kind, need_dx):
     layer, o, extra = run_case(P, S, d, dout, N, k, f, cap, kind, need_dx)
