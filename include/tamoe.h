@@ -132,6 +132,7 @@ typedef struct tamoe_router tamoe_router;
 #define TAMOE_R_LIST_START 11 /* int32  [N] start of each expert's range in CLIST */
 #define TAMOE_R_BAD 12        /* int32  [1] non-zero if a gate logit was non-finite */
 #define TAMOE_R_LOGITS 13     /* fp32   [P*S*N] (layer only) */
+#define TAMOE_R_GATE64 14     /* fp64   [P*S*k] gate_value in the reference's fp64 (standalone router only) */
 
 int tamoe_router_create(int P, int S, int N, int k, tamoe_router** out);
 int tamoe_router_destroy(tamoe_router* r);
@@ -146,6 +147,33 @@ int tamoe_router_route_gate(tamoe_router* r, const void* x, const void* wg, int 
 int tamoe_router_permute(tamoe_router* r, const void* x, int d, void* xp, int r_max, void* stream);
 /* Copy a routing array (TAMOE_R_*) to host or device memory; synchronises the stream. */
 int tamoe_router_read(tamoe_router* r, int what, void* dst, long long bytes, void* stream);
+
+/* ------------------------------------------------------------------ fp64 value-semantics gate operators
+ * The reference's gate API is fp64 (tad::Matrix, matrix.hpp:10-12).  These device entry points serve
+ * callers that keep that API (the drop-in shim integration/tad_gate_b200.cpp replacing gate.cpp) and follow
+ * the reference's arithmetic order: the matmuls are bit-identical (k ascending, zero skip, no FMA), exp is
+ * CUDA's (<= 1 ulp).  Device pointers, row-major; they synchronise `stream` only where a status depends on
+ * device data (non-finite logits). */
+
+/* softmax_rows (gate.cpp:12-28): probs [rows x cols]; may alias logits.  Status 2 on a non-finite logit. */
+int tamoe_softmax_rows_f64(const double* logits, int rows, int cols, double* probs, void* stream);
+/* gate_forward (gate.cpp:30-32): probs [S x N] = softmax_rows(x [S x d] * W [d x N]). */
+int tamoe_gate_forward_f64(const double* x, const double* w, int S, int d, int N, double* probs, void* stream);
+/* grad_aux_loss (gate.cpp:257-271): grad [d x N] = x^T dz, dz = p (coeff - <coeff, p>) row-wise;
+ * coeff is a HOST fp64 [N] vector (tamoe_aux_coefficients). */
+int tamoe_grad_aux_loss_f64(const double* x, const double* probs, const double* coeff, int S, int d, int N,
+                            double* grad, void* stream);
+
+/* Auxiliary losses on a routing result (host, N-vectors; counts int64 = RoutingResult::counts). */
+/* loss_balance (gate.cpp:209-214) */
+int tamoe_loss_balance(const long long* counts, const double* mean_probs, int N, int S, double* loss);
+/* loss_topo (gate.cpp:248-255): N * P * sum over the n = counts.size() entries; penalty [n] */
+int tamoe_loss_topo(const long long* counts, const double* mean_probs, const double* penalty, int n, int N, int P,
+                    int S, double* loss);
+/* balance_coefficients / topo_coefficients (gate.cpp:273-287) over n = counts.size() entries, scaled by
+ * N * P (topo): kind TAMOE_LOSS_BALANCE (penalty, N, P unused) or TAMOE_LOSS_TOPO. */
+int tamoe_aux_coefficients(int kind, const long long* counts, const double* penalty, int n, int N, int P, int S,
+                           double* coeff);
 
 /* ------------------------------------------------------------------ the MoE layer (trainer.cpp:243-356)
  * One step = gate -> route (capacity) -> permute -> experts -> combine -> task MSE + aux loss ->

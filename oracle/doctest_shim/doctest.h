@@ -6,6 +6,7 @@
 // CHECK_THROWS_AS and doctest::Approx(..).epsilon(..).
 #pragma once
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <functional>
@@ -77,6 +78,7 @@ int main() {
   int failed_cases = 0;
   for (const auto& c : registry()) {
     const long f0 = st().failures;
+    const auto t0 = std::chrono::steady_clock::now();
     for (int target = 0;; ++target) {
       st().target = target; st().seen = 0; st().entered = false;
       try { c.fn(); } catch (const RequireFailed&) {
@@ -86,6 +88,8 @@ int main() {
       if (st().seen <= target + 1) break;  // no further subcases
     }
     if (st().failures != f0) { ++failed_cases; std::fprintf(stderr, "FAILED: %s\n", c.name); }
+    std::fprintf(stderr, "[case] %-70s %8.3f s\n", c.name,
+                 std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
   }
   std::printf("[doctest-shim] test cases: %zu | failed: %d | checks: %ld | failed checks: %ld\n",
               registry().size(), failed_cases, st().checks, st().failures);

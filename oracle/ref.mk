@@ -30,3 +30,17 @@ TEST_SRCS := $(wildcard $(REF)/tests/test_*.cpp)
 tests: $(OUT)/unit_tests
 $(OUT)/unit_tests: $(OBJS) $(TEST_SRCS) oracle/doctest_shim/doctest.h
 	$(CXX) $(FLAGS) -Ioracle/doctest_shim -I$(REF)/tests -o $@ $(TEST_SRCS) $(OBJS)
+
+# The reference's own unit suite with gate.cpp REPLACED by the B200 drop-in shim
+# (integration/tad_gate_b200.cpp -> libtamoe.so): every gate / routing / aux-loss call of the suite, incl. the
+# ones inside the reference's train(), runs on the GPU.  Needs a GPU to run (the binary travels with gpurun).
+CUDA_HOME ?= /usr/local/cuda
+B200_LIB  := paper_2302_09915_b200/lib
+GATE_FREE_OBJS := $(filter-out $(OUT)/obj/gate.o,$(OBJS))
+suite_b200: $(OUT)/unit_tests_b200
+$(OUT)/obj/tad_gate_b200.o: integration/tad_gate_b200.cpp include/tamoe.h
+	@mkdir -p $(OUT)/obj
+	$(CXX) $(FLAGS) -Iinclude -I$(CUDA_HOME)/include -c $< -o $@
+$(OUT)/unit_tests_b200: $(GATE_FREE_OBJS) $(OUT)/obj/tad_gate_b200.o $(TEST_SRCS) oracle/doctest_shim/doctest.h $(B200_LIB)/libtamoe.so
+	$(CXX) $(FLAGS) -Ioracle/doctest_shim -I$(REF)/tests -o $@ $(TEST_SRCS) $(GATE_FREE_OBJS) $(OUT)/obj/tad_gate_b200.o \
+	  -L$(B200_LIB) -ltamoe -L$(CUDA_HOME)/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../../$(B200_LIB)'

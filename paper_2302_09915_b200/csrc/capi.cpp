@@ -13,6 +13,7 @@
 #include "ep.hpp"
 #include "expert.hpp"
 #include "gate.hpp"
+#include "gate_f64.hpp"
 #include "host_topology.hpp"
 #include "layer.hpp"
 #include "route.hpp"
@@ -55,6 +56,9 @@ ReadSpec route_array(const RouteWorkspace& rw, int what, const float* logits) {
     case TAMOE_R_CLIST: return {b.clist, picks * 4};
     case TAMOE_R_LIST_START: return {b.list_start, d.N * 4LL};
     case TAMOE_R_BAD: return {b.bad, 4};
+    case TAMOE_R_GATE64:
+      require(b.gate64 != nullptr, "fp64 gate values are only kept by the standalone router");
+      return {b.gate64, picks * 8};
     case TAMOE_R_LOGITS:
       require(logits != nullptr, "logits are only kept by the layer");
       return {logits, static_cast<long long>(d.P) * d.S * d.N * 4};
@@ -68,6 +72,23 @@ void read_array(const RouteWorkspace& rw, int what, void* dst, long long bytes, 
   TAMOE_CUDA(cudaMemcpyAsync(dst, r.src, r.bytes, cudaMemcpyDefault, s));
   TAMOE_CUDA(cudaStreamSynchronize(s));
 }
+
+// Stream-ordered device scratch for the fp64 operators.
+template <class T>
+struct DeviceScratch {
+  T* p = nullptr;
+  cudaStream_t s;
+  DeviceScratch(long long n, cudaStream_t st) : s(st) {
+    TAMOE_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * (n > 0 ? n : 1), s));
+  }
+  ~DeviceScratch() { cudaFreeAsync(p, s); }
+  T read(cudaStream_t st) const {
+    T v{};
+    TAMOE_CUDA(cudaMemcpyAsync(&v, p, sizeof(T), cudaMemcpyDeviceToHost, st));
+    TAMOE_CUDA(cudaStreamSynchronize(st));
+    return v;
+  }
+};
 
 void check_bad(const RouteWorkspace& rw, cudaStream_t s) {
   int bad = 0;
@@ -244,6 +265,74 @@ int tamoe_router_read(tamoe_router* r, int what, void* dst, long long bytes, voi
   return guarded([&] {
     require(r != nullptr, "read: null router");
     read_array(r->impl.rw, what, dst, bytes, static_cast<cudaStream_t>(stream), nullptr);
+  });
+}
+
+int tamoe_softmax_rows_f64(const double* logits, int rows, int cols, double* probs, void* stream) {
+  return guarded([&] {
+    require(rows >= 0 && cols >= 0 && (rows * static_cast<long long>(cols) == 0 || (logits && probs)),
+            "softmax_rows: null buffer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    DeviceScratch<int> bad(1, s);
+    TAMOE_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+    softmax_rows_f64(logits, probs, rows, cols, bad.p, s);
+    require(bad.read(s) == 0, "non-finite gate logit");
+  });
+}
+
+int tamoe_gate_forward_f64(const double* x, const double* w, int S, int d, int N, double* probs, void* stream) {
+  return guarded([&] {
+    require(S >= 0 && d >= 0 && N >= 0, "gate_forward: negative shape");
+    if (static_cast<long long>(S) * N == 0) return;
+    require(x && w && probs, "gate_forward: null buffer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    matmul_f64(x, w, probs, S, N, d, s);  // logits in place, then the row softmax
+    DeviceScratch<int> bad(1, s);
+    TAMOE_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+    softmax_rows_f64(probs, probs, S, N, bad.p, s);
+    require(bad.read(s) == 0, "non-finite gate logit");
+  });
+}
+
+int tamoe_grad_aux_loss_f64(const double* x, const double* probs, const double* coeff, int S, int d, int N,
+                            double* grad, void* stream) {
+  return guarded([&] {
+    require(S >= 0 && d >= 0 && N >= 0, "grad_aux_loss: negative shape");
+    if (static_cast<long long>(d) * N == 0) return;
+    require(grad && coeff && (S == 0 || (x && probs)), "grad_aux_loss: null buffer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    TAMOE_CUDA(cudaMemsetAsync(grad, 0, sizeof(double) * d * N, s));
+    if (S == 0) return;
+    DeviceScratch<double> c(N, s), dz(static_cast<long long>(S) * N, s);
+    TAMOE_CUDA(cudaMemcpyAsync(c.p, coeff, sizeof(double) * N, cudaMemcpyHostToDevice, s));
+    aux_dz_f64(probs, c.p, dz.p, S, N, s);
+    add_atb_f64(grad, x, dz.p, S, d, N, s);
+    TAMOE_CUDA(cudaStreamSynchronize(s));  // coeff is the caller's host memory
+  });
+}
+
+int tamoe_loss_balance(const long long* counts, const double* mean_probs, int N, int S, double* loss) {
+  return guarded([&] {
+    require(N >= 0 && (N == 0 || (counts && mean_probs)) && loss, "loss_balance: null buffer");
+    *loss = loss_balance(counts, mean_probs, N, S);
+  });
+}
+
+int tamoe_loss_topo(const long long* counts, const double* mean_probs, const double* penalty, int n, int N, int P,
+                    int S, double* loss) {
+  return guarded([&] {
+    require(n >= 0 && (n == 0 || (counts && mean_probs && penalty)) && loss, "loss_topo: null buffer");
+    *loss = loss_topo(counts, mean_probs, penalty, n, N, P, S);
+  });
+}
+
+int tamoe_aux_coefficients(int kind, const long long* counts, const double* penalty, int n, int N, int P, int S,
+                           double* coeff) {
+  return guarded([&] {
+    require(n >= 0 && (n == 0 || (counts && coeff)), "aux_coefficients: null buffer");
+    require(kind == TAMOE_LOSS_BALANCE || kind == TAMOE_LOSS_TOPO, "unknown aux loss kind");
+    auto c = aux_coefficients(kind, counts, penalty, n, N, P, S);
+    if (n) std::memcpy(coeff, c.data(), sizeof(double) * n);
   });
 }
 

@@ -133,4 +133,33 @@ std::vector<double> device_payload_tokens(const double* counts, int P, int N) {
   return out;
 }
 
+// gate.cpp:209-214: sum_e m_e * (c_e / S), expert order
+double loss_balance(const long long* counts, const double* mean_probs, int N, int S) {
+  double loss = 0.0;
+  for (int e = 0; e < N; ++e) loss += mean_probs[e] * (static_cast<double>(counts[e]) / S);
+  return loss;
+}
+
+// gate.cpp:248-255: N * P * sum_e p_e * m_e * (c_e / S)
+double loss_topo(const long long* counts, const double* mean_probs, const double* penalty, int n, int N, int P, int S) {
+  double loss = 0.0;
+  for (int e = 0; e < n; ++e) loss += penalty[e] * mean_probs[e] * (static_cast<double>(counts[e]) / S);
+  return static_cast<double>(N) * P * loss;
+}
+
+// gate.cpp:273-287: balance c_e / S^2; topo N*P/S^2 * p_e * c_e
+std::vector<double> aux_coefficients(int kind, const long long* counts, const double* penalty, int n, int N, int P,
+                                     int S) {
+  std::vector<double> coeff(static_cast<size_t>(n));
+  if (kind == 0) {
+    const double s2 = static_cast<double>(S) * S;
+    for (int e = 0; e < n; ++e) coeff[e] = static_cast<double>(counts[e]) / s2;
+  } else {
+    require(penalty != nullptr, "topo coefficients need the penalty row");
+    const double scale = static_cast<double>(N) * P / (static_cast<double>(S) * S);
+    for (int e = 0; e < n; ++e) coeff[e] = scale * penalty[e] * static_cast<double>(counts[e]);
+  }
+  return coeff;
+}
+
 }  // namespace tamoe

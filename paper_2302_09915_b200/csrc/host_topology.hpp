@@ -8,6 +8,11 @@ std::vector<double> penalty_weights(const double* c_hat_row, int n, int norm, do
 std::vector<double> target_closed_form(const double* beta, int P, int N, int k, int S);
 std::vector<long long> capacity_caps(int mode, double cf, int k, int S, int N, int P, const double* c_hat);
 std::vector<double> device_payload_tokens(const double* counts, int P, int N);
+// Auxiliary losses / gradient coefficients on a routing result (gate.cpp:209-214, 248-255, 273-287).
+double loss_balance(const long long* counts, const double* mean_probs, int N, int S);
+double loss_topo(const long long* counts, const double* mean_probs, const double* penalty, int n, int N, int P, int S);
+std::vector<double> aux_coefficients(int kind, const long long* counts, const double* penalty, int n, int N, int P,
+                                     int S);
 
 // ---- measured-topology pipeline (host_profile.cpp)
 std::vector<int> check_tree_levels(const int* levels, int n_levels, int P);

@@ -27,7 +27,7 @@ void Arena::commit() {
   for (const Slot& s : slots_) *s.ptr = base_ + s.off;
 }
 
-void RouteWorkspace::reserve(Arena& a, int P, int S, int N, int k) {
+void RouteWorkspace::reserve(Arena& a, int P, int S, int N, int k, bool with_gate64) {
   require(P >= 1 && S >= 1, "P and S must be positive");
   require(N >= 1 && N <= 1024, "N must be in [1, 1024]");
   require(k >= 1 && k <= N, "k must be in [1, N]");
@@ -60,6 +60,7 @@ void RouteWorkspace::reserve(Arena& a, int P, int S, int N, int k) {
   a.reserve(buf.bad, 1);
   a.reserve(buf.logits, static_cast<long long>(P) * S * N);
   a.reserve(caps, static_cast<long long>(P) * N);
+  if (with_gate64) a.reserve(buf.gate64, picks);
 }
 
 void RouteWorkspace::upload_caps(const long long* caps_host, cudaStream_t s) {
@@ -76,7 +77,7 @@ void RouteWorkspace::finish(int mode, cudaStream_t s) const {
 }
 
 Router::Router(int P, int S, int N, int k) {
-  rw.reserve(arena, P, S, N, k);
+  rw.reserve(arena, P, S, N, k, /*with_gate64=*/true);
   arena.commit();
 }
 

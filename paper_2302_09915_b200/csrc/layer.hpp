@@ -44,11 +44,11 @@ struct RouteWorkspace {
   RouteDims dims{};
   RouteBuffers buf{};
   int* caps = nullptr;  // [P*N] int32
-  void reserve(Arena& a, int P, int S, int N, int k);
+  void reserve(Arena& a, int P, int S, int N, int k, bool with_gate64 = false);
   void upload_caps(const long long* caps_host, cudaStream_t s);
   // gate outputs view of the workspace
   RowRouteOut row_out(float* logits, double* probs) const {
-    return RowRouteOut{buf.idx, buf.gate, buf.score, buf.hist4, buf.msum4, logits, probs, buf.bad};
+    return RowRouteOut{buf.idx, buf.gate, buf.score, buf.hist4, buf.msum4, logits, probs, buf.bad, buf.gate64};
   }
   void finish(int mode, cudaStream_t s) const;  // bucket + capacity
 };

@@ -76,6 +76,7 @@ struct RouteBuffers {
   int* total_rows = nullptr;  // [1]
   int* bad = nullptr;         // [1] non-finite logit flag
   float* logits = nullptr;    // [P*S*N] gate logits scratch (router API without a caller buffer)
+  double* gate64 = nullptr;   // [P*S*k] fp64 gate values (standalone router only; the layer uses fp32 gate)
 };
 
 // Gate epilogue / standalone router outputs (per-row routing, see gate.cu).
@@ -88,6 +89,7 @@ struct RowRouteOut {
   float* logits;  // optional [P*S*N]
   double* probs;  // optional [P*S*N]
   int* bad;
+  double* gate64 = nullptr;  // optional [P*S*k] fp64 gate values (reference Assignment::gate_value)
 };
 
 // Top-k selection from fp64 probabilities (P x S x N), the reference's topk_route input.

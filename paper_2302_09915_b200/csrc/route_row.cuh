@@ -80,7 +80,9 @@ __device__ __forceinline__ void finish_row(const TopK<KM>& tk, bool valid, long 
         const long long a = gtok * k + j;
         o.idx[a] = tk.e[j];
         o.score[a] = tk.p[j];
-        o.gate[a] = static_cast<float>(k == 1 ? tk.p[j] : tk.p[j] / mass);
+        const double g = k == 1 ? tk.p[j] : tk.p[j] / mass;
+        o.gate[a] = static_cast<float>(g);
+        if (o.gate64) o.gate64[a] = g;
       }
     }
   }

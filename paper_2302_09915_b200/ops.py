@@ -198,12 +198,12 @@ def device_payload_tokens(counts) -> np.ndarray:
 
 # ----------------------------------------------------------------------------- device router
 R_IDX, R_GATE, R_SCORE, R_KEPT, R_POS, R_COUNTS, R_DROPPED, R_MEAN_PROBS, R_SEG_START, R_SEG_ROWS, R_CLIST, \
-    R_LIST_START, R_BAD, R_LOGITS = range(14)
+    R_LIST_START, R_BAD, R_LOGITS, R_GATE64 = range(15)
 
 _R_DTYPES = {R_IDX: np.int32, R_GATE: np.float32, R_SCORE: np.float64, R_KEPT: np.uint8, R_POS: np.int32,
              R_COUNTS: np.int32, R_DROPPED: np.int32, R_MEAN_PROBS: np.float64, R_SEG_START: np.int32,
              R_SEG_ROWS: np.int32, R_CLIST: np.int32, R_LIST_START: np.int32, R_BAD: np.int32,
-             R_LOGITS: np.float32}
+             R_LOGITS: np.float32, R_GATE64: np.float64}
 
 
 def _stream():
@@ -233,6 +233,7 @@ class Router:
         picks = self.P * self.S * self.k
         pn = self.P * self.N
         return {R_IDX: (self.P, self.S, self.k), R_GATE: (self.P, self.S, self.k), R_SCORE: (self.P, self.S, self.k),
+                R_GATE64: (self.P, self.S, self.k),
                 R_KEPT: (self.P, self.S, self.k), R_POS: (self.P, self.S, self.k), R_COUNTS: (self.P, self.N),
                 R_DROPPED: (self.P, self.N), R_MEAN_PROBS: (self.P, self.N), R_SEG_START: (self.N,),
                 R_SEG_ROWS: (self.N,), R_CLIST: (picks,), R_LIST_START: (self.N,), R_BAD: (1,)}[what] if what != R_LOGITS \
@@ -285,6 +286,14 @@ for _name, _args in {
     "tamoe_router_permute": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
                              ctypes.c_void_p],
     "tamoe_router_read": [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p],
+    "tamoe_softmax_rows_f64": [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p],
+    "tamoe_gate_forward_f64": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                               ctypes.c_void_p, ctypes.c_void_p],
+    "tamoe_grad_aux_loss_f64": [ctypes.c_void_p, ctypes.c_void_p, _D, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                ctypes.c_void_p, ctypes.c_void_p],
+    "tamoe_loss_balance": [_L, _D, ctypes.c_int, ctypes.c_int, _D],
+    "tamoe_loss_topo": [_L, _D, _D, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _D],
+    "tamoe_aux_coefficients": [ctypes.c_int, _L, _D, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _D],
 }.items():
     getattr(_lib.lib, _name).argtypes = _args
     getattr(_lib.lib, _name).restype = ctypes.c_int
@@ -335,7 +344,7 @@ def topk_route(probs, k: int, policy: CapacityPolicy = CapacityPolicy(), c_hat=N
     caps = capacity_caps(policy, k, S, N, P, c_hat)
     r = Router(P, S, N, k)
     r.route_probs(p.to("cuda").contiguous(), policy, caps)
-    idx, gate, score, kept = r.read(R_IDX), r.read(R_GATE), r.read(R_SCORE), r.read(R_KEPT)
+    idx, gate, score, kept = r.read(R_IDX), r.read(R_GATE64), r.read(R_SCORE), r.read(R_KEPT)
     counts, dropped, mp = r.read(R_COUNTS), r.read(R_DROPPED), r.read(R_MEAN_PROBS)
     order = r.expert_order()
     res = [RoutingResult(idx[i], gate[i], score[i], kept[i].astype(bool), counts[i].astype(np.int64),
@@ -343,12 +352,88 @@ def topk_route(probs, k: int, policy: CapacityPolicy = CapacityPolicy(), c_hat=N
     return res[0] if single else res
 
 
+def _cll(a):
+    a = np.ascontiguousarray(a, dtype=np.int64)
+    return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong))
+
+
+def _cd(a):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
 def loss_balance(result: RoutingResult, S: int) -> float:  # gate.cpp:209-214
-    return float(np.sum(result.mean_probs * (result.counts / S)))
+    c, cp = _cll(result.counts)
+    m, mp = _cd(result.mean_probs)
+    out = ctypes.c_double()
+    _lib.call("tamoe_loss_balance", cp, mp, c.shape[0], S, ctypes.byref(out))
+    return out.value
 
 
 def loss_topo(result: RoutingResult, penalty, N: int, P: int, S: int) -> float:  # gate.cpp:248-255
-    penalty = np.asarray(penalty, np.float64)
-    if penalty.shape[0] != result.counts.shape[0]:
+    pen, pp = _cd(penalty)
+    if pen.shape[0] != result.counts.shape[0]:
         raise ValidationError("penalty row size does not match expert count")
-    return float(N) * P * float(np.sum(penalty * result.mean_probs * (result.counts / S)))
+    c, cp = _cll(result.counts)
+    m, mp = _cd(result.mean_probs)
+    out = ctypes.c_double()
+    _lib.call("tamoe_loss_topo", cp, mp, pp, c.shape[0], N, P, S, ctypes.byref(out))
+    return out.value
+
+
+def balance_coefficients(result: RoutingResult, S: int) -> np.ndarray:  # gate.cpp:273-278
+    c, cp = _cll(result.counts)
+    out, op = _cd(np.zeros(c.shape[0]))
+    _lib.call("tamoe_aux_coefficients", 0, cp, None, c.shape[0], 0, 0, S, op)
+    return out
+
+
+def topo_coefficients(result: RoutingResult, penalty, N: int, P: int, S: int) -> np.ndarray:  # gate.cpp:280-287
+    c, cp = _cll(result.counts)
+    pen, pp = _cd(penalty)
+    if pen.shape[0] < c.shape[0]:
+        raise ValidationError("penalty row size does not match expert count")
+    out, op = _cd(np.zeros(c.shape[0]))
+    _lib.call("tamoe_aux_coefficients", 1, cp, pp, c.shape[0], N, P, S, op)
+    return out
+
+
+def softmax_rows(logits) -> torch.Tensor:
+    """softmax_rows (gate.cpp:12-28) on the device in fp64, the reference's order.  Returns fp64 [S, N] (cuda)."""
+    z = torch.as_tensor(logits, dtype=torch.float64).to("cuda").contiguous()
+    out = torch.empty_like(z)
+    _lib.call("tamoe_softmax_rows_f64", ctypes.c_void_p(z.data_ptr()), z.shape[0], z.shape[1],
+              ctypes.c_void_p(out.data_ptr()), _stream())
+    return out
+
+
+def gate_forward_f64(x, W) -> torch.Tensor:
+    """gate_forward (gate.cpp:30-32) with the reference's fp64 semantics: bit-identical x W on the device,
+    then softmax_rows.  x [S, d], W [d, N] -> fp64 [S, N] (cuda)."""
+    xd = torch.as_tensor(x, dtype=torch.float64).to("cuda").contiguous()
+    wd = torch.as_tensor(W, dtype=torch.float64).to("cuda").contiguous()
+    if xd.shape[1] != wd.shape[0]:
+        raise ValidationError("gate_forward: x columns must match W rows")
+    out = torch.empty(xd.shape[0], wd.shape[1], dtype=torch.float64, device="cuda")
+    _lib.call("tamoe_gate_forward_f64", ctypes.c_void_p(xd.data_ptr()), ctypes.c_void_p(wd.data_ptr()), xd.shape[0],
+              xd.shape[1], wd.shape[1], ctypes.c_void_p(out.data_ptr()), _stream())
+    return out
+
+
+def grad_aux_loss(x, probs, coeff) -> torch.Tensor:
+    """grad_aux_loss (gate.cpp:257-271) on the device in fp64: x^T (p (coeff - <coeff, p>)), [d, N]."""
+    xd = torch.as_tensor(x, dtype=torch.float64).to("cuda").contiguous()
+    pd = torch.as_tensor(probs, dtype=torch.float64).to("cuda").contiguous()
+    c, cp = _cd(coeff)
+    out = torch.empty(xd.shape[1], pd.shape[1], dtype=torch.float64, device="cuda")
+    _lib.call("tamoe_grad_aux_loss_f64", ctypes.c_void_p(xd.data_ptr()), ctypes.c_void_p(pd.data_ptr()), cp,
+              pd.shape[0], xd.shape[1], pd.shape[1], ctypes.c_void_p(out.data_ptr()), _stream())
+    return out
+
+
+def grad_loss_balance(x, probs, result: RoutingResult, S: int) -> torch.Tensor:  # gate.cpp:289-291
+    return grad_aux_loss(x, probs, balance_coefficients(result, S))
+
+
+def grad_loss_topo(x, probs, result: RoutingResult, penalty, N: int, P: int, S: int) -> torch.Tensor:  # :293-296
+    return grad_aux_loss(x, probs, topo_coefficients(result, penalty, N, P, S))

@@ -102,3 +102,27 @@ def test_device_payload_tokens():
     for i in range(4):
         for j in range(4):
             assert pay[i, j] == counts[i, 2 * j:2 * j + 2].sum()
+
+
+def test_aux_losses_and_coefficients_match_oracle():
+    """loss_balance / loss_topo / *_coefficients (gate.cpp:209-214, 248-255, 273-287) through the C ABI are
+    bit-identical to the oracle restatement (itself pinned to the compiled reference in test_oracle_ref)."""
+    from paper_2302_09915_b200 import ops
+    O = oracle.orc()
+    rng = np.random.default_rng(7)
+    for N, P, S in [(4, 4, 24), (8, 2, 1024), (64, 8, 16384), (6, 1, 30)]:
+        counts = rng.integers(0, S, N).astype(np.int64)
+        mean = rng.dirichlet(np.ones(N))
+        pen = ops.penalty_weights(rng.uniform(0.5, 40.0, N))
+        res = ops.RoutingResult(None, None, None, None, counts, np.zeros(N, np.int64), mean, [])
+        assert ops.loss_balance(res, S) == O.loss_balance(counts, mean, S)
+        assert ops.loss_topo(res, pen, N, P, S) == O.loss_topo(counts, mean, pen, P, S)
+        assert np.array_equal(ops.topo_coefficients(res, pen, N, P, S), O.topo_coefficients(counts, pen, P, S))
+        assert np.array_equal(ops.balance_coefficients(res, S), O.balance_coefficients(counts, S))
+        if oracle.ref_available():
+            R = oracle.ref()
+            assert ops.loss_balance(res, S) == R.loss_balance(counts, mean, S)
+            assert ops.loss_topo(res, pen, N, P, S) == R.loss_topo(counts, mean, pen, P, S)
+    with pytest.raises(ops.ValidationError):
+        ops.loss_topo(ops.RoutingResult(None, None, None, None, np.zeros(4, np.int64), None, np.zeros(4), []),
+                      np.ones(3), 4, 1, 8)

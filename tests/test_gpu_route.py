@@ -34,6 +34,7 @@ def check_same(gpu, orc, P, S, k, N):
     assert np.array_equal(idx, orc["expert"])
     assert np.array_equal(score, orc["score"])          # same fp64 inputs -> identical bits
     np.testing.assert_allclose(gate, orc["gate"], rtol=1e-6)
+    assert np.array_equal(gpu.read(ops.R_GATE64), orc["gate"])  # fp64 gate_value: same expression, same bits
     assert np.array_equal(kept, orc["kept"])
     assert np.array_equal(gpu.read(ops.R_COUNTS), orc["counts"])
     assert np.array_equal(gpu.read(ops.R_DROPPED), orc["dropped"])
