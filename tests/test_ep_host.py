@@ -1,4 +1,4 @@
-"""Expert-parallel host logic on the CPU with world_size-2/4 gloo process groups.
+"""Expert-parallel host logic on the CPU with world_size-2/4/8 gloo process groups.
 
 Each rank routes its own process' tokens (oracle topk_route over all processes -- the
 reference's multi-process semantics), packs its kept picks in (expert, token) order with
@@ -92,7 +92,7 @@ def _worker(rank, world, port, mode, k, errq):
         raise
 
 
-@pytest.mark.parametrize("world,mode,k", [(2, 0, 1), (2, 3, 2), (4, 2, 2), (4, 3, 1)])
+@pytest.mark.parametrize("world,mode,k", [(2, 0, 1), (2, 3, 2), (4, 2, 2), (4, 3, 1), (8, 3, 1), (8, 2, 2)])
 def test_ep_exchange_layout_gloo(world, mode, k):
     ctx = mp.get_context("spawn")
     errq = ctx.SimpleQueue()
