@@ -94,6 +94,12 @@ int tamoe_smooth_profile(const int* levels, int n_levels, const double* alpha, c
 int tamoe_p2p_sweep(const void* nccl_id128, int world, int rank, const double* sizes_mb, int nsizes, int reps,
                     int warmup, double* time_us);
 
+/* Heterogeneous-topology emulation (BASELINE config 5): ranks in different groups of `group_size` consecutive
+ * ranks exchange over a link throttled `repeat` times -- every payload store to such a peer (dispatch, expert
+ * output return, dO, dX return, and the p2p sweep's copies) is issued `repeat` times, so the link delivers
+ * 1/repeat of its bandwidth.  Process-wide; applies to layers / sweeps created afterwards.  (0, 1) = off. */
+int tamoe_set_link_emulation(int group_size, int repeat);
+
 /* exchange_cost (comm_cost.cpp:24-55): c = dispatch matrix [P x N] tokens, payload d * b bytes per token.
  * pair_cost_us[P x P] (optional); summary[4] = bottleneck_us, total_bytes, size_exchange_us, total_estimate_us. */
 int tamoe_exchange_cost(const double* alpha, const double* beta, const double* c, int P, int N, int d, int b,

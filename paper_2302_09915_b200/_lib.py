@@ -50,6 +50,7 @@ SIGNATURES = {
     "tamoe_smooth_profile": [_I, c_int, _D, _D, c_int, c_double, _D, _D, _D, _D],
     "tamoe_exchange_cost": [_D, _D, _D, c_int, c_int, c_int, c_int, c_int, _D, _D],
     "tamoe_p2p_sweep": [_P, c_int, c_int, _D, c_int, c_int, c_int, _D],
+    "tamoe_set_link_emulation": [c_int, c_int],
     "tamoe_grouped_fwd": [_P, _P, c_int, c_int, c_int, c_int, _P, _P, _P, _P, c_int, _P],
     "tamoe_grouped_dgrad": [_P, _P, c_int, c_int, c_int, c_int, _P, _P, _P, _P, c_int, _P],
     "tamoe_grouped_wgrad": [_P, _P, c_int, c_int, c_int, c_int, _P, _P, _P, _P],

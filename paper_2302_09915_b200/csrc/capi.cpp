@@ -398,6 +398,14 @@ int tamoe_p2p_sweep(const void* nccl_id128, int world, int rank, const double* s
   });
 }
 
+int tamoe_set_link_emulation(int group_size, int repeat) {
+  return guarded([&] {
+    require(group_size >= 0 && repeat >= 1 && repeat <= 255, "link emulation: group_size >= 0, repeat in [1, 255]");
+    link_emulation().group_size = group_size;
+    link_emulation().repeat = repeat;
+  });
+}
+
 int tamoe_nccl_unique_id(void* out128) {
   return guarded([&] {
     require(out128 != nullptr, "nccl_unique_id: null output");

@@ -51,6 +51,7 @@ __global__ void __launch_bounds__(kCombWarps * 32) combine_loss_kernel(const __g
     float g[KM], dot[KM];
     const __nv_bfloat16* osrc[KM];
     __nv_bfloat16* odst[KM];
+    int orep[KM];
 #pragma unroll
     for (int j = 0; j < KM; ++j) {
       rows[j] = (j < k) ? a.pos[t * k + j] : -1;
@@ -60,12 +61,14 @@ __global__ void __launch_bounds__(kCombWarps * 32) combine_loss_kernel(const __g
       // for pos; a dropped pick's row is stale and is zeroed after the load)
       osrc[j] = (a.o_home && j < k) ? a.O.p[0] + (t * k + j) * a.dout : nullptr;
       odst[j] = nullptr;
+      orep[j] = 1;
       if (rows[j] >= 0) {
         const int ex = a.idx[t * k + j];
         const int owner = a.map.rank_of(ex);
         const long long r = a.map.row(rows[j], ex);
         if (!a.o_home) osrc[j] = a.O.p[owner] + r * a.dout;
         odst[j] = a.dO.p[owner] + r * a.dout;
+        orep[j] = a.dO.rep[owner];
       }
     }
     const int nv = a.dout / 8;
@@ -112,7 +115,9 @@ __global__ void __launch_bounds__(kCombWarps * 32) combine_loss_kernel(const __g
               dot[j] += r[i] * o[j][i];
               go[i] = a.mse_scale * g[j] * r[i];
             }
-            reinterpret_cast<uint4*>(odst[j])[v] = pack8(go);
+            const uint4 gv = pack8(go);
+            reinterpret_cast<uint4*>(odst[j])[v] = gv;
+            if (orep[j] > 1) store_repeat(reinterpret_cast<uint4*>(odst[j]) + v, gv, orep[j]);
           }
         }
       }

@@ -120,7 +120,8 @@ std::vector<double> P2PProbe::sweep(const double* sizes_mb, int nsizes, int reps
           comm_.barrier(flag_, stream_);  // everybody idle, previous transfer done
           if (me == src) {
             TAMOE_CUDA(cudaEventRecord(e0, stream_));
-            p2p_copy(bases_[static_cast<size_t>(dst)] + max_bytes_, buf_, bytes, stream_);
+            p2p_copy(bases_[static_cast<size_t>(dst)] + max_bytes_, buf_, bytes, stream_,
+                     link_emulation().factor(src, dst));
             TAMOE_CUDA(cudaEventRecord(e1, stream_));
             TAMOE_CUDA(cudaEventSynchronize(e1));
             float ms = 0.f;

@@ -100,7 +100,7 @@ class P2PProbe {
   int* flag_ = nullptr;
 };
 
-void p2p_copy(void* dst, const void* src, size_t bytes, cudaStream_t s);
+void p2p_copy(void* dst, const void* src, size_t bytes, cudaStream_t s, int rep = 1);
 
 // Host reference of the receive plan (CPU-testable): recv[src][e] (P x E) rows -> per local expert the
 // segment seg_start/seg_rows [E] and the row where each source's rows for it start, src_off [P x E].

@@ -100,7 +100,7 @@ __global__ void ep_barrier_kernel(const __grid_constant__ EpSignal a) {
 
 // Peer copy of the P2P sweep: 16-byte vectors, 8 per lane in flight, grid of 2 CTAs per SM.
 __global__ void __launch_bounds__(512) p2p_copy_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src,
-                                                       long long n) {
+                                                       long long n, int rep) {
   constexpr int kU = 8;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x * kU;
   for (long long i0 = static_cast<long long>(blockIdx.x) * blockDim.x * kU + threadIdx.x; i0 < n; i0 += stride) {
@@ -114,6 +114,13 @@ __global__ void __launch_bounds__(512) p2p_copy_kernel(uint4* __restrict__ dst, 
     for (int u = 0; u < kU; ++u) {
       const long long i = i0 + static_cast<long long>(u) * blockDim.x;
       if (i < n) dst[i] = v[u];
+    }
+    if (rep > 1) {
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const long long i = i0 + static_cast<long long>(u) * blockDim.x;
+        if (i < n) store_repeat(dst + i, v[u], rep);
+      }
     }
   }
 }
@@ -138,12 +145,13 @@ void peer_broadcast_words(const PeerWords& dst, long long dst_off_words, const v
   TAMOE_CUDA(cudaGetLastError());
 }
 
-void p2p_copy(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+void p2p_copy(void* dst, const void* src, size_t bytes, cudaStream_t s, int rep) {
   require(bytes % 16 == 0, "p2p copy: size must be a multiple of 16 bytes");
   const long long n = static_cast<long long>(bytes / 16);
   const long long per_block = 512LL * 8;
   const int grid = static_cast<int>(std::min<long long>(2LL * num_sms(), (n + per_block - 1) / per_block));
-  p2p_copy_kernel<<<std::max(grid, 1), 512, 0, s>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src), n);
+  p2p_copy_kernel<<<std::max(grid, 1), 512, 0, s>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src), n,
+                                                         rep);
   TAMOE_CUDA(cudaGetLastError());
 }
 

@@ -185,6 +185,8 @@ struct EpiSwap {
             __nv_bfloat16* dst = e.push.dst.p[code >> kPushRowBits] +
                                  static_cast<long long>(code & ((1 << kPushRowBits) - 1)) * e.ld + mcol + (lane & 3) * 8;
             *reinterpret_cast<uint4*>(dst) = v;
+            const int rep = e.push.dst.rep[code >> kPushRowBits];
+            if (rep > 1) store_repeat(dst, v, rep);
           }
         }
         __syncwarp();  // staging slot free again

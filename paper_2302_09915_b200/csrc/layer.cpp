@@ -17,6 +17,12 @@
 
 namespace tamoe {
 
+LinkEmulation& link_emulation() {
+  static LinkEmulation e;
+  return e;
+}
+
+
 Arena::~Arena() {
   if (base_) cudaFree(base_);
 }
@@ -207,6 +213,7 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
     TAMOE_CUDA(cudaMemset(sig_epoch_, 0, sizeof(unsigned int)));
     // every rank's arena has the same layout: map them all into this process (CUDA IPC over NVLink)
     ep_->map_peers(arena_.base(), bases_);
+    for (int j = 0; j < c.world_size; ++j) link_rep_[j] = link_emulation().factor(c.rank, j);
     sig_.P = c.world_size;
     sig_.me = c.rank;
     sig_.N = c.N;
@@ -281,7 +288,10 @@ PeerBufs Layer::peers(__nv_bfloat16* local) const {
     return pb;
   }
   const long long off = reinterpret_cast<char*>(local) - arena_.base();
-  for (size_t j = 0; j < bases_.size(); ++j) pb.p[j] = reinterpret_cast<__nv_bfloat16*>(bases_[j] + off);
+  for (size_t j = 0; j < bases_.size(); ++j) {
+    pb.p[j] = reinterpret_cast<__nv_bfloat16*>(bases_[j] + off);
+    pb.rep[j] = static_cast<unsigned char>(link_rep_[j]);
+  }
   return pb;
 }
 

@@ -161,6 +161,7 @@ class Layer {
   void ep_barrier(cudaStream_t s, bool publish_counts);
   std::vector<char*> bases_;
   RowMap map_{};
+  int link_rep_[kMaxRanks] = {};  // emulated link throttle per destination rank (LinkEmulation at creation)
   int r_local_ = 0;  // rows of this rank's own padded layout
   int n_pad_ = 0, n64_ = 0, r_max_ = 0, dw_splits_ = 1, P_global_ = 1;
   // activations (expert order, padded segments)

@@ -343,6 +343,7 @@ __global__ void __launch_bounds__(kPermWarps * 32) route_permute_kernel(RouteDim
   const long long drow = map.P == 1 ? r : static_cast<long long>(r) - start[e] + map.dst_off[e];
   uint4* dst = reinterpret_cast<uint4*>(xp.p[dst_rank] + drow * dx);
   const int nv = dx / 8;
+  const int rep = xp.rep[dst_rank];
   if (j < cnt[e]) {
     const int pick = b.clist[b.list_start[e] + j];
     const long long tok = pick / d.k;
@@ -361,11 +362,19 @@ __global__ void __launch_bounds__(kPermWarps * 32) route_permute_kernel(RouteDim
 #pragma unroll
       for (int u = 0; u < kU; ++u)
         if (v0 + 32 * u < nv) dst[v0 + 32 * u] = t[u];
+      if (rep > 1) {
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+          if (v0 + 32 * u < nv) store_repeat(dst + v0 + 32 * u, t[u], rep);
+      }
     }
   } else {
     if (lane == 0 && has_codes) codes.p[dst_rank][drow] = (me << kPushRowBits) | trash_row;
     const uint4 z = make_uint4(0, 0, 0, 0);
-    for (int v = lane; v < nv; v += 32) dst[v] = z;
+    for (int v = lane; v < nv; v += 32) {
+      dst[v] = z;
+      if (rep > 1) store_repeat(dst + v, z, rep);
+    }
     if (has_z) {
       uint4* zd = reinterpret_cast<uint4*>(zrows.p[dst_rank] + drow * zdim);
       for (int v = lane; v < zdim / 8; v += 32) zd[v] = z;

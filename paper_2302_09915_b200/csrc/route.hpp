@@ -32,9 +32,32 @@ struct PeerInts {
 };
 
 // The same buffer in every rank's address space (peer-mapped over NVLink; p[0] only when P == 1).
+// rep[r] > 1: emulated slow link to rank r (set_link_emulation) -- every payload store to r is issued rep[r]
+// times, so that link delivers 1/rep of its bandwidth (the extra copies rewrite identical bytes).
 struct PeerBufs {
   __nv_bfloat16* p[kMaxRanks];
+  unsigned char rep[kMaxRanks];
 };
+
+// Heterogeneous-topology emulation (BASELINE C5): ranks r, j in different groups of `group_size` consecutive
+// ranks talk over a link throttled by `repeat`.  Process-wide; off by default (group_size 0 / repeat <= 1).
+struct LinkEmulation {
+  int group_size = 0, repeat = 1;
+  int factor(int src, int dst) const {
+    return (group_size > 0 && repeat > 1 && src / group_size != dst / group_size) ? repeat : 1;
+  }
+};
+LinkEmulation& link_emulation();
+
+#ifdef __CUDACC__
+// The throttle's extra copies: volatile stores, so none is merged with the payload store it repeats.
+__device__ __forceinline__ void store_repeat(void* p, const uint4& v, int rep) {
+  for (int r = 1; r < rep; ++r)
+    asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+#endif
 constexpr int kRouteTile = 128;  // tokens per routing tile (= GEMM M tile), 4 warps of 32
 
 struct RouteDims {

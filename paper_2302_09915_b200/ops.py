@@ -156,6 +156,12 @@ def p2p_sweep(nccl_id: bytes, world: int, rank: int, sizes_mb=(1.0, 4.0, 16.0, 6
             for s in range(sz.size) for r in range(reps)]
 
 
+def set_link_emulation(group_size: int, repeat: int) -> None:
+    """Emulated heterogeneous topology (BASELINE C5): links between ranks in different groups of `group_size`
+    consecutive ranks carry every payload store `repeat` times (1/repeat of the bandwidth).  (0, 1) = off."""
+    _lib.call("tamoe_set_link_emulation", int(group_size), int(repeat))
+
+
 def solve_target_tree(levels, alpha, beta, N: int, k: int, S: int, self_beta_floor=DEFAULT_SELF_BETA_FLOOR):
     """solve_target for a symmetric tree (solver.cpp:119-150, closed-form branch): smooth, then Eq. 8 on
     beta_hat.  Returns (c_hat [P x N], alpha_hat, beta_hat)."""

@@ -3,13 +3,16 @@
 P2P matrix, plus the alpha-beta model (comm_cost.cpp:24-55) validated against the measured exchange.
 
   python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \\
-      scripts/c3_topology.py [--tokens 16384] [--levels 8] [--cross-throttle 1.0] [--out file.json]
+      scripts/c3_topology.py [--tokens 16384[,32768,...]] [--levels 8] [--cross-throttle 1] [--out file.jsonl]
 
 1. NVLink sweep (`tamoe_p2p_sweep`, every ordered pair incl. self, 1-128 MB x 5 reps) -> TransferSample rows
    -> fit_profile -> fill_partial_profile(tree) -> smooth_profile -> closed form c_hat (Eq. 8).
-   `--levels 2,4 --cross-throttle 4` is the C5 emulation: the cross-group samples are scaled by the
-   throttle before fitting (the transfers themselves are not slowed), so c_hat / predictions see a
-   [2,4] machine with slow cross-group links.
+   `--levels 2,2 --cross-throttle 4` is the C5 emulation: `tamoe_set_link_emulation(group, 4)` really
+   throttles every cross-group link -- each payload store to a peer in another group (the sweep's copies,
+   dispatch, expert-output return, dO, dX return) is issued 4 times, so the link delivers 1/4 of its
+   bandwidth -- and the sweep MEASURES those slow links; c_hat comes from the measured profile.
+   (`--posthoc` instead scales the cross-group samples before fitting and leaves the transfers alone.)
+   `--tokens` takes a comma list (C5 sweeps 4k-64k tokens/GPU); one JSON line per size.
 2. The C2 layer (d=1024, ffn=4096, 64 experts, top-1, GELU, bf16, dX on) with expert parallelism, twice:
    even      : local capacity (cf 1.25), balance loss, no gate bias;
    topo-aware: proportional capacity from c_hat (cf 1.25), topo loss.
@@ -34,7 +37,8 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--tokens", type=int, default=16384)
+    ap.add_argument("--tokens", default="16384")
+    ap.add_argument("--posthoc", action="store_true", help="scale cross-group samples instead of throttling links")
     ap.add_argument("--levels", default=None, help="symmetric tree, e.g. 8 or 2,4 (default: one switch)")
     ap.add_argument("--cross-throttle", type=float, default=1.0)
     ap.add_argument("--steps", type=int, default=10)
@@ -65,18 +69,32 @@ def main():
 
     levels = [int(v) for v in args.levels.split(",")] if args.levels else [world]
     assert int(np.prod(levels)) == world, "levels must multiply to the world size"
-    N, k, S, d, f = 64, 1, args.tokens, 1024, 4096
+    N, k, d, f = 64, 1, 1024, 4096
+    token_list = [int(v) for v in args.tokens.split(",")]
+    group_size = levels[-1]
+    emulate = args.cross_throttle != 1.0 and not args.posthoc
+    if emulate:
+        ops.set_link_emulation(group_size, int(round(args.cross_throttle)))
 
     # ---- 1. measured profile -> c_hat
     sizes = (1.0, 4.0, 16.0, 64.0, 128.0)  # >= L2 at the top: the self link is a real HBM copy
     samples = ops.p2p_sweep(bcast_id(), world, rank, sizes, reps=args.reps, warmup=2)
-    group_size = levels[-1]
-    thr = [(i, j, mb, us * (args.cross_throttle if (i // group_size != j // group_size) else 1.0))
+    post = args.cross_throttle if args.posthoc else 1.0
+    thr = [(i, j, mb, us * (post if (i // group_size != j // group_size) else 1.0))
            for (i, j, mb, us) in samples]
     if rank == 0 and args.samples_csv:
         ops.save_samples_csv(args.samples_csv, thr)
     alpha, beta = ops.fit_profile(thr, world)
     alpha, beta = ops.fill_partial_profile(alpha, beta, levels)
+    for S in token_list:
+        run_size(args, ops, torch, dist, dev, rank, world, levels, emulate, sizes, alpha, beta, bcast_id,
+                 N, k, S, d, f, LayerConfig, TAMoELayer, LOSS_BALANCE, LOSS_TOPO, ACT_GELU)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def run_size(args, ops, torch, dist, dev, rank, world, levels, emulate, sizes, alpha, beta, bcast_id,
+             N, k, S, d, f, LayerConfig, TAMoELayer, LOSS_BALANCE, LOSS_TOPO, ACT_GELU):
     c_topo, a_hat, b_hat = ops.solve_target_tree(levels, alpha, beta, N, k, S)
     c_even = ops.target_closed_form(np.ones((world, world)), N, k, S)
 
@@ -158,6 +176,9 @@ def main():
     if rank == 0:
         out = {"config": {"workload": "C5 emulation" if args.cross_throttle != 1.0 else "C3",
                           "gpus": world, "tokens_per_gpu": S, "levels": levels, "cross_throttle": args.cross_throttle,
+                          "throttle_mode": ("links throttled (every cross-group payload store issued "
+                                            f"{int(round(args.cross_throttle))}x), profile measured on them")
+                          if emulate else ("post-hoc sample scaling" if args.cross_throttle != 1.0 else "none"),
                           "layer": "C2: d=1024 ffn=4096 64 experts top-1 bf16 GELU dX on", "capacity_factor": 1.25},
                "profile": {"sizes_mb": list(sizes), "reps": args.reps,
                            "alpha_us": alpha.tolist(), "beta_us_per_mb": beta.tolist(),
@@ -167,10 +188,9 @@ def main():
         line = json.dumps(out)
         print(line, flush=True)
         if args.out:
-            with open(args.out, "w") as fh:
+            with open(args.out, "a") as fh:
                 fh.write(line + "\n")
     dist.barrier()
-    dist.destroy_process_group()
 
 
 if __name__ == "__main__":

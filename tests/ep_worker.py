@@ -22,6 +22,8 @@ CASES = {
     # global capacity across ranks (gate.cpp:157-164): one cap per expert over every rank's picks
     # (cf 0.5: about half of the picks are dropped, so the cross-rank selection order is exercised)
     "ffn_global": dict(S=512, d=256, dout=256, f=512, k=2, cap=1, kind=0, need_dx=True, cf=0.5),
+    # C5 link-throttle emulation on every cross-rank link (each payload store issued 3x): same results
+    "ffn_prop_throttled": dict(S=512, d=256, dout=256, f=512, k=2, cap=3, kind=1, need_dx=True, throttle=3),
 }
 
 
@@ -45,6 +47,8 @@ def main():
     from paper_2302_09915_b200.layer import LayerConfig, TAMoELayer, nccl_unique_id
 
     S, d, dout, f, k = c["S"], c["d"], c["dout"], c["f"], c["k"]
+    if c.get("throttle"):
+        ops.set_link_emulation(1, c["throttle"])
     N = 8 * world
     E = N // world
     P = world

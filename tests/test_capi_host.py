@@ -126,3 +126,13 @@ def test_aux_losses_and_coefficients_match_oracle():
     with pytest.raises(ops.ValidationError):
         ops.loss_topo(ops.RoutingResult(None, None, None, None, np.zeros(4, np.int64), None, np.zeros(4), []),
                       np.ones(3), 4, 1, 8)
+
+
+def test_link_emulation_validation():
+    from paper_2302_09915_b200 import ops
+    ops.set_link_emulation(2, 4)
+    ops.set_link_emulation(0, 1)  # off again
+    with pytest.raises(ops.ValidationError):
+        ops.set_link_emulation(2, 0)
+    with pytest.raises(ops.ValidationError):
+        ops.set_link_emulation(-1, 2)

@@ -20,7 +20,7 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("case", ["ffn_prop", "linear_none", "ffn_local", "ffn_global"])
+@pytest.mark.parametrize("case", ["ffn_prop", "linear_none", "ffn_local", "ffn_global", "ffn_prop_throttled"])
 def test_ep_parity_multi_gpu(case):
     n = torch.cuda.device_count()
     if n < 2:
