@@ -27,7 +27,7 @@ def re1_beta(P):
     return np.array([[0.1 if i == j else (1.0 if i // 2 == j // 2 else 4.0) for j in range(P)] for i in range(P)])
 
 
-def run_case(P, S, d, dout, N, k, f, cap, kind, need_dx, seed=0, cf=1.25):
+def run_case(P, S, d, dout, N, k, f, cap, kind, need_dx, seed=0, cf=1.25, hot_expert=None):
     from paper_2302_09915_b200 import ops
     from paper_2302_09915_b200.layer import LayerConfig, TAMoELayer
     O = oracle.orc()
@@ -35,6 +35,10 @@ def run_case(P, S, d, dout, N, k, f, cap, kind, need_dx, seed=0, cf=1.25):
     x = bf(rng.normal(size=(P, S, d)))
     y = bf(rng.normal(size=(P, S, dout)) * 0.5)
     gates = bf(rng.normal(size=(P, d, N)) * 0.05)
+    if hot_expert is not None:  # every token's top choice is `hot_expert` (extreme imbalance)
+        x[:, :, 0] = 1.0
+        gates[:, 0, :] = 0.0
+        gates[:, 0, hot_expert] = 8.0
     if f == 0:
         U = bf(rng.normal(size=(N, d, dout)) / np.sqrt(d))
         W1 = W2 = None
@@ -214,3 +218,23 @@ def test_layer_graph_falls_back_when_buffers_change():
         torch.cuda.synchronize()
         assert torch.equal(layer.losses.cpu(), ref)
         assert torch.equal(yh2, yh)
+
+
+@pytest.mark.parametrize("P,S,d,dout,N,k,f,cap,kind,need_dx", [
+    (1, 1, 256, 128, 8, 1, 256, 0, 0, True),       # a single token
+    (3, 48, 256, 128, 12, 2, 0, 3, 1, True),       # tiny multi-process (S % 128 != 0), proportional capacity
+    (1, 300, 256, 128, 256, 8, 256, 2, 1, True),   # the device maxima: N = 256 experts, top-8
+])
+def test_layer_edge_shapes(P, S, d, dout, N, k, f, cap, kind, need_dx):
+    layer, o, extra = run_case(P, S, d, dout, N, k, f, cap, kind, need_dx, seed=3)
+    check(layer, o, extra, P, S, N, k, f, need_dx)
+
+
+@pytest.mark.parametrize("cap,cf", [(0, 1.0), (2, 1.25), (1, 0.05)])
+def test_layer_all_tokens_on_one_expert(cap, cf):
+    """Extreme imbalance: every token's top-1 is expert 5 -- one full expert segment, the rest empty (no
+    capacity), or almost everything dropped (local / tiny global capacity)."""
+    P, S, d, dout, N, k, f = 2, 640, 256, 128, 8, 2, 256
+    layer, o, extra = run_case(P, S, d, dout, N, k, f, cap, 1, True, seed=5, cf=cf, hot_expert=5)
+    assert (o["expert"][:, :, 0] == 5).all()
+    check(layer, o, extra, P, S, N, k, f, True)
