@@ -7,6 +7,7 @@
 //   dX     = dz Wg + sum_slots dX_perm[pos]     (tcgen05 GEMM whose epilogue gathers the expert
 //                                                path's input gradient back to token order)
 // plus the loss finalisation (task MSE, aux loss: trainer.cpp:334-345, 360-361).
+#include <cstdlib>
 #include <cuda_bf16.h>
 
 #include <cmath>
@@ -298,6 +299,84 @@ struct EpiGateDx {
   }
 };
 
+// Tile-ahead variant for top-1 / top-2 (BN = 128; warp h owns the 64 columns [64h, 64h + 64) of its 32
+// tokens).  The expert-path rows and their pos flags of tile i+1 stream into the warp's second staging buffer
+// with cp.async (coalesced: 8 lanes per 128-byte row segment, 128-byte swizzled in shared memory) while tile
+// i is finished; the sum is written back into the staging tile in place and leaves as one 4 KiB TMA store.
+struct GateDxAheadParams {
+  CUtensorMap out;   // dx [T x d], box {64, 32}, 128B swizzle (the staging layout)
+  const __nv_bfloat16* dxp;
+  const int* pos;
+  int S, d;
+};
+
+template <int KT>
+struct EpiGateDxAhead {
+  using Params = GateDxAheadParams;
+  static constexpr int kSlotBytes = 32 * 128;               // 32 tokens x 64 columns bf16
+  static constexpr int kBufBytes = KT * kSlotBytes + 1024;  // + pos flags, 1 KiB aligned for the swizzle
+  static constexpr int kWarpBytes = 2 * kBufBytes;
+  static __device__ __forceinline__ void prefetch(const Params& e, const GemmParams&, const TileInfo& ti, int q, int h,
+                                                  int lane, uint8_t* buf, const int*) {
+    if (lane == 0) ptx::bulk_wait_read<0>();  // the store issued from this buffer two tiles ago has read it
+    __syncwarp();
+    const int tok0 = ti.m0 + q * 32;
+    const long long g0 = static_cast<long long>(ti.g) * e.S + tok0;
+    const int col0 = ti.n0 + 64 * h;
+#pragma unroll
+    for (int i = 0; i < 8 * KT; ++i) {
+      const int id = i * 32 + lane;
+      const int j = id >> 8, rr = (id >> 3) & 31, c = id & 7;
+      const bool ok = tok0 + rr < e.S;
+      const __nv_bfloat16* src = e.dxp + ((ok ? g0 + rr : 0) * KT + j) * e.d + col0 + 8 * c;
+      ptx::cp_async_16(buf + j * kSlotBytes + rr * 128 + ((c ^ (rr & 7)) * 16), src, ok);
+    }
+    const bool ok = tok0 + lane < e.S;
+    ptx::cp_async_small<4 * KT>(buf + KT * kSlotBytes + lane * 4 * KT, e.pos + (ok ? g0 + lane : 0) * KT, ok);
+    ptx::cp_async_commit();
+  }
+  static __device__ __forceinline__ void prefetch_none() { ptx::cp_async_commit(); }
+  static __device__ __forceinline__ void finish(const Params&, int lane) {
+    ptx::cp_async_wait<0>();
+    if (lane == 0) ptx::bulk_wait<0>();
+    __syncwarp();
+  }
+  static __device__ __forceinline__ void run(const Params& e, const GemmParams&, const TileInfo& ti,
+                                             uint32_t tmem_tile, int q, int h, int lane, uint8_t* buf, const int*) {
+    ptx::cp_async_wait<1>();  // this tile's group (the next tile's may still be in flight)
+    __syncwarp();
+    const int* posf = reinterpret_cast<const int*>(buf + KT * kSlotBytes) + lane * KT;
+    bool keep[KT];
+#pragma unroll
+    for (int j = 0; j < KT; ++j) keep[j] = posf[j] >= 0;  // dropped picks: their dxp rows are stale
+    uint8_t* row = buf + lane * 128;
+    const int sw = lane & 7;
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      float v[32];
+      load_acc32(tmem_tile, 64 * h + 32 * cc, v);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int off = ((cc * 4 + u) ^ sw) * 16;
+#pragma unroll
+        for (int j = 0; j < KT; ++j)
+          if (keep[j]) EpiGateDx<KT>::add8(v + 8 * u, *reinterpret_cast<const uint4*>(row + j * kSlotBytes + off));
+        uint4 w;
+        __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&w);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) hh[i] = __floats2bfloat162_rn(v[8 * u + 2 * i], v[8 * u + 2 * i + 1]);
+        *reinterpret_cast<uint4*>(row + off) = w;  // in place: slot 0 becomes the output staging tile
+      }
+    }
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      ptx::tma_store_2d(&e.out, buf, ti.n0 + 64 * h, static_cast<int>(static_cast<long long>(ti.g) * e.S + ti.m0 + q * 32));
+      ptx::bulk_commit();
+    }
+  }
+};
+
 }  // namespace
 
 void gate_dz(const GateDzArgs& a, cudaStream_t s) {
@@ -356,6 +435,18 @@ void gate_dx(const __nv_bfloat16* dz, const __nv_bfloat16* wg, int P, int S, int
   CUtensorMap ta = make_tmap_bf16(dz, n64, T, n64, 128);                         // A = dz (K-major)
   CUtensorMap tb = make_tmap_bf16(wg, d, static_cast<uint64_t>(P) * n_pad, d, 64);  // B = Wg (MN-major)
   GemmParams p{1, nullptr, nullptr, 0, d, n_pad, 1, S, n_pad, P, 0, 1, 0, 0};
+  // tile-ahead TMA path: top-1 / top-2, local expert-path rows, and 32-token warp groups that never straddle
+  // two processes (the TMA store writes whole 32-row boxes; rows past T are clipped)
+  static const bool ahead_on = [] {
+    const char* v = std::getenv("TAMOE_GATE_DX_AHEAD");
+    return !(v && v[0] == '0');
+  }();
+  if (ahead_on && (k == 1 || k == 2) && map.P == 1 && (P == 1 || S % 32 == 0)) {
+    GateDxAheadParams ea{make_tmap_bf16_box(dx, d, T, d, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B), dxp.p[0], pos, S, d};
+    if (k == 1) launch_gemm<kModeGateDx, 128, false, true, EpiGateDxAhead<1>>(ta, tb, p, ea, 0, s);
+    else launch_gemm<kModeGateDx, 128, false, true, EpiGateDxAhead<2>>(ta, tb, p, ea, 0, s);
+    return;
+  }
   GateDxParams ep{dx, dxp, pos, idx, map, k, S, d};
   if (k == 1) launch_gemm<kModeGateDx, 256, false, true, EpiGateDx<1>>(ta, tb, p, ep, 0, s);
   else if (k == 2) launch_gemm<kModeGateDx, 256, false, true, EpiGateDx<2>>(ta, tb, p, ep, 0, s);

@@ -73,6 +73,18 @@ struct EpiEarly<Epi, decltype(void(Epi::kEarlyRelease))> {
   static constexpr bool value = Epi::kEarlyRelease;
 };
 
+// Epilogues that declare `static constexpr int kBufBytes` get two staging buffers per warp and are driven one
+// tile ahead: Epi::prefetch(..., buffer) for tile i+1 is issued before the accumulator wait of tile i, so its
+// loads are in flight during that tile's epilogue (Epi::prefetch_none() keeps async-group counts uniform).
+template <class Epi, class = void>
+struct EpiAhead {
+  static constexpr bool value = false;
+};
+template <class Epi>
+struct EpiAhead<Epi, decltype(void(Epi::kBufBytes))> {
+  static constexpr bool value = true;
+};
+
 template <class Epi, class = void>
 struct EpiSmem {
   static constexpr int warp = 0;
@@ -460,6 +472,38 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int q = warp & 3, h = warp >> 2;
     uint8_t* wsm = smem + L::kEpiOffset + warp * EpiSmem<Epi>::warp;
     int it = 0;
+    if constexpr (EpiAhead<Epi>::value) {
+      static_assert(!EpiEarly<Epi>::value, "tile-ahead epilogues release TMEM after run()");
+      TileInfo nx;
+      if (cluster_id < total_tiles) {
+        decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, cluster_id, nx);
+        nx.m0 += static_cast<int>(rank) * kBM;
+        Epi::prefetch(ep, p, nx, q, h, lane, wsm, s_start);
+      }
+      for (int t = cluster_id; t < total_tiles; t += num_clusters, ++it) {
+        const TileInfo ti = nx;
+        const int tn = t + num_clusters;
+        if (tn < total_tiles) {
+          decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, tn, nx);
+          nx.m0 += static_cast<int>(rank) * kBM;
+          Epi::prefetch(ep, p, nx, q, h, lane, wsm + ((it + 1) & 1) * Epi::kBufBytes, s_start);
+        } else {
+          Epi::prefetch_none();
+        }
+        const int buf = it & 1;
+        const uint32_t use = static_cast<uint32_t>(it >> 1);
+        ptx::mbar_wait(&tfull_bar[buf], use & 1);
+        ptx::tc_fence_after();
+        const uint32_t tmem_tile = tmem_base + buf * BN + (static_cast<uint32_t>(q * 32) << 16);
+        Epi::run(ep, p, ti, tmem_tile, q, h, lane, wsm + (it & 1) * Epi::kBufBytes, s_start);
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (kCG == 2) ptx::mbar_arrive_remote(ptx::mapa(&tempty_bar[buf], 0));
+          else ptx::mbar_arrive(&tempty_bar[buf]);
+        }
+      }
+    } else
     for (int t = cluster_id; t < total_tiles; t += num_clusters, ++it) {
       TileInfo ti;
       decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, t, ti);

@@ -213,6 +213,13 @@ __device__ __forceinline__ void cp_async_16(void* smem_dst, const void* gsrc, bo
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)), "l"(gsrc), "r"(sz)
                : "memory");
 }
+template <int kBytes>  // 4 or 8 bytes (.ca); src-size 0 zero-fills
+__device__ __forceinline__ void cp_async_small(void* smem_dst, const void* gsrc, bool pred) {
+  const uint32_t sz = pred ? static_cast<uint32_t>(kBytes) : 0u;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(smem_u32(smem_dst)), "l"(gsrc), "n"(kBytes),
+               "r"(sz)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
