@@ -65,6 +65,16 @@ __global__ void __launch_bounds__(kDzWarps * 32) gate_dz_kernel(const __grid_con
   if (t >= static_cast<long long>(a.P) * a.S) return;
   const int proc = static_cast<int>(t / a.S);
   const int k = KT > 0 ? KT : a.k;
+  // every per-token load up front (independent of the softmax below), so their latencies overlap
+  int ex_in[KM];
+  float dl_in[KM];
+  double sc_in[KM];
+#pragma unroll
+  for (int j = 0; j < KM; ++j) {
+    ex_in[j] = j < k ? a.idx[t * k + j] : -1;
+    dl_in[j] = j < k ? a.dldg[t * k + j] : 0.f;
+    sc_in[j] = (k > 1 && j < k) ? a.score[t * k + j] : 0.0;
+  }
   // softmax of the stored fp32 logits (fp32 math, max-subtracted)
   float l[NPL], p[NPL], dpi[NPL];
   float mx = -INFINITY;
@@ -96,8 +106,8 @@ __global__ void __launch_bounds__(kDzWarps * 32) gate_dz_kernel(const __grid_con
   int ex[KM];
   float add[KM];
   if (k == 1) {
-    ex[0] = a.idx[t];
-    add[0] = a.dldg[t];
+    ex[0] = ex_in[0];
+    add[0] = dl_in[0];
 #pragma unroll
     for (int j = 1; j < KM; ++j) {
       ex[j] = -1;
@@ -108,9 +118,9 @@ __global__ void __launch_bounds__(kDzWarps * 32) gate_dz_kernel(const __grid_con
     double mass = 0.0;
 #pragma unroll
     for (int j = 0; j < KM; ++j) {
-      ex[j] = j < k ? a.idx[t * k + j] : -1;
-      sc[j] = j < k ? a.score[t * k + j] : 0.0;
-      dg[j] = j < k ? static_cast<double>(a.dldg[t * k + j]) : 0.0;
+      ex[j] = ex_in[j];
+      sc[j] = sc_in[j];
+      dg[j] = static_cast<double>(dl_in[j]);
       mass += sc[j];
     }
     const double inv2 = 1.0 / (mass * mass);
@@ -191,8 +201,20 @@ __global__ void dwg_reduce_kernel(const float* __restrict__ part, int splits, in
     const int n = static_cast<int>((i / d) % n_pad);
     const int proc = static_cast<int>(i / (static_cast<long long>(d) * n_pad));
     float s = 0.f;
-    if (n < N)
-      for (int ks = 0; ks < splits; ++ks) s += part[((static_cast<long long>(ks) * P + proc) * n64 + n) * d + m];
+    if (n < N) {
+      // eight partials in flight per thread, summed in split order (deterministic)
+      const long long stride = static_cast<long long>(P) * n64 * d;
+      const float* src = part + (static_cast<long long>(proc) * n64 + n) * d + m;
+      int ks = 0;
+      for (; ks + 8 <= splits; ks += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldg(src + (ks + u) * stride);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += v[u];
+      }
+      for (; ks < splits; ++ks) s += __ldg(src + ks * stride);
+    }
     dwg[i] = s;
   }
 }
