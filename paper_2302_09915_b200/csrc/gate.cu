@@ -64,21 +64,24 @@ struct EpiLogits {
 // Per-token routing over fp32 logits: fp64 softmax exactly as the reference (max-subtract, exp, sequential
 // sum in expert order, divide: gate.cpp:12-28), top-k in (probability desc, expert asc) order
 // (gate.cpp:117-134), per-32-token-group expert histograms and probability sums (gate.cpp:115).
-// A block of 4 warps owns one 32-token group (= one hist4/msum4 slot); each warp takes 8 tokens with its
+// A block of 16 warps owns one 32-token group (= one hist4/msum4 slot); each warp takes 2 tokens with its
 // lanes across experts (expert c on lane c % 32), so every exp is computed once and parked in shared
-// memory for the sequential denominator, and top-k is a warp arg-max.
-constexpr int kRouteRowsPerWarp = 8;
+// memory for the sequential denominator, and top-k is a warp arg-max.  (2 tokens per warp: the per-warp
+// chain of dependent loads, shuffles and the serial fp64 denominator is the kernel's critical path.)
+constexpr int kRouteRowsPerWarp = 2;
+constexpr int kRouteGroupWarps = 32 / kRouteRowsPerWarp;
 
 template <int EPL, int KM>
-__global__ void __launch_bounds__(128) route_logits_kernel(const float* __restrict__ logits, RouteDims d,
+__global__ void __launch_bounds__(kRouteGroupWarps * 32) route_logits_kernel(const float* __restrict__ logits, RouteDims d,
                                                            RowRouteOut o) {
   constexpr int NC = EPL * 32;
   constexpr int RPW = kRouteRowsPerWarp;
   extern __shared__ double route_smem[];
-  auto E = reinterpret_cast<double (*)[RPW][NC + 1]>(route_smem);  // [4][RPW][NC+1] exps
-  __shared__ double den[4][RPW];
+  constexpr int WPG = kRouteGroupWarps;
+  auto E = reinterpret_cast<double (*)[RPW][NC + 1]>(route_smem);  // [WPG][RPW][NC+1] exps
+  __shared__ double den[WPG][RPW];
   auto ms = reinterpret_cast<double (*)[NC]>(route_smem);            // reuses E after the block barrier
-  auto hs = reinterpret_cast<int (*)[NC]>(route_smem + 4 * NC);
+  auto hs = reinterpret_cast<int (*)[NC]>(route_smem + WPG * NC);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x;  // 32-token group == hist4 / msum4 slot
   const int groups = d.TB * 4;
@@ -186,7 +189,9 @@ __global__ void __launch_bounds__(128) route_logits_kernel(const float* __restri
           const long long a = gtok * k + t;
           o.idx[a] = pe[t];
           o.score[a] = pp[t];
-          o.gate[a] = static_cast<float>(k == 1 ? pp[t] : pp[t] / mass);
+          const double g = k == 1 ? pp[t] : pp[t] / mass;
+          o.gate[a] = static_cast<float>(g);
+          if (o.gate64) o.gate64[a] = g;
         }
       }
     }
@@ -200,15 +205,22 @@ __global__ void __launch_bounds__(128) route_logits_kernel(const float* __restri
   }
   __syncthreads();
   for (int c = threadIdx.x; c < N; c += blockDim.x) {
-    o.hist4[static_cast<long long>(b) * N + c] = hs[0][c] + hs[1][c] + hs[2][c] + hs[3][c];
-    o.msum4[static_cast<long long>(b) * N + c] = ((ms[0][c] + ms[1][c]) + ms[2][c]) + ms[3][c];
+    int hsum = 0;
+    double msum_c = 0.0;
+#pragma unroll
+    for (int w = 0; w < WPG; ++w) {  // fixed order: deterministic
+      hsum += hs[w][c];
+      msum_c += ms[w][c];
+    }
+    o.hist4[static_cast<long long>(b) * N + c] = hsum;
+    o.msum4[static_cast<long long>(b) * N + c] = msum_c;
   }
 }
 
 template <int EPL, int KM>
 static void route_logits_launch_k(const float* logits, const RouteDims& d, const RowRouteOut& o, cudaStream_t s) {
-  constexpr int smem = 4 * kRouteRowsPerWarp * (EPL * 32 + 1) * 8;
-  static_assert(smem >= 4 * EPL * 32 * 12, "E must cover the reduction scratch");
+  constexpr int smem = kRouteGroupWarps * kRouteRowsPerWarp * (EPL * 32 + 1) * 8;
+  static_assert(smem >= kRouteGroupWarps * EPL * 32 * 12, "E must cover the reduction scratch");
   static unsigned long long attr_set = 0;  // per device
   int dev = 0;
   TAMOE_CUDA(cudaGetDevice(&dev));
@@ -216,7 +228,7 @@ static void route_logits_launch_k(const float* logits, const RouteDims& d, const
     TAMOE_CUDA(cudaFuncSetAttribute(route_logits_kernel<EPL, KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set |= 1ull << dev;
   }
-  route_logits_kernel<EPL, KM><<<static_cast<unsigned>(d.tiles()) * 4, 128, smem, s>>>(logits, d, o);
+  route_logits_kernel<EPL, KM><<<static_cast<unsigned>(d.tiles()) * 4, kRouteGroupWarps * 32, smem, s>>>(logits, d, o);
   TAMOE_CUDA(cudaGetLastError());
 }
 
