@@ -58,6 +58,29 @@ def peaks():
     return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, source="fallback")
 
 
+def bind_to_gpu_numa(cuda_index):
+    """Pin this process to the CPUs NVML reports as local to the GPU, so the pinned host buffers of the e2e leg
+    are first-touched on the GPU's NUMA node (with 4-8 ranks on one host, remote-node buffers halve H2D).
+    Returns the CPU count bound to, or None when NVML / the affinity call is unavailable."""
+    try:
+        import pynvml as nv
+        import torch
+        nv.nvmlInit()
+        pr = torch.cuda.get_device_properties(cuda_index)
+        h = nv.nvmlDeviceGetHandleByPciBusId(
+            f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0")
+        ncpu = os.cpu_count() or 1
+        words = nv.nvmlDeviceGetCpuAffinity(h, (ncpu + 63) // 64)
+        cpus = {w * 64 + b for w, m in enumerate(words) for b in range(64) if (int(m) >> b) & 1}
+        cpus &= set(os.sched_getaffinity(0))
+        if not cpus:
+            return None
+        os.sched_setaffinity(0, cpus)
+        return len(cpus)
+    except Exception:
+        return None
+
+
 # ------------------------------------------------------------------------------------------ clocks
 class ClockSampler:
     """SM clock + clock-event (throttle) reasons sampled DURING the timed region through NVML every ~1 ms
@@ -227,6 +250,8 @@ def main():
 
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        # stdout carries exactly one JSON line: NCCL's own log lines (e.g. NCCL_DEBUG=VERSION) go to stderr
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if args.impl == "reference":
@@ -326,6 +351,9 @@ def main():
     # ---------------- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
+        # N > 1: every rank's host buffers on its GPU's NUMA node (the N=1 line keeps all host cores for the
+        # CPU-baseline leg, which runs on rank 0 at N=1 only)
+        numa_cpus = bind_to_gpu_numa(local) if world > 1 else None
         xh = x.cpu().pin_memory()
         yh = y.cpu().pin_memory()
         lh = torch.zeros(2, dtype=torch.float64).pin_memory()
@@ -370,7 +398,8 @@ def main():
         e2e = {"value": world * S / (ems / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": int(x.numel() * 2 + y.numel() * 2), "d2h_bytes_per_step": 16,
                "ms_per_step": ems, "note": "pinned host x,y copied H2D every step on a copy stream "
-                                           "(double-buffered), losses read back D2H every step"}
+                                           "(double-buffered), losses read back D2H every step",
+               "host_numa_cpus": numa_cpus}
 
     # ---------------- roofline of the dominant kernel family (expert grouped GEMMs, tcgen05)
     # Per launch: FLOPs 2*R*d*f and ALGORITHMIC bytes = this GPU's expert weights (E = N/world experts, read for

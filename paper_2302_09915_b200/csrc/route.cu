@@ -330,8 +330,12 @@ __global__ void __launch_bounds__(kPermWarps * 32) route_permute_kernel(RouteDim
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rows = min(total, r_max);
+  // Under expert parallelism the rows are owner-major; every rank starts at its own owner segment and walks
+  // the owners cyclically, so at any moment the P senders target P different receivers (no incast on rank 0).
+  const int rot = (map.P > 1 && me * map.E < N && rows > 0) ? min(start[me * map.E], rows) % rows : 0;
   // warps stride over the rows (the block's expert scan above is amortised over many rows)
-  for (int r = blockIdx.x * kPermWarps + warp; r < rows; r += gridDim.x * kPermWarps) {
+  for (int rl = blockIdx.x * kPermWarps + warp; rl < rows; rl += gridDim.x * kPermWarps) {
+  const int r = rl + rot < rows ? rl + rot : rl + rot - rows;
   int lo = 0, hi = N - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;

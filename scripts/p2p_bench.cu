@@ -36,11 +36,12 @@ __global__ void copy_kernel(const uint4* __restrict__ src, uint4* __restrict__ d
 }
 
 // all-to-all: GPU g writes chunk j of its source (n/P vectors) into GPU j's destination at slot g
-__global__ void a2a_kernel(const uint4* __restrict__ src, uint4** dsts, int P, int me, long long chunk) {
+// stagger = 1: GPU g starts at chunk g and walks the peers cyclically (no incast on one receiver)
+__global__ void a2a_kernel(const uint4* __restrict__ src, uint4** dsts, int P, int me, long long chunk, int stagger) {
   const long long total = chunk * P;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
-    const int j = static_cast<int>(i / chunk);
+    const int j = static_cast<int>((i / chunk + (stagger ? me : 0)) % P);
     const long long o = i % chunk;
     dsts[j][me * chunk + o] = src[i];
   }
@@ -83,9 +84,9 @@ __global__ void __launch_bounds__(256) rows_a2a_kernel(const uint4* __restrict__
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long total = rows_per_peer * P;
   for (long long r = static_cast<long long>(blockIdx.x) * 8 + warp; r < total; r += static_cast<long long>(gridDim.x) * 8) {
-    const int j = static_cast<int>(r / rows_per_peer);
+    const int j = static_cast<int>((r / rows_per_peer + me) % P);  // staggered
     const long long o = r % rows_per_peer;
-    const uint4* s = src + r * 128;
+    const uint4* s = src + (j * rows_per_peer + o) * 128;
     uint4* d = dsts[j] + (me * rows_per_peer + o) * 128;
     uint4 v[4];
 #pragma unroll
@@ -108,6 +109,24 @@ __global__ void __launch_bounds__(256) rows_a2a_kernel(const uint4* __restrict__
     }
   }
   if (MODE == 1 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// Row all-to-all as pulls: GPU `me` reads rows [me*rpp, (me+1)*rpp) of every GPU's source into its slot j.
+__global__ void __launch_bounds__(256) rows_pull_kernel(uint4** srcs, uint4* __restrict__ dst, int P, int me,
+                                                        long long rows_per_peer) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long total = rows_per_peer * P;
+  for (long long r = static_cast<long long>(blockIdx.x) * 8 + warp; r < total; r += static_cast<long long>(gridDim.x) * 8) {
+    const int j = static_cast<int>((r / rows_per_peer + me) % P);
+    const long long o = r % rows_per_peer;
+    const uint4* s = srcs[j] + (me * rows_per_peer + o) * 128;
+    uint4* d = dst + (j * rows_per_peer + o) * 128;
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = s[lane + 32 * u];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) d[lane + 32 * u] = v[u];
+  }
 }
 
 static float time_ms(cudaStream_t s, cudaEvent_t a, cudaEvent_t b) {
@@ -165,8 +184,9 @@ int main() {
         printf("SM %-4s grid %5d block %5d : %7.1f GB/s\n", dir == 0 ? "push" : "pull", gi, bi, bytes / best / 1e6);
       }
   }
-  // 3) all-to-all over all GPUs, SM stores, every GPU concurrently
-  for (int gi : grids) {
+  // 3) all-to-all over all GPUs, SM stores, every GPU concurrently (plain order, then staggered)
+  for (int stagger = 0; stagger < 2; ++stagger)
+  for (int gi : {148, 296, 592, 1184, 2368}) {
     std::vector<uint4**> dptr(ng);
     for (int g = 0; g < ng; ++g) {
       CK(cudaSetDevice(g));
@@ -186,7 +206,7 @@ int main() {
         CK(cudaEventCreate(&ea[g]));
         CK(cudaEventCreate(&eb[g]));
         CK(cudaEventRecord(ea[g], st[g]));
-        a2a_kernel<<<gi, 512, 0, st[g]>>>(buf[g], dptr[g], ng, g, chunk);
+        a2a_kernel<<<gi, 512, 0, st[g]>>>(buf[g], dptr[g], ng, g, chunk, stagger);
         CK(cudaEventRecord(eb[g], st[g]));
       }
       float mx = 0;
@@ -197,7 +217,8 @@ int main() {
       if (it) worst = mx;
     }
     const double off = bytes * (ng - 1.0) / ng;
-    printf("a2a %d GPUs grid %5d: %7.1f GB/s off-rank per GPU (%.1f us for %zu MiB/GPU)\n", ng, gi,
+    printf("a2a %d GPUs %s grid %5d: %7.1f GB/s off-rank per GPU (%.1f us for %zu MiB/GPU)\n", ng,
+           stagger ? "staggered" : "in order ", gi,
            off / worst / 1e6, worst * 1e3, bytes >> 20);
   }
   // 3b) row all-to-all: SM stores vs TMA bulk stores
@@ -210,7 +231,7 @@ int main() {
     }
     const long long rows_per_peer = (bytes / 2048) / ng;
     for (int mode = 0; mode < 2; ++mode)
-      for (int gi : {296, 592, 1184}) {
+      for (int gi : {296, 592, 1184, 2368}) {
         float worst = 0;
         for (int it = 0; it < 3; ++it) {
           for (int g = 0; g < ng; ++g) {
@@ -237,6 +258,85 @@ int main() {
         const double off = bytes * (ng - 1.0) / ng;
         printf("rows a2a %s grid %5d: %7.1f GB/s off-rank per GPU\n", mode ? "TMA bulk" : "SM st  ", gi, off / worst / 1e6);
       }
+  }
+  // 3c) row all-to-all as pulls (every GPU reads its 1/P slot from every peer) and larger grids
+  {
+    std::vector<uint4**> sptr(ng);
+    for (int g = 0; g < ng; ++g) {
+      CK(cudaSetDevice(g));
+      CK(cudaMalloc(&sptr[g], sizeof(uint4*) * ng));
+      CK(cudaMemcpy(sptr[g], buf.data(), sizeof(uint4*) * ng, cudaMemcpyHostToDevice));
+    }
+    const long long rows_per_peer = (bytes / 2048) / ng;
+    for (int gi : {592, 1184, 2368, 4736}) {
+      float worst = 0;
+      for (int it = 0; it < 3; ++it) {
+        for (int g = 0; g < ng; ++g) {
+          CK(cudaSetDevice(g));
+          CK(cudaDeviceSynchronize());
+        }
+        std::vector<cudaEvent_t> ea(ng), eb(ng);
+        for (int g = 0; g < ng; ++g) {
+          CK(cudaSetDevice(g));
+          CK(cudaEventCreate(&ea[g]));
+          CK(cudaEventCreate(&eb[g]));
+          CK(cudaEventRecord(ea[g], st[g]));
+          rows_pull_kernel<<<gi, 256, 0, st[g]>>>(sptr[g], buf2[g], ng, g, rows_per_peer);
+          CK(cudaEventRecord(eb[g], st[g]));
+        }
+        float mx = 0;
+        for (int g = 0; g < ng; ++g) {
+          CK(cudaSetDevice(g));
+          mx = std::max(mx, time_ms(st[g], ea[g], eb[g]));
+        }
+        if (it) worst = mx;
+      }
+      const double off = bytes * (ng - 1.0) / ng;
+      printf("rows a2a pull     grid %5d: %7.1f GB/s off-rank per GPU\n", gi, off / worst / 1e6);
+    }
+  }
+  // 3d) all-to-all on the copy engines: every GPU issues P-1 peer copies on P-1 streams at once
+  {
+    std::vector<std::vector<cudaStream_t>> cs(ng, std::vector<cudaStream_t>(ng));
+    for (int g = 0; g < ng; ++g) {
+      CK(cudaSetDevice(g));
+      for (int j = 0; j < ng; ++j) CK(cudaStreamCreateWithFlags(&cs[g][j], cudaStreamNonBlocking));
+    }
+    const size_t chunk = bytes / ng;
+    float worst = 0;
+    for (int it = 0; it < 4; ++it) {
+      for (int g = 0; g < ng; ++g) {
+        CK(cudaSetDevice(g));
+        CK(cudaDeviceSynchronize());
+      }
+      std::vector<cudaEvent_t> ea(ng), eb(ng);
+      for (int g = 0; g < ng; ++g) {
+        CK(cudaSetDevice(g));
+        CK(cudaEventCreate(&ea[g]));
+        CK(cudaEventCreate(&eb[g]));
+        CK(cudaEventRecord(ea[g], st[g]));
+        for (int j = 0; j < ng; ++j) {
+          if (j == g) continue;
+          CK(cudaStreamWaitEvent(cs[g][j], ea[g], 0));
+          CK(cudaMemcpyPeerAsync(reinterpret_cast<char*>(buf2[j]) + g * chunk, j,
+                                 reinterpret_cast<char*>(buf[g]) + j * chunk, g, chunk, cs[g][j]));
+          cudaEvent_t ej;
+          CK(cudaEventCreateWithFlags(&ej, cudaEventDisableTiming));
+          CK(cudaEventRecord(ej, cs[g][j]));
+          CK(cudaStreamWaitEvent(st[g], ej, 0));
+        }
+        CK(cudaEventRecord(eb[g], st[g]));
+      }
+      float mx = 0;
+      for (int g = 0; g < ng; ++g) {
+        CK(cudaSetDevice(g));
+        mx = std::max(mx, time_ms(st[g], ea[g], eb[g]));
+      }
+      if (it) worst = mx;
+    }
+    const double off = bytes * (ng - 1.0) / ng;
+    printf("a2a copy engines  (%d streams/GPU): %7.1f GB/s off-rank per GPU (%.1f us)\n", ng - 1, off / worst / 1e6,
+           worst * 1e3);
   }
   // 4) segmented all-to-all (push / pull), 64 B .. 2 KB segments
   {
