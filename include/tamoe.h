@@ -170,6 +170,21 @@ int tamoe_gate_forward_f64(const double* x, const double* w, int S, int d, int N
 int tamoe_grad_aux_loss_f64(const double* x, const double* probs, const double* coeff, int S, int d, int N,
                             double* grad, void* stream);
 
+/* One reference-precision MoE layer step: BASELINE config 1 (fp64, linear experts) on the device.  Replaces the
+ * inline step of train() (trainer.cpp:246-356): fp64 gate_forward per process -> topk_route on router r
+ * (created with P, S, N, k) -> expert x U_e -> combine -> MSE -> backward (dL/dg, top-k Jacobian, aux
+ * coefficients, softmax backward, x^T dz).  Sums run in the reference's order without FMA, so gradients are
+ * bit-identical to the reference's whenever the softmax is.  Device fp64, row-major: x [P*S x d],
+ * y [P*S x d_out], gates [P x d x N], experts [N x d x d_out]; outputs gate_grads [P x d x N],
+ * expert_grads [N x d x d_out], optional probs [P*S x N] and y_hat [P*S x d_out].  Host: penalty [P x N]
+ * (topo loss; NULL for balance), caps [P x N] (tamoe_capacity_caps), losses [2] = task, aux (TrainReport).
+ * Routing arrays stay readable through tamoe_router_read.  Status 2 on a non-finite logit or an aux kind
+ * other than balance / topo; status 1 when the step diverges (trainer.cpp:362-366). */
+int tamoe_layer_step_f64(tamoe_router* r, int d, int d_out, const double* x, const double* y, const double* gates,
+                         const double* experts, const double* penalty, int aux_kind, double aux_weight, int cap_mode,
+                         const long long* caps, double* probs, double* gate_grads, double* expert_grads,
+                         double* y_hat, double* losses, void* stream);
+
 /* Auxiliary losses on a routing result (host, N-vectors; counts int64 = RoutingResult::counts). */
 /* loss_balance (gate.cpp:209-214) */
 int tamoe_loss_balance(const long long* counts, const double* mean_probs, int N, int S, double* loss);

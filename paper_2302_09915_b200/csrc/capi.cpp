@@ -14,6 +14,7 @@
 #include "expert.hpp"
 #include "gate.hpp"
 #include "gate_f64.hpp"
+#include "layer_f64.hpp"
 #include "host_topology.hpp"
 #include "layer.hpp"
 #include "route.hpp"
@@ -308,6 +309,33 @@ int tamoe_grad_aux_loss_f64(const double* x, const double* probs, const double* 
     aux_dz_f64(probs, c.p, dz.p, S, N, s);
     add_atb_f64(grad, x, dz.p, S, d, N, s);
     TAMOE_CUDA(cudaStreamSynchronize(s));  // coeff is the caller's host memory
+  });
+}
+
+int tamoe_layer_step_f64(tamoe_router* r, int d, int d_out, const double* x, const double* y, const double* gates,
+                         const double* experts, const double* penalty, int aux_kind, double aux_weight, int cap_mode,
+                         const long long* caps, double* probs, double* gate_grads, double* expert_grads,
+                         double* y_hat, double* losses, void* stream) {
+  return guarded([&] {
+    require(r != nullptr, "layer_step_f64: null router");
+    F64StepArgs a;
+    a.d = d;
+    a.d_out = d_out;
+    a.x = x;
+    a.y = y;
+    a.gates = gates;
+    a.experts = experts;
+    a.penalty = penalty;
+    a.aux_kind = aux_kind;
+    a.aux_weight = aux_weight;
+    a.cap_mode = cap_mode;
+    a.caps = caps;
+    a.probs = probs;
+    a.gate_grads = gate_grads;
+    a.expert_grads = expert_grads;
+    a.y_hat = y_hat;
+    a.losses = losses;
+    layer_step_f64(r->impl.rw, a, static_cast<cudaStream_t>(stream));
   });
 }
 

@@ -443,3 +443,66 @@ def grad_loss_balance(x, probs, result: RoutingResult, S: int) -> torch.Tensor: 
 
 def grad_loss_topo(x, probs, result: RoutingResult, penalty, N: int, P: int, S: int) -> torch.Tensor:  # :293-296
     return grad_aux_loss(x, probs, topo_coefficients(result, penalty, N, P, S))
+
+
+# ----------------------------------------------------------------------------- reference-precision layer step
+_lib.lib.tamoe_layer_step_f64.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int] + [ctypes.c_void_p] * 4 + \
+    [_D, ctypes.c_int, ctypes.c_double, ctypes.c_int, _L] + [ctypes.c_void_p] * 4 + [_D, ctypes.c_void_p]
+_lib.lib.tamoe_layer_step_f64.restype = ctypes.c_int
+
+
+def layer_step_f64(x, y, gates, experts, k: int, policy: CapacityPolicy = CapacityPolicy(), c_hat=None,
+                   aux_kind: int = 0, aux_weight: float = 1.0, penalties=None, router: Router = None):
+    """One step of the reference's MoE layer in its own precision (BASELINE config 1: fp64, linear experts) on
+    the device -- the inline step of train() (trainer.cpp:246-356).  x [P, S, d], y [P, S, d_out],
+    gates [P, d, N] (GateState::W), experts [N, d, d_out] (U_e); numpy or torch (moved to the GPU as fp64).
+    aux_kind 0 balance / 1 topo (penalties [P, N] = penalty_weights of each c_hat row).  Returns a dict with
+    task_loss / aux_loss (TrainReport), gate_grads [P, d, N], expert_grads [N, d, d_out], probs [P, S, N],
+    y_hat [P, S, d_out] (device fp64 tensors) and the router (routing arrays via Router.read)."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    def dt(a):
+        t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.asarray(a))
+        return t.to(device=dev, dtype=torch.float64).contiguous()
+
+    x, y, gates, experts = dt(x), dt(y), dt(gates), dt(experts)
+    P, S, d = x.shape
+    d_out = y.shape[2]
+    N = gates.shape[2]
+    if router is None or (router.P, router.S, router.N, router.k) != (P, S, N, k):
+        router = Router(P, S, N, k)
+    caps = capacity_caps(policy, k, S, N, P, c_hat)
+    pen = _f64(penalties) if penalties is not None else None
+    probs = torch.empty(P, S, N, dtype=torch.float64, device=dev)
+    gg = torch.empty(P, d, N, dtype=torch.float64, device=dev)
+    eg = torch.empty(N, d, d_out, dtype=torch.float64, device=dev)
+    yh = torch.empty(P, S, d_out, dtype=torch.float64, device=dev)
+    losses = np.zeros(2)
+    _lib.call("tamoe_layer_step_f64", router._h, d, d_out, ctypes.c_void_p(x.data_ptr()),
+              ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(gates.data_ptr()), ctypes.c_void_p(experts.data_ptr()),
+              pen.ctypes.data_as(_D) if pen is not None else None, int(aux_kind), float(aux_weight),
+              int(policy.mode), caps.ctypes.data_as(_L), ctypes.c_void_p(probs.data_ptr()),
+              ctypes.c_void_p(gg.data_ptr()), ctypes.c_void_p(eg.data_ptr()), ctypes.c_void_p(yh.data_ptr()),
+              losses.ctypes.data_as(_D), _stream())
+    return dict(task_loss=float(losses[0]), aux_loss=float(losses[1]), gate_grads=gg, expert_grads=eg, probs=probs,
+                y_hat=yh, router=router)
+
+
+def train_f64(x, y, gates, experts, k: int, steps: int, lr: float, policy: CapacityPolicy = CapacityPolicy(),
+              c_hat=None, aux_kind: int = 0, aux_weight: float = 1.0, penalties=None):
+    """train()'s step loop (trainer.cpp:245-416) around layer_step_f64: per step the layer step, then the
+    synchronized SGD update in the reference's rounding (W -= lr * grad, product rounded first).  Returns the
+    task / aux loss trajectories and the final weights (device fp64)."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    g = torch.as_tensor(np.asarray(gates) if not isinstance(gates, torch.Tensor) else gates).to(dev, torch.float64).clone()
+    U = torch.as_tensor(np.asarray(experts) if not isinstance(experts, torch.Tensor) else experts).to(dev, torch.float64).clone()
+    task, aux = [], []
+    router = None
+    for _ in range(steps):
+        o = layer_step_f64(x, y, g, U, k, policy, c_hat, aux_kind, aux_weight, penalties, router)
+        router = o["router"]
+        task.append(o["task_loss"])
+        aux.append(o["aux_loss"])
+        g.sub_(o["gate_grads"] * lr)
+        U.sub_(o["expert_grads"] * lr)
+    return dict(task_loss=np.array(task), aux_loss=np.array(aux), gates=g, experts=U)
