@@ -287,12 +287,33 @@ struct EpiWgrad {
   }
 };
 
+// cg: CTAs per cluster -- 1, 2 (a pair: cta_group::2, M = 256) or 4 (two pairs on adjacent 256-row weight blocks
+// sharing the token operand by TMA multicast)
 template <int kMode, int BN, bool A_MN, bool B_MN, class Epi>
-static void launch_pair_or_single(bool pair, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
+static void launch_pair_or_single(int cg, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
                                   const typename Epi::Params& ep, cudaStream_t s) {
-  if (pair) launch_gemm<kMode, BN, A_MN, B_MN, Epi, 2>(ta, tb, p, ep, 0, s);
+  if constexpr (kMode == kModeSwap && !B_MN) {
+    if (cg == 4) {
+      launch_gemm<kMode, BN, A_MN, B_MN, Epi, 4>(ta, tb, p, ep, 0, s);
+      return;
+    }
+  }
+  if (cg >= 2) launch_gemm<kMode, BN, A_MN, B_MN, Epi, 2>(ta, tb, p, ep, 0, s);
   else launch_gemm<kMode, BN, A_MN, B_MN, Epi, 1>(ta, tb, p, ep, 0, s);
 }
+
+// Swap-GEMM cluster shape for M weight rows: one pair when M % 256 == 0, else single CTAs.  TAMOE_MC=1 selects
+// two multicasting pairs when M % 512 == 0 -- correct, but measured 3-18 % slower at C2, so off.
+static int swap_cluster(int M) {
+  static const int mc = [] {
+    const char* v = std::getenv("TAMOE_MC");
+    return v ? std::atoi(v) : 0;
+  }();
+  if (M % 512 == 0 && mc) return 4;
+  return M % 256 == 0 ? 2 : 1;
+}
+
+static uint32_t swap_token_box(int cg) { return cg == 4 ? 64 : (cg == 2 ? 128 : 256); }
 
 static SwapParams swap_params(__nv_bfloat16* out, __nv_bfloat16* pre_out, const __nv_bfloat16* pre_in, int M,
                               int R, int act_out, int act_grad) {
@@ -327,10 +348,10 @@ void grouped_fwd(const __nv_bfloat16* tokens, const __nv_bfloat16* w, int G, int
   check_groups(G);
   require(M % kBM == 0, "grouped_fwd: M must be a multiple of 128");
   require(K % 64 == 0, "grouped_fwd: K must be a multiple of 64");
-  const bool pair = M % 256 == 0;
+  const int pair = swap_cluster(M);
   const int Gw = w_mod > 0 ? w_mod : G;  // distinct weight matrices
   CUtensorMap ta = make_tmap_bf16(w, K, static_cast<uint64_t>(Gw) * M, K, kBM);
-  CUtensorMap tb = make_tmap_bf16(tokens, K, R, K, pair ? 128 : 256);
+  CUtensorMap tb = make_tmap_bf16(tokens, K, R, K, swap_token_box(pair));
   GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1, w_mod, 1, env_int("TAMOE_PF_DIST", 0),
                env_int("TAMOE_PF_B", 0)};
   SwapParams ep = swap_params(out, pre_out, nullptr, M, R, act, kActNone);
@@ -352,10 +373,10 @@ void grouped_dgrad(const __nv_bfloat16* grad_tokens, const __nv_bfloat16* w, int
   check_groups(G);
   require(M % kBM == 0, "grouped_dgrad: M must be a multiple of 128");
   require(K % 64 == 0, "grouped_dgrad: K must be a multiple of 64");
-  const bool pair = M % 256 == 0;
+  const int pair = swap_cluster(M);
   const int Gw = w_mod > 0 ? w_mod : G;
   CUtensorMap ta = make_tmap_bf16(w, M, static_cast<uint64_t>(Gw) * K, M, 64);
-  CUtensorMap tb = make_tmap_bf16(grad_tokens, K, R, K, pair ? 128 : 256);
+  CUtensorMap tb = make_tmap_bf16(grad_tokens, K, R, K, swap_token_box(pair));
   GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1, w_mod, 1, env_int("TAMOE_PF_DIST", 0),
                env_int("TAMOE_PF_B", 0)};
   SwapParams ep = swap_params(out, nullptr, pre_in, M, R, kActNone, pre_in ? act : kActNone);
@@ -381,7 +402,7 @@ void grouped_wgrad(const __nv_bfloat16* a_tokens, const __nv_bfloat16* b_tokens,
   require(nsub >= 1 && G * nsub <= kMaxGroups, "grouped_wgrad: too many sub-segments");
   GemmParams p{G, seg_start, seg_rows, M, N, 0, 1, 1, 1, 1, 0, nsub, 0, 0};
   EpiWgrad::Params ep{make_tmap_bf16_box(out, N, static_cast<uint64_t>(G) * M, N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)};
-  launch_pair_or_single<kModeWgrad, 256, true, true, EpiWgrad>(M % 256 == 0, ta, tb, p, ep, s);
+  launch_pair_or_single<kModeWgrad, 256, true, true, EpiWgrad>(M % 256 == 0 ? 2 : 1, ta, tb, p, ep, s);
 }
 
 }  // namespace tamoe

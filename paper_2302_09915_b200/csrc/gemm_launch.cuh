@@ -1,11 +1,14 @@
 // Host-side launcher of the persistent tcgen05 GEMM engine (one CTA per SM).
 #pragma once
+#include <algorithm>
+
 #include "common.hpp"
 #include "gemm_sm100.cuh"
 
 namespace tamoe {
 
-// kCG = 2 launches CTA pairs (cluster 2x1x1) running tcgen05.mma.cta_group::2 (M = 256 per pair).
+// kCG = 2 launches CTA pairs (cluster 2x1x1) running tcgen05.mma.cta_group::2 (M = 256 per pair); kCG = 4 two
+// pairs per cluster sharing the token operand by TMA multicast (swap GEMMs).
 template <int kMode, int BN, bool A_MN, bool B_MN, class Epi, int kCG = 1>
 void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, const typename Epi::Params& ep,
                  int grid_limit, cudaStream_t s) {
@@ -33,6 +36,17 @@ void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams&
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if constexpr (kCG > 1) {
+    // a persistent grid must be co-resident: GPCs whose SM count is not a multiple of kCG leave SMs idle
+    static int max_clusters[64] = {};
+    if (max_clusters[dev] == 0) {
+      int n = 0;
+      TAMOE_CUDA(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
+      max_clusters[dev] = n > 0 ? n : 1;
+    }
+    grid = std::min(grid, max_clusters[dev] * kCG);
+    cfg.gridDim = dim3(grid);
+  }
   TAMOE_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, p, ep));
 }
 

@@ -99,7 +99,7 @@ struct EpiSmem<Epi, decltype(void(Epi::kWarpBytes))> {
 template <int BN, int kEpiBytes = 0, int kCG = 1>
 struct GemmSmem {
   static constexpr int kABytes = kBM * kBK * 2;
-  static constexpr int kBBytes = (BN / kCG) * kBK * 2;  // a CTA pair splits B's N between its CTAs
+  static constexpr int kBBytes = (BN / (kCG == 1 ? 1 : 2)) * kBK * 2;  // a CTA pair splits B's N between its CTAs
   static constexpr int kStageBytes = kABytes + kBBytes;
   // barriers: full[S], empty[S], tfull[2], tempty[2]; tmem addr; tile prefix; group starts / rows
   static constexpr int kMiscBytes = (2 * 8 + 4) * 8 + 16 + (3 * kMaxGroups + 1) * 4;
@@ -236,6 +236,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const GemmParams p, const __grid_constant__ typename Epi::Params ep) {
   static_assert(kCG == 1 || kMode == kModeSwap || kMode == kModeWgrad, "CTA pairs only for grouped modes");
+  // kCG = 4: two CTA pairs per cluster on adjacent weight blocks of the same token tile; the token (B) operand
+  // is loaded once per cluster and multicast to both pairs (halves its L2 -> SMEM traffic)
+  static_assert(kCG != 4 || (kMode == kModeSwap && !B_MN), "pair multicast only for K-major swap GEMMs");
+  static_assert(kCG == 1 || kCG == 2 || kCG == 4, "cluster of 1 CTA, one pair or two pairs");
+  constexpr int kCGm = kCG == 1 ? 1 : 2;  // CTAs per tcgen05.mma (cta_group)
   using L = GemmSmem<BN, EpiSmem<Epi>::value, kCG>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -250,8 +255,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const int warp = ptx::warp_id();
   const int lane = ptx::lane_id();
-  const uint32_t rank = kCG == 2 ? ptx::cluster_ctarank() : 0u;
-  const bool leader = rank == 0;
+  const uint32_t rank = kCG > 1 ? ptx::cluster_ctarank() : 0u;
+  const uint32_t pair_base = rank & ~1u;  // rank of this CTA's pair leader
+  const bool leader = (rank & 1u) == 0;
   const int cluster_id = blockIdx.x / kCG;
   const int num_clusters = gridDim.x / kCG;
 
@@ -285,20 +291,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     ptx::prefetch_tmap(&tmB);
     for (int s = 0; s < L::kStages; ++s) {
       ptx::mbar_init(&full_bar[s], 1);
-      ptx::mbar_init(&empty_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], kCG == 4 ? 2 : 1);  // kCG 4: both pairs read every stage
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull_bar[b], 1);
-      ptx::mbar_init(&tempty_bar[b], kEpiWarps * kCG);
+      ptx::mbar_init(&tempty_bar[b], kEpiWarps * kCGm);
     }
     ptx::fence_barrier_init();
   }
   if (warp == kMmaWarp) {
-    if constexpr (kCG == 2) ptx::tmem_alloc_cg2<L::kTmemCols>(tmem_slot);
+    if constexpr (kCG > 1) ptx::tmem_alloc_cg2<L::kTmemCols>(tmem_slot);
     else ptx::tmem_alloc<L::kTmemCols>(tmem_slot);
   }
   ptx::tc_fence_before();
-  if constexpr (kCG == 2) ptx::cluster_sync();
+  if constexpr (kCG > 1) ptx::cluster_sync();
   else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
@@ -315,7 +321,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if constexpr (kMode == kModeSwap) {
           if constexpr (A_MN) { ti.ax = my_m0; ti.ay = ti.wg * p.Kw; }
           else { ti.ay = ti.wg * p.Mw + my_m0; }
-          ti.by += static_cast<int>(rank) * (ti.n / kCG);  // this CTA's half of the token tile
+          ti.by += static_cast<int>(rank & 1u) * (ti.n / kCGm);  // this CTA's half of the token tile
         } else if constexpr (kMode == kModeWgrad) {
           ti.ax = my_m0;
           ti.bx += static_cast<int>(rank) * (BN / kCG);
@@ -367,16 +373,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
             uint8_t* sa = smem + stage * L::kStageBytes;
             uint8_t* sb = sa + L::kABytes;
-            if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], kCG * L::kStageBytes);
-            if constexpr (kCG == 2) {
-              const uint32_t bar = ptx::mapa(&full_bar[stage], 0);
+            if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], kCGm * L::kStageBytes);
+            if constexpr (kCG > 1) {
+              const uint32_t bar = ptx::mapa(&full_bar[stage], pair_base);
               if constexpr (A_MN) {
                 ptx::tma_load_2d_cg2(sa, &tmA, bar, ti.ax, ti.ay + kb * kBK);
                 ptx::tma_load_2d_cg2(sa + 8192, &tmA, bar, ti.ax + 64, ti.ay + kb * kBK);
               } else {
                 ptx::tma_load_2d_cg2(sa, &tmA, bar, ti.ax + kb * kBK, ti.ay);
               }
-              if constexpr (B_MN) {
+              if constexpr (kCG == 4) {
+                // this pair loads one half of the CTA-half token box; both pairs' CTAs of the same half get it
+                const int pp = static_cast<int>(rank >> 1);
+                const uint16_t mask = static_cast<uint16_t>((1u << (rank & 1u)) | (1u << ((rank & 1u) + 2)));
+                ptx::tma_load_2d_cg2_mc(sb + pp * (L::kBBytes / 2), &tmB, bar, ti.bx + kb * kBK,
+                                        ti.by + pp * (BN / 4), mask);
+              } else if constexpr (B_MN) {
 #pragma unroll
                 for (int j = 0; j < BN / 128; ++j)
                   ptx::tma_load_2d_cg2(sb + j * 8192, &tmB, bar, ti.bx + 64 * j, ti.by + kb * kBK);
@@ -418,7 +430,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         ptx::mbar_wait(&tempty_bar[buf], (use & 1) ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * BN;
-        const uint32_t idesc = ptx::idesc_bf16(kBM * kCG, ti.n, A_MN, B_MN);
+        const uint32_t idesc = ptx::idesc_bf16(kBM * kCGm, ti.n, A_MN, B_MN);
         const int nsub = (kMode == kModeWgrad) ? p.nsub : 1;
         uint32_t acc = 0;
         int nkb_total = 0;
@@ -439,10 +451,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 const uint64_t bdesc = B_MN ? ptx::smem_desc_sw128(sb + kk * 2048, 8192, 1024)
                                             : ptx::smem_desc_sw128(sb + kk * 32, 16, 1024);
                 const uint32_t accum = (acc | static_cast<uint32_t>(kk > 0)) ? 1u : 0u;
-                if constexpr (kCG == 2) ptx::mma_bf16_cg2(d_tmem, adesc, bdesc, idesc, accum);
+                if constexpr (kCG > 1) ptx::mma_bf16_cg2(d_tmem, adesc, bdesc, idesc, accum);
                 else ptx::mma_bf16(d_tmem, adesc, bdesc, idesc, accum);
               }
-              if constexpr (kCG == 2) ptx::mma_commit_cg2(&empty_bar[stage], 0x3);
+              if constexpr (kCG == 4) ptx::mma_commit_cg2(&empty_bar[stage], 0xF);  // B came from both pairs
+              else if constexpr (kCG == 2) ptx::mma_commit_cg2(&empty_bar[stage], 0x3);
               else ptx::mma_commit(&empty_bar[stage]);
             }
             if (nk > 0) acc = 1u;
@@ -453,12 +466,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int nkb = nkb_total;
         if (ptx::elect_one()) {
           if (nkb > 0) {
-            if constexpr (kCG == 2) ptx::mma_commit_cg2(&tfull_bar[buf], 0x3);
+            if constexpr (kCG > 1) ptx::mma_commit_cg2(&tfull_bar[buf], static_cast<uint16_t>(0x3u << pair_base));
             else ptx::mma_commit(&tfull_bar[buf]);
           } else {
-            if constexpr (kCG == 2) {
-              ptx::mbar_arrive_remote(ptx::mapa(&tfull_bar[buf], 0));
-              ptx::mbar_arrive_remote(ptx::mapa(&tfull_bar[buf], 1));
+            if constexpr (kCG > 1) {
+              ptx::mbar_arrive_remote(ptx::mapa(&tfull_bar[buf], pair_base));
+              ptx::mbar_arrive_remote(ptx::mapa(&tfull_bar[buf], pair_base + 1));
             } else {
               ptx::mbar_arrive(&tfull_bar[buf]);
             }
@@ -499,7 +512,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          if constexpr (kCG == 2) ptx::mbar_arrive_remote(ptx::mapa(&tempty_bar[buf], 0));
+          if constexpr (kCG > 1) ptx::mbar_arrive_remote(ptx::mapa(&tempty_bar[buf], pair_base));
           else ptx::mbar_arrive(&tempty_bar[buf]);
         }
       }
@@ -518,7 +531,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          if constexpr (kCG == 2) ptx::mbar_arrive_remote(ptx::mapa(&tempty_bar[buf], 0));
+          if constexpr (kCG > 1) ptx::mbar_arrive_remote(ptx::mapa(&tempty_bar[buf], pair_base));
           else ptx::mbar_arrive(&tempty_bar[buf]);
         }
       };
@@ -531,11 +544,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     Epi::finish(ep, lane);
   }
-  if constexpr (kCG == 2) ptx::cluster_sync();
+  if constexpr (kCG > 1) ptx::cluster_sync();
   else __syncthreads();
   if (warp == kMmaWarp) {
     ptx::tc_fence_after();
-    if constexpr (kCG == 2) ptx::tmem_dealloc_cg2<L::kTmemCols>(tmem_base);
+    if constexpr (kCG > 1) ptx::tmem_dealloc_cg2<L::kTmemCols>(tmem_base);
     else ptx::tmem_dealloc<L::kTmemCols>(tmem_base);
   }
 }

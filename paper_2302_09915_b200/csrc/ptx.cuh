@@ -177,6 +177,16 @@ __device__ __forceinline__ void tma_load_2d_cg2(void* smem_dst, const void* tmap
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_cluster), "r"(c0), "r"(c1)
       : "memory");
 }
+// The same for a cluster of CTA pairs: the box lands at the same offset in every CTA of `mask`, and each
+// destination's bytes complete on the barrier at `bar_cluster`'s offset in that destination's pair leader.
+__device__ __forceinline__ void tma_load_2d_cg2_mc(void* smem_dst, const void* tmap, uint32_t bar_cluster, int c0,
+                                                   int c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_cluster), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc_cg2(uint32_t* smem_result) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_result)),
