@@ -177,13 +177,14 @@ int tamoe_grad_aux_loss_f64(const double* x, const double* probs, const double* 
  * bit-identical to the reference's whenever the softmax is.  Device fp64, row-major: x [P*S x d],
  * y [P*S x d_out], gates [P x d x N], experts [N x d x d_out]; outputs gate_grads [P x d x N],
  * expert_grads [N x d x d_out], optional probs [P*S x N] and y_hat [P*S x d_out].  Host: penalty [P x N]
- * (topo loss; NULL for balance), caps [P x N] (tamoe_capacity_caps), losses [2] = task, aux (TrainReport).
- * Routing arrays stay readable through tamoe_router_read.  Status 2 on a non-finite logit or an aux kind
- * other than balance / topo; status 1 when the step diverges (trainer.cpp:362-366). */
+ * (topo loss; NULL otherwise), c_hat [P x N] (aux_kind 2 = compulsory quota routing, apply_compulsory_quota
+ * trainer.cpp:121-169, top-1 only; NULL otherwise), caps [P x N] (tamoe_capacity_caps), losses [2] = task, aux
+ * (TrainReport).  Routing arrays stay readable through tamoe_router_read.  Status 2 on a non-finite logit or
+ * an unknown aux kind; status 1 when the step diverges (trainer.cpp:362-366). */
 int tamoe_layer_step_f64(tamoe_router* r, int d, int d_out, const double* x, const double* y, const double* gates,
-                         const double* experts, const double* penalty, int aux_kind, double aux_weight, int cap_mode,
-                         const long long* caps, double* probs, double* gate_grads, double* expert_grads,
-                         double* y_hat, double* losses, void* stream);
+                         const double* experts, const double* penalty, const double* c_hat, int aux_kind,
+                         double aux_weight, int cap_mode, const long long* caps, double* probs, double* gate_grads,
+                         double* expert_grads, double* y_hat, double* losses, void* stream);
 
 /* Auxiliary losses on a routing result (host, N-vectors; counts int64 = RoutingResult::counts). */
 /* loss_balance (gate.cpp:209-214) */
@@ -290,6 +291,15 @@ typedef struct {
 
 int tamoe_train(const tamoe_layer_config* cfg, const double* c_hat, const tamoe_train_opts* opts, const void* x,
                 const void* y, void* wg, void* w1, void* w2, tamoe_train_report* report, void* stream);
+/* train() in the reference's own precision (BASELINE C1): every step is tamoe_layer_step_f64 (fp64, linear
+ * experts, the reference's summation order) followed by the fp64 SGD update (W -= lr * grad).  cfg supplies P, S,
+ * d, d_out, N, k, cap_mode, capacity_factor, aux_weight, penalty_norm, temperature (f, act, need_dx ignored);
+ * opts->kind 0 balance / 1 topo / 2 compulsory.  x [P*S x d], y [P*S x d_out], gates [P x d x N],
+ * experts [N x d x d_out]: device fp64 in the reference's layouts, weights updated in place.  This is the
+ * entry point of the drop-in train() replacement integration/tad_train_b200.cpp. */
+int tamoe_train_f64(const tamoe_layer_config* cfg, const double* c_hat, const tamoe_train_opts* opts,
+                    const double* x, const double* y, double* gates, double* experts, tamoe_train_report* report,
+                    void* stream);
 int tamoe_layer_step(tamoe_layer* l, const tamoe_layer_io* io, void* stream);
 int tamoe_layer_read(tamoe_layer* l, int what, void* dst, long long bytes, void* stream);
 int tamoe_layer_n_pad(int N);

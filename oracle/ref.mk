@@ -44,3 +44,22 @@ $(OUT)/obj/tad_gate_b200.o: integration/tad_gate_b200.cpp include/tamoe.h
 $(OUT)/unit_tests_b200: $(GATE_FREE_OBJS) $(OUT)/obj/tad_gate_b200.o $(TEST_SRCS) oracle/doctest_shim/doctest.h $(B200_LIB)/libtamoe.so
 	$(CXX) $(FLAGS) -Ioracle/doctest_shim -I$(REF)/tests -o $@ $(TEST_SRCS) $(GATE_FREE_OBJS) $(OUT)/obj/tad_gate_b200.o \
 	  -L$(B200_LIB) -ltamoe -L$(CUDA_HOME)/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../../$(B200_LIB)'
+
+# The reference's own unit suite with BOTH gate.cpp and train()'s inline MoE layer step on the B200: the gate
+# shim as above plus integration/tad_train_b200.cpp (train() over tamoe_train_f64: the whole step -- gate,
+# routing, linear experts, combine, MSE, backward, SGD -- in fp64 on the GPU).  trainer.cpp's other functions
+# (gen_synthetic, tv_distance, compare_runs, apply_compulsory_quota, ...) stay the reference's: it is compiled
+# once more with its train() renamed out of the way.
+TRAIN_FREE_OBJS := $(filter-out $(OUT)/obj/gate.o $(OUT)/obj/trainer.o,$(OBJS))
+suite_b200_train: $(OUT)/unit_tests_b200_train
+$(OUT)/obj/trainer_notrain.o: $(REF)/core/src/trainer.cpp
+	@mkdir -p $(OUT)/obj
+	$(CXX) $(FLAGS) -Dtrain=tad_reference_train_unused -c $< -o $@
+$(OUT)/obj/tad_train_b200.o: integration/tad_train_b200.cpp include/tamoe.h
+	@mkdir -p $(OUT)/obj
+	$(CXX) $(FLAGS) -Iinclude -I$(CUDA_HOME)/include -c $< -o $@
+$(OUT)/unit_tests_b200_train: $(TRAIN_FREE_OBJS) $(OUT)/obj/trainer_notrain.o $(OUT)/obj/tad_gate_b200.o \
+    $(OUT)/obj/tad_train_b200.o $(TEST_SRCS) oracle/doctest_shim/doctest.h $(B200_LIB)/libtamoe.so
+	$(CXX) $(FLAGS) -Ioracle/doctest_shim -I$(REF)/tests -o $@ $(TEST_SRCS) $(TRAIN_FREE_OBJS) \
+	  $(OUT)/obj/trainer_notrain.o $(OUT)/obj/tad_gate_b200.o $(OUT)/obj/tad_train_b200.o \
+	  -L$(B200_LIB) -ltamoe -L$(CUDA_HOME)/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../../$(B200_LIB)'

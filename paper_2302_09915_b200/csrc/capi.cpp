@@ -313,9 +313,9 @@ int tamoe_grad_aux_loss_f64(const double* x, const double* probs, const double* 
 }
 
 int tamoe_layer_step_f64(tamoe_router* r, int d, int d_out, const double* x, const double* y, const double* gates,
-                         const double* experts, const double* penalty, int aux_kind, double aux_weight, int cap_mode,
-                         const long long* caps, double* probs, double* gate_grads, double* expert_grads,
-                         double* y_hat, double* losses, void* stream) {
+                         const double* experts, const double* penalty, const double* c_hat, int aux_kind,
+                         double aux_weight, int cap_mode, const long long* caps, double* probs, double* gate_grads,
+                         double* expert_grads, double* y_hat, double* losses, void* stream) {
   return guarded([&] {
     require(r != nullptr, "layer_step_f64: null router");
     F64StepArgs a;
@@ -326,6 +326,7 @@ int tamoe_layer_step_f64(tamoe_router* r, int d, int d_out, const double* x, con
     a.gates = gates;
     a.experts = experts;
     a.penalty = penalty;
+    a.c_hat = c_hat;
     a.aux_kind = aux_kind;
     a.aux_weight = aux_weight;
     a.cap_mode = cap_mode;
@@ -374,6 +375,40 @@ int tamoe_layer_create(const tamoe_layer_config* cfg, const double* c_hat, tamoe
   });
 }
 
+namespace {
+
+TrainOptions train_options(const tamoe_train_opts* opts) {
+  TrainOptions o;
+  o.kind = opts->kind;
+  o.steps = opts->steps;
+  o.lr = opts->lr;
+  o.switch_step = opts->has_switch ? opts->switch_step : INT_MIN;
+  o.report_window = opts->report_window;
+  o.bytes_per_element = opts->bytes_per_element;
+  o.alpha_hat = opts->alpha_hat;
+  o.beta_hat = opts->beta_hat;
+  o.intra_groups = opts->intra_groups;
+  return o;
+}
+
+void fill_report(const TrainReport& r, tamoe_train_report* report) {
+  auto put = [](double* dst, const std::vector<double>& v) {
+    if (dst && !v.empty()) std::memcpy(dst, v.data(), sizeof(double) * v.size());
+  };
+  put(report->task_loss, r.task_loss);
+  put(report->aux_loss, r.aux_loss);
+  put(report->comm_us, r.comm_us);
+  put(report->dropped_rate, r.dropped_rate);
+  put(report->initial_dispatch, r.initial_dispatch);
+  put(report->final_dispatch, r.final_dispatch);
+  put(report->tv_rows, r.tv_rows);
+  const double sm[9] = {r.tv_initial_mean, r.tv_final_mean, r.col_balance_max_dev, r.min_expert_load,
+                        r.intra_share, r.final_task_loss, r.final_aux_loss, r.final_comm_us, r.dropped_total_rate};
+  std::memcpy(report->summary, sm, sizeof(sm));
+}
+
+}  // namespace
+
 int tamoe_train(const tamoe_layer_config* cfg, const double* c_hat, const tamoe_train_opts* opts, const void* x,
                 const void* y, void* wg, void* w1, void* w2, tamoe_train_report* report, void* stream) {
   return guarded([&] {
@@ -382,33 +417,25 @@ int tamoe_train(const tamoe_layer_config* cfg, const double* c_hat, const tamoe_
     LayerConfig c{cfg->P, cfg->S, cfg->d, cfg->d_out, cfg->N, cfg->k, cfg->f, cfg->act, cfg->cap_mode,
                   cfg->capacity_factor, cfg->aux_kind, cfg->aux_weight, cfg->penalty_norm, cfg->temperature,
                   cfg->need_dx, cfg->world_size, cfg->rank};
-    TrainOptions o;
-    o.kind = opts->kind;
-    o.steps = opts->steps;
-    o.lr = opts->lr;
-    o.switch_step = opts->has_switch ? opts->switch_step : INT_MIN;
-    o.report_window = opts->report_window;
-    o.bytes_per_element = opts->bytes_per_element;
-    o.alpha_hat = opts->alpha_hat;
-    o.beta_hat = opts->beta_hat;
-    o.intra_groups = opts->intra_groups;
-    const TrainReport r = train_layer(c, c_hat, o, static_cast<const __nv_bfloat16*>(x),
+    const TrainReport r = train_layer(c, c_hat, train_options(opts), static_cast<const __nv_bfloat16*>(x),
                                       static_cast<const __nv_bfloat16*>(y), static_cast<__nv_bfloat16*>(wg),
                                       static_cast<__nv_bfloat16*>(w1), static_cast<__nv_bfloat16*>(w2),
                                       static_cast<cudaStream_t>(stream));
-    auto put = [](double* dst, const std::vector<double>& v) {
-      if (dst && !v.empty()) std::memcpy(dst, v.data(), sizeof(double) * v.size());
-    };
-    put(report->task_loss, r.task_loss);
-    put(report->aux_loss, r.aux_loss);
-    put(report->comm_us, r.comm_us);
-    put(report->dropped_rate, r.dropped_rate);
-    put(report->initial_dispatch, r.initial_dispatch);
-    put(report->final_dispatch, r.final_dispatch);
-    put(report->tv_rows, r.tv_rows);
-    const double sm[9] = {r.tv_initial_mean, r.tv_final_mean, r.col_balance_max_dev, r.min_expert_load,
-                          r.intra_share, r.final_task_loss, r.final_aux_loss, r.final_comm_us, r.dropped_total_rate};
-    std::memcpy(report->summary, sm, sizeof(sm));
+    fill_report(r, report);
+  });
+}
+
+int tamoe_train_f64(const tamoe_layer_config* cfg, const double* c_hat, const tamoe_train_opts* opts,
+                    const double* x, const double* y, double* gates, double* experts, tamoe_train_report* report,
+                    void* stream) {
+  return guarded([&] {
+    require(cfg && opts && report && gates && experts, "train_f64: null argument");
+    require(cfg->P >= 1 && cfg->S >= 0 && cfg->d >= 1 && cfg->d_out >= 1 && cfg->N >= 1, "train_f64: bad shape");
+    require(static_cast<long long>(cfg->P) * cfg->S == 0 || (x && y), "train_f64: null batch");
+    const TrainReport r = train_f64(cfg->P, cfg->S, cfg->d, cfg->d_out, cfg->N, cfg->k, cfg->cap_mode,
+                                    cfg->capacity_factor, cfg->aux_weight, cfg->penalty_norm, cfg->temperature, c_hat,
+                                    train_options(opts), x, y, gates, experts, static_cast<cudaStream_t>(stream));
+    fill_report(r, report);
   });
 }
 

@@ -13,9 +13,11 @@
 
 #include <algorithm>
 #include <cmath>
+#include <vector>
 
 #include "common.hpp"
 #include "gate_f64.hpp"
+#include "host_topology.hpp"
 #include "layer_f64.hpp"
 
 namespace tamoe {
@@ -244,8 +246,10 @@ void layer_step_f64(RouteWorkspace& rw, const F64StepArgs& a, cudaStream_t s) {
   const RouteDims& dm = rw.dims;
   const int P = dm.P, S = dm.S, N = dm.N, d = a.d, dout = a.d_out;
   require(d > 0 && dout > 0, "layer_step_f64: d and d_out must be positive");
-  require(a.aux_kind == 0 || a.aux_kind == 1, "layer_step_f64: aux kind must be balance (0) or topo (1)");
-  require(a.aux_kind == 0 || a.penalty != nullptr, "layer_step_f64: topo loss needs penalty weights");
+  require(a.aux_kind >= 0 && a.aux_kind <= 2, "layer_step_f64: aux kind must be balance, topo or compulsory");
+  require(a.aux_kind != 1 || a.penalty != nullptr, "layer_step_f64: topo loss needs penalty weights");
+  require(a.aux_kind != 2 || (a.c_hat != nullptr && dm.k == 1),
+          "compulsory routing supports top-1 only and requires a target pattern");
   require(a.x && a.y && a.gates && a.experts && a.gate_grads && a.expert_grads && a.losses && a.caps,
           "layer_step_f64: null buffer");
   require(rw.buf.gate64 != nullptr, "layer_step_f64: router without fp64 gate values");
@@ -269,11 +273,35 @@ void layer_step_f64(RouteWorkspace& rw, const F64StepArgs& a, cudaStream_t s) {
   // topk_route (trainer.cpp:249-250)
   rw.upload_caps(a.caps, s);
   route_rows_from_probs(probs, dm, rw.row_out(nullptr, nullptr), s);
-  rw.finish(a.cap_mode, s);
+  if (a.aux_kind == 2) {
+    // apply_compulsory_quota (trainer.cpp:121-169): quota_i = LRR(c_hat_i / sum(c_hat_i) * S, S); tokens by
+    // score claim experts in probability order; every token kept, gate value = the claimed probability
+    std::vector<int> q(static_cast<size_t>(P) * N);
+    for (int i = 0; i < P; ++i) {
+      const double* row = a.c_hat + static_cast<size_t>(i) * N;
+      double sum = 0.0;
+      for (int e = 0; e < N; ++e) sum += row[e];
+      std::vector<double> share(static_cast<size_t>(N));
+      for (int e = 0; e < N; ++e) share[static_cast<size_t>(e)] = row[e] / sum * static_cast<double>(S);
+      const auto lrr = largest_remainder_round(share.data(), N, S);
+      for (int e = 0; e < N; ++e) q[static_cast<size_t>(i) * N + e] = static_cast<int>(lrr[static_cast<size_t>(e)]);
+    }
+    Scratch<int> quota(static_cast<long long>(P) * N, s);
+    const size_t ws_bytes = compulsory_workspace_bytes(P, S);
+    Scratch<unsigned char> ws(static_cast<long long>(ws_bytes), s);
+    TAMOE_CUDA(cudaMemcpyAsync(quota.p, q.data(), sizeof(int) * q.size(), cudaMemcpyHostToDevice, s));
+    route_compulsory(dm, rw.buf, probs, quota.p, ws.p, ws_bytes, s);
+    TAMOE_CUDA(cudaMemcpyAsync(rw.buf.gate64, rw.buf.score, sizeof(double) * dm.picks(), cudaMemcpyDeviceToDevice, s));
+    rw.finish(0, s);
+    TAMOE_CUDA(cudaStreamSynchronize(s));  // q is host memory
+  } else {
+    rw.finish(a.cap_mode, s);
+  }
+  const int loss_kind = a.aux_kind == 1 ? 1 : 0;  // compulsory trains with the balance loss (trainer.cpp:253)
 
   Scratch<double> out(picks * dout, s), resid(T * dout, s), dldg(picks, s), task_part(T, s), dz(T * N, s),
       mean(static_cast<long long>(P) * N, s), coeff(static_cast<long long>(P) * N, s), pen(P * N, s), loss_d(2, s);
-  if (a.aux_kind == 1)
+  if (loss_kind == 1)
     TAMOE_CUDA(cudaMemcpyAsync(pen.p, a.penalty, sizeof(double) * P * N, cudaMemcpyHostToDevice, s));
   const double mse_scale = 2.0 / (static_cast<double>(P) * S * dout);
   const double task_den = static_cast<double>(P) * S * dout;
@@ -291,7 +319,7 @@ void layer_step_f64(RouteWorkspace& rw, const F64StepArgs& a, cudaStream_t s) {
   const dim3 gw((dout + kT - 1) / kT, (d + kT - 1) / kT, N);
   expert_wgrad_f64_kernel<<<gw, dim3(kT, kT), 0, s>>>(dm, rw.buf, a.x, resid.p, d, dout, mse_scale, a.expert_grads);
   TAMOE_CUDA(cudaGetLastError());
-  aux_f64_kernel<<<1, 256, 0, s>>>(dm, rw.buf, probs, pen.p, a.aux_kind, task_part.p, task_den, mean.p, coeff.p,
+  aux_f64_kernel<<<1, 256, 0, s>>>(dm, rw.buf, probs, pen.p, loss_kind, task_part.p, task_den, mean.p, coeff.p,
                                    loss_d.p);
   TAMOE_CUDA(cudaGetLastError());
   if (T > 0) {

@@ -20,7 +20,8 @@ struct F64StepArgs {
   const double* gates = nullptr;    // device [P x d x N]   (GateState::W per process, trainer.cpp:207-216)
   const double* experts = nullptr;  // device [N x d x d_out] (linear experts U_e, trainer.cpp:219-223)
   const double* penalty = nullptr;  // host [P x N] (topo loss only)
-  int aux_kind = 0;                 // 0 balance, 1 topo
+  const double* c_hat = nullptr;    // host [P x N] (compulsory quotas only)
+  int aux_kind = 0;                 // 0 balance, 1 topo, 2 compulsory (quota routing, balance loss)
   double aux_weight = 1.0;
   int cap_mode = 0;
   const long long* caps = nullptr;  // host [P x N] (tamoe_capacity_caps)

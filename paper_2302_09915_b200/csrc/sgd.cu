@@ -35,6 +35,13 @@ __global__ void widen_kernel(const __nv_bfloat16* __restrict__ w, float* __restr
     master[i] = __bfloat162float(w[i]);
 }
 
+// fp64 weights in the reference's rounding: w -= (lr * g), product rounded first (no FMA)
+__global__ void sgd_f64_kernel(double* __restrict__ w, const double* __restrict__ grad, double lr, long long n) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    w[i] = __dsub_rn(w[i], __dmul_rn(lr, grad[i]));
+}
+
 int grid_for(long long n) {
   const long long b = (n + 255) / 256;
   return static_cast<int>(b < 4LL * num_sms() ? (b > 0 ? b : 1) : 4LL * num_sms());
@@ -49,6 +56,12 @@ void sgd_step(float* master, const __nv_bfloat16* grad, float lr, __nv_bfloat16*
 
 void sgd_step(float* master, const float* grad, float lr, __nv_bfloat16* work, long long n, cudaStream_t s) {
   sgd_kernel<<<grid_for(n), 256, 0, s>>>(master, grad, lr, work, n);
+  TAMOE_CUDA(cudaGetLastError());
+}
+
+void sgd_step_f64(double* w, const double* grad, double lr, long long n, cudaStream_t s) {
+  if (n <= 0) return;
+  sgd_f64_kernel<<<grid_for(n), 256, 0, s>>>(w, grad, lr, n);
   TAMOE_CUDA(cudaGetLastError());
 }
 

@@ -11,6 +11,7 @@
 
 #include "common.hpp"
 #include "host_topology.hpp"
+#include "layer_f64.hpp"
 #include "sgd.hpp"
 
 namespace tamoe {
@@ -50,43 +51,17 @@ struct DevBuf {
 
 }  // namespace
 
-TrainReport train_layer(LayerConfig cfg, const double* c_hat, const TrainOptions& o, const __nv_bfloat16* x,
-                        const __nv_bfloat16* y, __nv_bfloat16* wg, __nv_bfloat16* w1, __nv_bfloat16* w2,
-                        cudaStream_t s) {
-  require(cfg.world_size == 1, "train: single-device layer (P logical processes)");
-  require(o.kind >= 0 && o.kind <= 2, "train: unknown loss kind");
-  require(o.steps >= 0, "train: steps must be >= 0");
-  require(o.kind == 0 || c_hat != nullptr, "topo and compulsory losses require a target pattern");
-  cfg.aux_kind = o.kind;  // 2 = compulsory quota routing + balance loss
-  const int P = cfg.P, S = cfg.S, N = cfg.N, k = cfg.k, E = N / P;
-  require(N % P == 0, "N must be divisible by P");
-  Layer layer(cfg, cfg.aux_kind != 0 ? c_hat : nullptr);
-  const int n_pad = layer.n_pad();
-  const long long n_wg = static_cast<long long>(P) * n_pad * cfg.d;
-  const long long n_w1 = static_cast<long long>(N) * (cfg.f == 0 ? cfg.d_out : cfg.f) * cfg.d;
-  const long long n_w2 = cfg.f == 0 ? 0 : static_cast<long long>(N) * cfg.d_out * cfg.f;
+namespace {
 
-  DevBuf buf;
-  float* m_wg = buf.get<float>(n_wg);
-  float* m_w1 = buf.get<float>(n_w1);
-  float* m_w2 = n_w2 ? buf.get<float>(n_w2) : nullptr;
-  widen_bf16(wg, m_wg, n_wg, s);
-  widen_bf16(w1, m_w1, n_w1, s);
-  if (n_w2) widen_bf16(w2, m_w2, n_w2, s);
-  LayerIO io{};
-  io.x = x;
-  io.y = y;
-  io.wg = wg;
-  io.w1 = w1;
-  io.w2 = n_w2 ? w2 : nullptr;
-  io.dwg = buf.get<float>(n_wg);
-  io.dw1 = buf.get<__nv_bfloat16>(n_w1);
-  io.dw2 = n_w2 ? buf.get<__nv_bfloat16>(n_w2) : nullptr;
-  io.dx = cfg.need_dx ? buf.get<__nv_bfloat16>(static_cast<long long>(P) * S * cfg.d) : nullptr;
-  io.losses = buf.get<double>(2);
-
+// The bookkeeping of train() (trainer.cpp:227-452) around a device step: `step(i, losses, counts, dropped)` runs
+// step i (forward, backward, the synchronized SGD update) and returns its task / aux loss and the per-(process,
+// expert) kept / dropped counts; everything the report derives from them is restated here on the host.
+template <class Step>
+TrainReport run_train(int P, int S, int N, int k, int d, int cap_mode, double aux_weight, const double* c_hat,
+                      const TrainOptions& o, Step&& step_fn) {
+  const int E = N / P;
   const bool has_profile = o.alpha_hat != nullptr && o.beta_hat != nullptr;
-  const int rounds = (cfg.cap_mode == 1 || cfg.cap_mode == 3) ? 1 : 0;  // global / proportional: size round
+  const int rounds = (cap_mode == 1 || cap_mode == 3) ? 1 : 0;  // global / proportional: size round
   TrainReport rep;
   const int window = std::max(1, std::min(o.report_window, std::max(o.steps, 1)));
   const int window_start = std::max(0, o.steps - window);
@@ -96,23 +71,11 @@ TrainReport train_layer(LayerConfig cfg, const double* c_hat, const TrainOptions
   std::vector<int> counts_i(static_cast<size_t>(P) * N), dropped_i(static_cast<size_t>(P) * N);
   std::vector<double> counts(static_cast<size_t>(P) * N);
   double losses[2];
-  const RouteBuffers& rb = layer.route().buf;
 
   for (int step = 0; step < o.steps; ++step) {
-    if (o.kind == 1 && o.switch_step != INT_MIN && step > o.switch_step) layer.set_aux_kind(0);
-    layer.step(io, s);
-    TAMOE_CUDA(cudaMemcpyAsync(losses, io.losses, sizeof(losses), cudaMemcpyDeviceToHost, s));
-    TAMOE_CUDA(cudaMemcpyAsync(counts_i.data(), rb.counts, sizeof(int) * counts_i.size(), cudaMemcpyDeviceToHost, s));
-    TAMOE_CUDA(cudaMemcpyAsync(dropped_i.data(), rb.dropped, sizeof(int) * dropped_i.size(), cudaMemcpyDeviceToHost,
-                               s));
-    // synchronized update, fixed order (gates, then experts)
-    sgd_step(m_wg, io.dwg, static_cast<float>(o.lr), wg, n_wg, s);
-    sgd_step(m_w1, io.dw1, static_cast<float>(o.lr), w1, n_w1, s);
-    if (n_w2) sgd_step(m_w2, io.dw2, static_cast<float>(o.lr), w2, n_w2, s);
-    TAMOE_CUDA(cudaStreamSynchronize(s));
-
+    step_fn(step, losses, counts_i.data(), dropped_i.data());
     const double task = losses[0], aux = losses[1];
-    if (!std::isfinite(task + cfg.aux_weight * aux))
+    if (!std::isfinite(task + aux_weight * aux))
       throw std::runtime_error("training diverged at step " + std::to_string(step) + " (task=" +
                                std::to_string(task) + ", aux=" + std::to_string(aux) + "); lower the learning rate");
     long long dropped_step = 0;
@@ -124,7 +87,7 @@ TrainReport train_layer(LayerConfig cfg, const double* c_hat, const TrainOptions
     double comm = 0.0;
     if (has_profile) {
       // DispatchConfig{k, S, N, P, d, b}: payload of d * bytes_per_element per token (trainer.cpp:239)
-      const double mb_per_token = cfg.d * o.bytes_per_element / 1e6;
+      const double mb_per_token = d * o.bytes_per_element / 1e6;
       const std::vector<double> pay = device_payload_tokens(counts.data(), P, N);
       double bott = 0.0, max_alpha = 0.0;
       for (int i = 0; i < P * P; ++i) {
@@ -191,6 +154,113 @@ TrainReport train_layer(LayerConfig cfg, const double* c_hat, const TrainOptions
     rep.tv_final_mean = tv1 / P;
   }
   return rep;
+}
+
+
+}  // namespace
+
+TrainReport train_layer(LayerConfig cfg, const double* c_hat, const TrainOptions& o, const __nv_bfloat16* x,
+                        const __nv_bfloat16* y, __nv_bfloat16* wg, __nv_bfloat16* w1, __nv_bfloat16* w2,
+                        cudaStream_t s) {
+  require(cfg.world_size == 1, "train: single-device layer (P logical processes)");
+  require(o.kind >= 0 && o.kind <= 2, "train: unknown loss kind");
+  require(o.steps >= 0, "train: steps must be >= 0");
+  require(o.kind == 0 || c_hat != nullptr, "topo and compulsory losses require a target pattern");
+  cfg.aux_kind = o.kind;  // 2 = compulsory quota routing + balance loss
+  require(cfg.N % cfg.P == 0, "N must be divisible by P");
+  const int P = cfg.P, S = cfg.S, N = cfg.N;
+  Layer layer(cfg, cfg.aux_kind != 0 ? c_hat : nullptr);
+  const int n_pad = layer.n_pad();
+  const long long n_wg = static_cast<long long>(P) * n_pad * cfg.d;
+  const long long n_w1 = static_cast<long long>(N) * (cfg.f == 0 ? cfg.d_out : cfg.f) * cfg.d;
+  const long long n_w2 = cfg.f == 0 ? 0 : static_cast<long long>(N) * cfg.d_out * cfg.f;
+
+  DevBuf buf;
+  float* m_wg = buf.get<float>(n_wg);
+  float* m_w1 = buf.get<float>(n_w1);
+  float* m_w2 = n_w2 ? buf.get<float>(n_w2) : nullptr;
+  widen_bf16(wg, m_wg, n_wg, s);
+  widen_bf16(w1, m_w1, n_w1, s);
+  if (n_w2) widen_bf16(w2, m_w2, n_w2, s);
+  LayerIO io{};
+  io.x = x;
+  io.y = y;
+  io.wg = wg;
+  io.w1 = w1;
+  io.w2 = n_w2 ? w2 : nullptr;
+  io.dwg = buf.get<float>(n_wg);
+  io.dw1 = buf.get<__nv_bfloat16>(n_w1);
+  io.dw2 = n_w2 ? buf.get<__nv_bfloat16>(n_w2) : nullptr;
+  io.dx = cfg.need_dx ? buf.get<__nv_bfloat16>(static_cast<long long>(P) * S * cfg.d) : nullptr;
+  io.losses = buf.get<double>(2);
+
+  const RouteBuffers& rb = layer.route().buf;
+  return run_train(cfg.P, cfg.S, cfg.N, cfg.k, cfg.d, cfg.cap_mode, cfg.aux_weight, c_hat, o,
+                   [&](int step, double* losses, int* counts_i, int* dropped_i) {
+                     if (o.kind == 1 && o.switch_step != INT_MIN && step > o.switch_step) layer.set_aux_kind(0);
+                     layer.step(io, s);
+                     const size_t pn = static_cast<size_t>(cfg.P) * cfg.N;
+                     TAMOE_CUDA(cudaMemcpyAsync(losses, io.losses, sizeof(double) * 2, cudaMemcpyDeviceToHost, s));
+                     TAMOE_CUDA(cudaMemcpyAsync(counts_i, rb.counts, sizeof(int) * pn, cudaMemcpyDeviceToHost, s));
+                     TAMOE_CUDA(cudaMemcpyAsync(dropped_i, rb.dropped, sizeof(int) * pn, cudaMemcpyDeviceToHost, s));
+                     // synchronized update, fixed order (gates, then experts)
+                     sgd_step(m_wg, io.dwg, static_cast<float>(o.lr), wg, n_wg, s);
+                     sgd_step(m_w1, io.dw1, static_cast<float>(o.lr), w1, n_w1, s);
+                     if (n_w2) sgd_step(m_w2, io.dw2, static_cast<float>(o.lr), w2, n_w2, s);
+                     TAMOE_CUDA(cudaStreamSynchronize(s));
+                   });
+}
+
+TrainReport train_f64(int P, int S, int d, int d_out, int N, int k, int cap_mode, double cf, double aux_weight,
+                      int norm, double temperature, const double* c_hat, const TrainOptions& o, const double* x,
+                      const double* y, double* gates, double* experts, cudaStream_t s) {
+  require(o.kind >= 0 && o.kind <= 2, "train: unknown loss kind");
+  require(o.steps >= 0, "train: steps must be >= 0");
+  require(N % P == 0, "N must be divisible by P");
+  require(o.kind == 0 || c_hat != nullptr, "topo and compulsory losses require a target pattern");
+  std::vector<double> pen;
+  if (c_hat) {
+    for (int i = 0; i < P; ++i) {
+      const auto row = penalty_weights(c_hat + static_cast<size_t>(i) * N, N, norm, temperature);
+      pen.insert(pen.end(), row.begin(), row.end());
+    }
+  }
+  // the reference withholds c_hat from balance routing (trainer.cpp:250)
+  const auto caps = capacity_caps(cap_mode, cf, k, S, N, P, o.kind == 0 ? nullptr : c_hat);
+  Router router(P, S, N, k);
+  DevBuf buf;
+  const long long n_g = static_cast<long long>(P) * d * N, n_u = static_cast<long long>(N) * d * d_out;
+  double* gg = buf.get<double>(n_g);
+  double* eg = buf.get<double>(n_u);
+  const RouteBuffers& rb = router.rw.buf;
+  return run_train(P, S, N, k, d, cap_mode, aux_weight, c_hat, o,
+                   [&](int step, double* losses, int* counts_i, int* dropped_i) {
+                     F64StepArgs a;
+                     a.d = d;
+                     a.d_out = d_out;
+                     a.x = x;
+                     a.y = y;
+                     a.gates = gates;
+                     a.experts = experts;
+                     const bool switched = o.kind == 1 && o.switch_step != INT_MIN && step > o.switch_step;
+                     a.aux_kind = switched ? 0 : o.kind;
+                     a.penalty = pen.empty() ? nullptr : pen.data();
+                     a.c_hat = c_hat;
+                     a.aux_weight = aux_weight;
+                     a.cap_mode = cap_mode;
+                     a.caps = caps.data();
+                     a.gate_grads = gg;
+                     a.expert_grads = eg;
+                     a.losses = losses;
+                     layer_step_f64(router.rw, a, s);
+                     const size_t pn = static_cast<size_t>(P) * N;
+                     TAMOE_CUDA(cudaMemcpyAsync(counts_i, rb.counts, sizeof(int) * pn, cudaMemcpyDeviceToHost, s));
+                     TAMOE_CUDA(cudaMemcpyAsync(dropped_i, rb.dropped, sizeof(int) * pn, cudaMemcpyDeviceToHost, s));
+                     // synchronized update, fixed order (gates, then experts), in the reference's rounding
+                     sgd_step_f64(gates, gg, o.lr, n_g, s);
+                     sgd_step_f64(experts, eg, o.lr, n_u, s);
+                     TAMOE_CUDA(cudaStreamSynchronize(s));
+                   });
 }
 
 }  // namespace tamoe

@@ -35,6 +35,13 @@ TrainReport train_layer(LayerConfig cfg, const double* c_hat, const TrainOptions
                         const __nv_bfloat16* y, __nv_bfloat16* wg, __nv_bfloat16* w1, __nv_bfloat16* w2,
                         cudaStream_t s);
 
+// The same loop in the reference's own precision (BASELINE C1): fp64 device step (layer_step_f64, linear experts)
+// and fp64 SGD.  x [P*S x d], y [P*S x d_out], gates [P x d x N], experts [N x d x d_out]: device fp64 in the
+// reference's layouts; gates / experts are the initial weights on entry and the trained weights on return.
+TrainReport train_f64(int P, int S, int d, int d_out, int N, int k, int cap_mode, double cf, double aux_weight,
+                      int norm, double temperature, const double* c_hat, const TrainOptions& opts, const double* x,
+                      const double* y, double* gates, double* experts, cudaStream_t s);
+
 double tv_distance(const double* a, const double* b, int n);  // trainer.cpp:88-96
 
 }  // namespace tamoe

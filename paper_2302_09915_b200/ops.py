@@ -447,7 +447,7 @@ def grad_loss_topo(x, probs, result: RoutingResult, penalty, N: int, P: int, S: 
 
 # ----------------------------------------------------------------------------- reference-precision layer step
 _lib.lib.tamoe_layer_step_f64.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int] + [ctypes.c_void_p] * 4 + \
-    [_D, ctypes.c_int, ctypes.c_double, ctypes.c_int, _L] + [ctypes.c_void_p] * 4 + [_D, ctypes.c_void_p]
+    [_D, _D, ctypes.c_int, ctypes.c_double, ctypes.c_int, _L] + [ctypes.c_void_p] * 4 + [_D, ctypes.c_void_p]
 _lib.lib.tamoe_layer_step_f64.restype = ctypes.c_int
 
 
@@ -456,7 +456,8 @@ def layer_step_f64(x, y, gates, experts, k: int, policy: CapacityPolicy = Capaci
     """One step of the reference's MoE layer in its own precision (BASELINE config 1: fp64, linear experts) on
     the device -- the inline step of train() (trainer.cpp:246-356).  x [P, S, d], y [P, S, d_out],
     gates [P, d, N] (GateState::W), experts [N, d, d_out] (U_e); numpy or torch (moved to the GPU as fp64).
-    aux_kind 0 balance / 1 topo (penalties [P, N] = penalty_weights of each c_hat row).  Returns a dict with
+    aux_kind 0 balance / 1 topo (penalties [P, N] = penalty_weights of each c_hat row) / 2 compulsory quota
+    routing (top-1, quotas from c_hat, balance loss).  Returns a dict with
     task_loss / aux_loss (TrainReport), gate_grads [P, d, N], expert_grads [N, d, d_out], probs [P, S, N],
     y_hat [P, S, d_out] (device fp64 tensors) and the router (routing arrays via Router.read)."""
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -471,8 +472,10 @@ def layer_step_f64(x, y, gates, experts, k: int, policy: CapacityPolicy = Capaci
     N = gates.shape[2]
     if router is None or (router.P, router.S, router.N, router.k) != (P, S, N, k):
         router = Router(P, S, N, k)
-    caps = capacity_caps(policy, k, S, N, P, c_hat)
+    # the reference withholds c_hat from balance routing (trainer.cpp:250)
+    caps = capacity_caps(policy, k, S, N, P, c_hat if aux_kind != 0 else None)
     pen = _f64(penalties) if penalties is not None else None
+    ch = _f64(c_hat) if (c_hat is not None and aux_kind == 2) else None
     probs = torch.empty(P, S, N, dtype=torch.float64, device=dev)
     gg = torch.empty(P, d, N, dtype=torch.float64, device=dev)
     eg = torch.empty(N, d, d_out, dtype=torch.float64, device=dev)
@@ -480,7 +483,8 @@ def layer_step_f64(x, y, gates, experts, k: int, policy: CapacityPolicy = Capaci
     losses = np.zeros(2)
     _lib.call("tamoe_layer_step_f64", router._h, d, d_out, ctypes.c_void_p(x.data_ptr()),
               ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(gates.data_ptr()), ctypes.c_void_p(experts.data_ptr()),
-              pen.ctypes.data_as(_D) if pen is not None else None, int(aux_kind), float(aux_weight),
+              pen.ctypes.data_as(_D) if pen is not None else None, ch.ctypes.data_as(_D) if ch is not None else None,
+              int(aux_kind), float(aux_weight),
               int(policy.mode), caps.ctypes.data_as(_L), ctypes.c_void_p(probs.data_ptr()),
               ctypes.c_void_p(gg.data_ptr()), ctypes.c_void_p(eg.data_ptr()), ctypes.c_void_p(yh.data_ptr()),
               losses.ctypes.data_as(_D), _stream())

@@ -15,6 +15,7 @@ import oracle
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SUITE = os.path.join(ROOT, "oracle", "_ref", "unit_tests_b200")
+SUITE_TRAIN = os.path.join(ROOT, "oracle", "_ref", "unit_tests_b200_train")
 
 
 def _ops():
@@ -80,4 +81,18 @@ def test_reference_unit_suite_on_the_b200_gate():
     assert summary, r.stdout[-2000:] + r.stderr[-4000:]
     print(summary[0])
     assert r.returncode == 0, summary[0] + "\n" + r.stderr[-6000:]
+    assert "failed: 0 " in summary[0]
+
+
+def test_reference_unit_suite_with_train_step_on_the_b200():
+    """The reference's 68-case suite with gate.cpp AND train()'s inline layer step replaced: every train() call of
+    test_trainer.cpp / test_report_io.cpp runs its whole step (gate, routing, experts, combine, backward, SGD) on
+    the GPU in fp64 through tamoe_train_f64 (integration/tad_train_b200.cpp)."""
+    if not os.path.exists(SUITE_TRAIN):
+        pytest.skip("oracle/_ref/unit_tests_b200_train not built (make -f oracle/ref.mk suite_b200_train)")
+    r = subprocess.run([SUITE_TRAIN], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    summary = [ln for ln in r.stdout.splitlines() if "[doctest-shim]" in ln]
+    assert summary, r.stdout[-2000:] + r.stderr[-4000:]
+    print(summary[0])
+    assert r.returncode == 0, summary[0] + "\n" + r.stdout[-4000:] + r.stderr[-6000:]
     assert "failed: 0 " in summary[0]

@@ -3,6 +3,7 @@ the inline step of train(), trainer.cpp:246-356) against
   * the reference itself (train(), compiled from its sources into oracle/_ref): per-step task / aux loss
     trajectories with SGD in between (the gradients feed every later step), and
   * the C restatement (oracle/tamoe_oracle.c, layer_step): routing arrays, y_hat, gate and expert gradients.
+Compulsory quota routing (aux kind 2, apply_compulsory_quota trainer.cpp:121-169) is pinned by the trajectories.
 
 The device follows the reference's summation order without FMA, so everything downstream of the softmax agrees
 to the last few ulp (CUDA's exp may differ from glibc's by one ulp): tolerance rel 1e-12, far inside the north
@@ -45,7 +46,7 @@ def run(P, S, d, dout, N, k, cap, kind, cf=1.25, seed=0, sparse_x=False):
     c_hat = ops.target_closed_form(re1_beta(P), N, k, S) if P > 1 else np.full((1, N), float(S * k) / N)
     pen = np.stack([ops.penalty_weights(c_hat[i]) for i in range(P)])
     pol = ops.CapacityPolicy(ops.CapacityMode(cap), cf)
-    got = ops.layer_step_f64(x, y, gates, U, k, pol, c_hat if cap == 3 else None, kind, 1.0,
+    got = ops.layer_step_f64(x, y, gates, U, k, pol, c_hat if (cap == 3 or kind == 2) else None, kind, 1.0,
                              pen if kind == 1 else None)
     o = oracle.orc().layer_step(x, y, gates, U=U, k=k, cap_mode=cap, cf=cf, c_hat=c_hat, aux_kind=kind,
                                 penalties=pen, act=0, want_dx=False)
@@ -87,7 +88,7 @@ def test_layer_step_f64_cases(P, S, d, dout, N, k, cap, kind, sparse):
 
 
 @pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built")
-@pytest.mark.parametrize("kind,cap,k", [(1, 3, 2), (0, 0, 2), (0, 2, 1)])
+@pytest.mark.parametrize("kind,cap,k", [(1, 3, 2), (0, 0, 2), (0, 2, 1), (2, 2, 1)])
 def test_c1_trajectory_vs_reference_train(kind, cap, k):
     """The reference's own train() (compiled from its sources) vs train_f64 on the device, C1 shape: the SGD
     updates make every step depend on all of the previous step's gradients."""
@@ -97,9 +98,9 @@ def test_c1_trajectory_vs_reference_train(kind, cap, k):
     c_hat = ops.target_closed_form(re1_beta(P), N, k, S)
     pen = np.stack([ops.penalty_weights(c_hat[i]) for i in range(P)])
     ref = oracle.ref().train(x, y, gates, U, kind=kind, cap_mode=cap, cf=1.25,
-                             c_hat=c_hat if kind == 1 else None, lr=lr, steps=steps, k=k)
+                             c_hat=c_hat if kind != 0 else None, lr=lr, steps=steps, k=k)
     got = ops.train_f64(x, y, gates, U, k, steps, lr, ops.CapacityPolicy(ops.CapacityMode(cap), 1.25),
-                        c_hat if cap == 3 else None, kind, 1.0, pen if kind == 1 else None)
+                        c_hat if kind != 0 else None, kind, 1.0, pen if kind == 1 else None)
     np.testing.assert_allclose(got["task_loss"], ref["task_loss"], rtol=1e-11)
     np.testing.assert_allclose(got["aux_loss"], ref["aux_loss"], rtol=1e-11)
     assert got["task_loss"][-1] < got["task_loss"][0]
@@ -109,7 +110,11 @@ def test_layer_step_f64_validation():
     from paper_2302_09915_b200 import ops, _lib
     x, y, gates, U = inputs(1, 32, 16, 16, 4)
     with pytest.raises(_lib.ValidationError):
-        ops.layer_step_f64(x, y, gates, U, 1, aux_kind=2)  # compulsory needs the quota path
+        ops.layer_step_f64(x, y, gates, U, 1, aux_kind=2)  # compulsory without a target pattern
+    with pytest.raises(_lib.ValidationError):
+        ops.layer_step_f64(x, y, gates, U, 2, c_hat=np.ones((1, 4)), aux_kind=2)  # compulsory is top-1 only
+    with pytest.raises(_lib.ValidationError):
+        ops.layer_step_f64(x, y, gates, U, 1, aux_kind=3)
     with pytest.raises(_lib.ValidationError):
         ops.layer_step_f64(x, y, gates, U, 1, aux_kind=1)  # topo without penalties
     bad = gates.copy()
