@@ -236,12 +236,32 @@ def run_reference_arm(args, rank, world):
             "cpu_baseline": {"value": r["value"], "unit": r["unit"], "cores": r["cores"], "kind": r["kind"],
                              "sample": r["sample"]},
             "e2e": {"value": r["value"], "unit": r["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ------------------------------------------------------------------------------------------ our arm
+_REAL_STDOUT = None
+
+
+def hold_stdout():
+    """Native libraries (NCCL's version banner, CUDA / driver messages) write to fd 1 directly; the contract is
+    ONE JSON line on stdout, so fd 1 points at stderr until emit() restores it for that line."""
+    global _REAL_STDOUT
+    sys.stdout.flush()
+    _REAL_STDOUT = os.dup(1)
+    os.dup2(2, 1)
+
+
+def emit(line):
+    sys.stdout.flush()
+    if _REAL_STDOUT is not None:
+        os.dup2(_REAL_STDOUT, 1)
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
+    hold_stdout()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -457,7 +477,7 @@ def main():
                 "roofline": roof, "all_to_all": a2a, "phases_ms": phases, "timed_steps_for_phases": tsteps,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": layer.launches_per_step() * args.steps,
                 "clocks": clocks, "losses_last_step": losses}
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

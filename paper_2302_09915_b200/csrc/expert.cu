@@ -133,6 +133,7 @@ struct EpiSwap {
     }
     ptx::tmem_ld_wait();
     release();
+    if constexpr (V == 4) return;  // experiment: accumulator drained, nothing stored (epilogue-cost probe)
     __nv_bfloat16* st_out = reinterpret_cast<__nv_bfloat16*>(wsm);
     __nv_bfloat16* extra = reinterpret_cast<__nv_bfloat16*>(wsm + (V == 1 ? 2 : 1) * kChunk);  // act' ring (V1 / V2)
     const int mcol = ti.m0 + q * 32;
@@ -359,6 +360,8 @@ void grouped_fwd(const __nv_bfloat16* tokens, const __nv_bfloat16* w, int G, int
   if (push) {
     ep.push = *push;
     launch_pair_or_single<kModeSwap, 256, false, false, EpiSwap<3>>(pair, ta, tb, p, ep, s);
+  } else if (env_int("TAMOE_EPI_DISCARD", 0)) {
+    launch_pair_or_single<kModeSwap, 256, false, false, EpiSwap<4>>(pair, ta, tb, p, ep, s);
   } else if (pre_out) {
     launch_pair_or_single<kModeSwap, 256, false, false, EpiSwap<1>>(pair, ta, tb, p, ep, s);
   } else {
