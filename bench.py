@@ -24,6 +24,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "MoE-layer tokens/sec (fwd+bwd)"
+A2A_CEILING_GBS = 587.0  # best concurrent 4-GPU all-to-all measured on this pool (scripts/p2p_bench.cu)
 C2 = dict(S=16384, d=1024, d_out=1024, f=4096, N=64, k=1)
 # BASELINE configs timed by bench.py: c2 (default, the headline) and c4 (large layer, proportional capacity)
 CONFIGS = {
@@ -358,13 +359,16 @@ def main():
                "dispatch_ms": disp_ms, "combine_ms": comb_ms,
                "dispatch_bus_gbs": nbytes[0] / (disp_ms / 1e3) / 1e9 if disp_ms > 0 else 0.0,
                "combine_bus_gbs": nbytes[2] / (comb_ms / 1e3) / 1e9 if comb_ms > 0 else 0.0,
-               "peak_gbs": 900.0, "measured_peer_peak_gbs": 690.0, "measured_a2a_gbs": 533.0,
+               "peak_gbs": 900.0, "measured_peer_peak_gbs": 698.0, "measured_a2a_gbs": A2A_CEILING_GBS,
                "note": "all payload moves as NVLink peer stores fused into compute kernels: dispatch (permute kernel "
                        "-> owner's layout), O return (owner's fwd2 epilogue -> home rank), dO (combine kernel -> "
                        "owner), dX return (owner's dgrad1 epilogue -> home rank); bus GB/s = off-rank bytes / phase "
-                       "time (CUDA events, "
-                       "incl. the stream-ordered NCCL barrier); measured peaks: profiles/r01_p2p_bench.txt "
-                       "(single-pair SM pull 690 GB/s, 4-GPU all-to-all SM stores 533 GB/s per GPU)"}
+                       "time (CUDA events, incl. the phase's device barrier); peaks: NVLink 5 nominal 900 GB/s per "
+                       "direction; measured on this pool (profiles/r01_p2p_bench.txt): single pair 698 GB/s, best "
+                       "4-GPU all-to-all of any engine (SM stores, TMA bulk, pulls, copy engines) 587 GB/s per GPU"}
+        for kk in ("dispatch", "combine"):
+            a2a[kk + "_frac_of_nvlink_peak"] = a2a[kk + "_bus_gbs"] / 900.0
+            a2a[kk + "_frac_of_measured_a2a"] = a2a[kk + "_bus_gbs"] / A2A_CEILING_GBS
     losses = layer.losses.cpu().tolist()
     value = world * S / (ms / 1e3)
 

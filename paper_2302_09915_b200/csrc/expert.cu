@@ -78,7 +78,24 @@ struct SwapParams {
 
 // V = 0: plain store; 1: store act(x) and the activation derivative act'(x) (kept for the backward in
 // place of the pre-activation); 2: multiply by the stored act'(x); 3: plain, each row stored into its
-// home rank over NVLink (16-byte peer stores from the staging tile, 4 per lane and chunk).
+// home rank over NVLink (16-byte peer stores from the staging tile, 4 per lane and chunk); 4: experiment only
+// (drain TMEM, store nothing).
+//
+// The transpose (accumulator rows = features, output rows = tokens) is done by the shared-memory store: the
+// accumulator is read from TMEM in the mma fragment layout (tcgen05.ld 16x256b) and written with
+// stmatrix.trans, four 8x8 tiles per instruction, into a staging tile [32 tokens][32 features] whose 16-byte
+// pieces are XOR-swizzled by (token >> 1) & 3 -- the TMA 64-byte swizzle of the store maps, which makes the
+// stmatrix rows (64 B apart) bank-conflict free.
+__device__ __forceinline__ int swz64(int row, int piece) { return row * 32 + ((piece ^ ((row >> 1) & 3)) << 3); }
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ float2 unpack_bf16x2(uint32_t v) {
+  return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&v));
+}
+
 template <int V>
 struct EpiSwap {
   static constexpr int kChunk = 2048;  // 32 x 32 bf16
@@ -101,7 +118,7 @@ struct EpiSwap {
         const bool ok = ch * 32 + r < ti.n;
         const __nv_bfloat16* src =
             e.pre_in + static_cast<long long>(row0 + ch * 32 + (ok ? r : 0)) * e.ld + mcol + part * 8;
-        ptx::cp_async_16(slot + r * 32 + part * 8, src, ok);
+        ptx::cp_async_16(slot + swz64(r, part), src, ok);
       }
     }
     ptx::cp_async_commit();  // uniform group count, even when empty
@@ -119,16 +136,20 @@ struct EpiSwap {
   static __device__ __forceinline__ void run(const Params& e, const GemmParams&, const TileInfo& ti,
                                              uint32_t tmem_tile, int q, int h, int lane, uint8_t* wsm,
                                              const int* s_start, Release&& release) {
-    // copy this warp's share of the accumulator to registers and hand TMEM back to the MMA at once
+    // copy this warp's share of the accumulator to registers (fragment layout: acc[j][16 hh + 4 k + 2 rg + b] =
+    // feature 16 hh + 8 rg + lane / 4, token 32 ch + 8 k + 2 (lane % 4) + b) and hand TMEM back at once
     const int nch_all = (ti.n + 31) / 32;
-    float acc[kMaxCh][32];
+    uint32_t acc[kMaxCh][32];
 #pragma unroll
     for (int j = 0; j < kMaxCh; ++j) {
       if (h + 2 * j < nch_all) {
-        uint32_t r[32];
-        ptx::tmem_ld_32x32b_x32(tmem_tile + (h + 2 * j) * 32, r);
+        uint32_t r[16];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) acc[j][i] = __uint_as_float(r[i]);
+        for (int hh = 0; hh < 2; ++hh) {
+          ptx::tmem_ld_16x256b_x4(tmem_tile + (static_cast<uint32_t>(16 * hh) << 16) + (h + 2 * j) * 32, r);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[j][16 * hh + i] = r[i];
+        }
       }
     }
     ptx::tmem_ld_wait();
@@ -139,6 +160,8 @@ struct EpiSwap {
     const int mcol = ti.m0 + q * 32;
     const int row0 = s_start[ti.g] + ti.n0;
     const int nch = (ti.n + 31) / 32;
+    // this lane's stmatrix / ldmatrix row: token 8k + (lane % 8) of matrix (feature block) lane / 8
+    const int srow = lane & 7, spiece = lane >> 3;
     if (lane == 0) ptx::bulk_wait_read<0>();  // staging tiles free again
     __syncwarp();
 #pragma unroll
@@ -149,7 +172,6 @@ struct EpiSwap {
         ptx::cp_async_wait<kPf - 1>();
         __syncwarp();
       }
-      const float* v = acc[j];
       if (kRing ? j >= 2 : j >= 1) {  // the slot's previous TMA store has read it
         if (lane == 0) {
           if constexpr (kRing) ptx::bulk_wait_read<1>();
@@ -159,19 +181,31 @@ struct EpiSwap {
       }
       __nv_bfloat16* so = st_out + (kRing ? (j & 1) * 1024 : 0);
       __nv_bfloat16* sx = extra + (j & 1) * 1024;
+      const uint32_t so_u = ptx::smem_u32(so), sx_u = ptx::smem_u32(sx);
 #pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        const float x = v[c];
-        if constexpr (V == 1) {
-          float y, dy;
-          act_both(e.act_out, x, y, dy);
-          sx[c * 32 + lane] = __float2bfloat16(dy);
-          so[c * 32 + lane] = __float2bfloat16(y);
-        } else if constexpr (V == 2) {
-          so[c * 32 + lane] = __float2bfloat16(x * __bfloat162float(sx[c * 32 + lane]));
-        } else {  // V = 0 / 3
-          so[c * 32 + lane] = __float2bfloat16(act_fwd(e.act_out, x));
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t off = static_cast<uint32_t>(swz64(8 * k + srow, spiece)) * 2;
+        uint32_t o[4], dy[4];
+        if constexpr (V == 2) ptx::ldmatrix_x4_trans(sx_u + off, dy);
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {  // matrix m = features 8m..8m+7 = (hh, rg) = (m >> 1, m & 1)
+          const float x0 = __uint_as_float(acc[j][16 * (m >> 1) + 4 * k + 2 * (m & 1)]);
+          const float x1 = __uint_as_float(acc[j][16 * (m >> 1) + 4 * k + 2 * (m & 1) + 1]);
+          if constexpr (V == 1) {
+            float y0, y1, d0, d1;
+            act_both(e.act_out, x0, y0, d0);
+            act_both(e.act_out, x1, y1, d1);
+            o[m] = pack_bf16x2(y0, y1);
+            dy[m] = pack_bf16x2(d0, d1);
+          } else if constexpr (V == 2) {
+            const float2 g = unpack_bf16x2(dy[m]);
+            o[m] = pack_bf16x2(x0 * g.x, x1 * g.y);
+          } else {  // V = 0 / 3
+            o[m] = pack_bf16x2(act_fwd(e.act_out, x0), act_fwd(e.act_out, x1));
+          }
         }
+        ptx::stmatrix_x4_trans(so_u + off, o[0], o[1], o[2], o[3]);
+        if constexpr (V == 1) ptx::stmatrix_x4_trans(sx_u + off, dy[0], dy[1], dy[2], dy[3]);
       }
       if constexpr (V == 3) {
         __syncwarp();
@@ -182,7 +216,7 @@ struct EpiSwap {
           const int r = (lane >> 2) + 8 * i;
           if (r < rows) {
             const int code = __ldg(e.push.row_code + y + r);
-            const uint4 v = *reinterpret_cast<const uint4*>(so + r * 32 + (lane & 3) * 8);
+            const uint4 v = *reinterpret_cast<const uint4*>(so + swz64(r, lane & 3));
             __nv_bfloat16* dst = e.push.dst.p[code >> kPushRowBits] +
                                  static_cast<long long>(code & ((1 << kPushRowBits) - 1)) * e.ld + mcol + (lane & 3) * 8;
             *reinterpret_cast<uint4*>(dst) = v;
@@ -319,11 +353,12 @@ static uint32_t swap_token_box(int cg) { return cg == 4 ? 64 : (cg == 2 ? 128 : 
 static SwapParams swap_params(__nv_bfloat16* out, __nv_bfloat16* pre_out, const __nv_bfloat16* pre_in, int M,
                               int R, int act_out, int act_grad) {
   SwapParams e;
-  e.out32 = make_tmap_bf16_box(out, M, R, M, 32, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
-  e.out16 = make_tmap_bf16_box(out, M, R, M, 32, 16, CU_TENSOR_MAP_SWIZZLE_NONE);
+  // staging tiles are 64-byte swizzled (EpiSwap: conflict-free stmatrix rows)
+  e.out32 = make_tmap_bf16_box(out, M, R, M, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+  e.out16 = make_tmap_bf16_box(out, M, R, M, 32, 16, CU_TENSOR_MAP_SWIZZLE_64B);
   if (pre_out) {
-    e.pre32 = make_tmap_bf16_box(pre_out, M, R, M, 32, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
-    e.pre16 = make_tmap_bf16_box(pre_out, M, R, M, 32, 16, CU_TENSOR_MAP_SWIZZLE_NONE);
+    e.pre32 = make_tmap_bf16_box(pre_out, M, R, M, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+    e.pre16 = make_tmap_bf16_box(pre_out, M, R, M, 32, 16, CU_TENSOR_MAP_SWIZZLE_64B);
   } else {
     e.pre32 = e.out32;
     e.pre16 = e.out16;
