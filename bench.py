@@ -322,10 +322,15 @@ def main():
     for _ in range(args.warmup):
         layer.step(x, y, params)
     torch.cuda.synchronize()
+    # NVML set-up and events before the barrier: any host work between the barrier and the first timed launch
+    # on one rank is time the other ranks' GPUs spend in the step's device barrier (max over ranks)
+    clk = ClockSampler(local)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with clk:
+        # one untimed step enqueued ahead of ev0: its device barriers re-align the ranks' GPUs after any host skew
+        layer.step(x, y, params)
         ev0.record(stream)
         for _ in range(args.steps):
             layer.step(x, y, params)
