@@ -244,7 +244,8 @@ int tamoe_layer_create(const tamoe_layer_config* cfg, const double* c_hat, tamoe
  * (dispatch), the owners' fwd2 / dgrad1 GEMM epilogues store expert outputs / input gradients back into the
  * tokens' home ranks, the combine kernel stores dO into the owners; phases are ordered by a device-side
  * barrier over the mapped workspaces that also carries the counts all-gather (NCCL is used at setup only).
- * Capacities are rank-local (local / proportional, gate.cpp:165-180).  tamoe_nccl_unique_id fills 128 bytes on one rank; broadcast them to all ranks, then
+ * Local / proportional capacities are rank-local (gate.cpp:165-180); global capacity across ranks adds a picks
+ * exchange into every rank's global view (gate.cpp:157-164).  tamoe_nccl_unique_id fills 128 bytes on one rank; broadcast them to all ranks, then
  * every rank calls tamoe_layer_create_ep with its cfg.rank / cfg.world_size. */
 int tamoe_nccl_unique_id(void* out128);
 int tamoe_layer_create_ep(const tamoe_layer_config* cfg, const double* c_hat, const void* nccl_id128,
