@@ -136,3 +136,17 @@ def test_link_emulation_validation():
         ops.set_link_emulation(2, 0)
     with pytest.raises(ops.ValidationError):
         ops.set_link_emulation(-1, 2)
+
+
+def test_reference_precision_entry_points_validate_before_touching_the_device():
+    """tamoe_layer_step_f64 / tamoe_train_f64 (BASELINE C1 in fp64, the drop-in train()) reject malformed calls
+    with status 2 on the host, as the reference throws ValidationError (no GPU needed for these checks)."""
+    from paper_2302_09915_b200 import _lib
+    L = _lib.lib
+    L.tamoe_layer_step_f64.restype = ctypes.c_int
+    assert L.tamoe_layer_step_f64(None, 4, 4, None, None, None, None, None, None, 0, ctypes.c_double(1.0), 0,
+                                  None, None, None, None, None, None, None) == 2
+    assert b"null router" in L.tamoe_last_error()
+    L.tamoe_train_f64.restype = ctypes.c_int
+    assert L.tamoe_train_f64(None, None, None, None, None, None, None, None, None) == 2
+    assert b"null argument" in L.tamoe_last_error()
