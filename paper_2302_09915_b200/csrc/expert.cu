@@ -78,8 +78,7 @@ struct SwapParams {
 
 // V = 0: plain store; 1: store act(x) and the activation derivative act'(x) (kept for the backward in
 // place of the pre-activation); 2: multiply by the stored act'(x); 3: plain, each row stored into its
-// home rank over NVLink (16-byte peer stores from the staging tile, 4 per lane and chunk); 4: experiment only
-// (drain TMEM, store nothing).
+// home rank over NVLink (16-byte peer stores from the staging tile, 4 per lane and chunk).
 //
 // The transpose (accumulator rows = features, output rows = tokens) is done by the shared-memory store: the
 // accumulator is read from TMEM in the mma fragment layout (tcgen05.ld 16x256b) and written with
@@ -154,7 +153,6 @@ struct EpiSwap {
     }
     ptx::tmem_ld_wait();
     release();
-    if constexpr (V == 4) return;  // experiment: accumulator drained, nothing stored (epilogue-cost probe)
     __nv_bfloat16* st_out = reinterpret_cast<__nv_bfloat16*>(wsm);
     __nv_bfloat16* extra = reinterpret_cast<__nv_bfloat16*>(wsm + (V == 1 ? 2 : 1) * kChunk);  // act' ring (V1 / V2)
     const int mcol = ti.m0 + q * 32;
@@ -375,6 +373,16 @@ static int env_int(const char* name, int dflt) {
   return v ? std::atoi(v) : dflt;
 }
 
+// L2 prefetch distance of the swap GEMMs' operands (TAMOE_PF_DIST / TAMOE_PF_B; off by default), read once
+static int pf_dist() {
+  static const int v = env_int("TAMOE_PF_DIST", 0);
+  return v;
+}
+static int pf_b() {
+  static const int v = env_int("TAMOE_PF_B", 0);
+  return v;
+}
+
 static void check_groups(int G) { require(G >= 1 && G <= kMaxGroups, "group count out of range [1, 1024]"); }
 
 
@@ -388,15 +396,12 @@ void grouped_fwd(const __nv_bfloat16* tokens, const __nv_bfloat16* w, int G, int
   const int Gw = w_mod > 0 ? w_mod : G;  // distinct weight matrices
   CUtensorMap ta = make_tmap_bf16(w, K, static_cast<uint64_t>(Gw) * M, K, kBM);
   CUtensorMap tb = make_tmap_bf16(tokens, K, R, K, swap_token_box(pair));
-  GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1, w_mod, 1, env_int("TAMOE_PF_DIST", 0),
-               env_int("TAMOE_PF_B", 0)};
+  GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1, w_mod, 1, pf_dist(), pf_b()};
   SwapParams ep = swap_params(out, pre_out, nullptr, M, R, act, kActNone);
   require(!(push && pre_out), "grouped_fwd: push needs a plain output");
   if (push) {
     ep.push = *push;
     launch_pair_or_single<kModeSwap, 256, false, false, EpiSwap<3>>(pair, ta, tb, p, ep, s);
-  } else if (env_int("TAMOE_EPI_DISCARD", 0)) {
-    launch_pair_or_single<kModeSwap, 256, false, false, EpiSwap<4>>(pair, ta, tb, p, ep, s);
   } else if (pre_out) {
     launch_pair_or_single<kModeSwap, 256, false, false, EpiSwap<1>>(pair, ta, tb, p, ep, s);
   } else {
@@ -415,8 +420,7 @@ void grouped_dgrad(const __nv_bfloat16* grad_tokens, const __nv_bfloat16* w, int
   const int Gw = w_mod > 0 ? w_mod : G;
   CUtensorMap ta = make_tmap_bf16(w, M, static_cast<uint64_t>(Gw) * K, M, 64);
   CUtensorMap tb = make_tmap_bf16(grad_tokens, K, R, K, swap_token_box(pair));
-  GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1, w_mod, 1, env_int("TAMOE_PF_DIST", 0),
-               env_int("TAMOE_PF_B", 0)};
+  GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1, w_mod, 1, pf_dist(), pf_b()};
   SwapParams ep = swap_params(out, nullptr, pre_in, M, R, kActNone, pre_in ? act : kActNone);
   require(!(push && pre_in), "grouped_dgrad: push needs a plain output");
   if (push) {
