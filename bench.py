@@ -146,6 +146,34 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------ CPU baseline
+def host_threads(bytes_per_thread=1.6e9):
+    """The host cores this process may use (up to 64), bounded by memory: each concurrent reference train() at the C2
+    shape holds ~1.6 GB (its copies of the 64 fp64 expert maps and their gradients), and the arm must not drive
+    the box out of memory -- at most 40 % of MemAvailable / the cgroup headroom."""
+    ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    avail = None
+    try:
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemAvailable:"):
+                    avail = int(ln.split()[1]) * 1024
+    except OSError:
+        pass
+    try:
+        with open("/sys/fs/cgroup/memory.max") as f:
+            lim = f.read().strip()
+        if lim != "max":
+            with open("/sys/fs/cgroup/memory.current") as f:
+                head = int(lim) - int(f.read().strip())
+            avail = head if avail is None else min(avail, head)
+    except (OSError, ValueError):
+        pass
+    if avail is None:
+        return min(ncpu, 16)
+    # capped at 64 threads so the arm's K-step run stays within a few minutes on many-core hosts
+    return max(1, min(ncpu, 64, int(0.4 * avail / bytes_per_thread)))
+
+
 def reference_cpu(tokens_per_thread=256, threads=None, steps=1, seed=0):
     """The reference's own train() step (compiled from its sources, oracle/_ref) at the C2 router/expert
     shape (d=1024, N=64, top-1; the reference expert is a linear d->d map, trainer.cpp:284-289),
@@ -153,7 +181,7 @@ def reference_cpu(tokens_per_thread=256, threads=None, steps=1, seed=0):
     C restatement (oracle port) when oracle/_ref is absent."""
     import numpy as np
     import oracle
-    threads = threads or min(os.cpu_count() or 1, 16)
+    threads = threads or host_threads()
     d, N, k = C2["d"], C2["N"], C2["k"]
     rng = np.random.default_rng(seed)
     U = rng.normal(size=(N, d, d)) / np.sqrt(d)
