@@ -39,7 +39,7 @@ CONFIGS = {
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--tokens", type=int, default=None, help="tokens per GPU (default: the config's)")
@@ -113,15 +113,24 @@ class ClockSampler:
         except Exception as e:  # no NVML: reported, not fatal
             self.err = f"nvml unavailable: {e}"
 
-    def _sample(self):
+    def sample_now(self):
+        """One synchronous sample from the launching thread (taken while queued steps still run on the GPU), so a
+        short timed region has samples even when the sampler thread is starved of the GIL."""
+        if self.h is None:
+            return True
         nv = self.nv
         reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
             nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        try:
+            self.rows.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM), reasons(self.h)))
+            return True
+        except Exception as e:
+            self.err = str(e)
+            return False
+
+    def _sample(self):
         while not self.stop.is_set():
-            try:
-                self.rows.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM), reasons(self.h)))
-            except Exception as e:
-                self.err = str(e)
+            if not self.sample_now():
                 return
             time.sleep(self.period)
 
@@ -257,7 +266,7 @@ def workload_config(S, world, name="c2"):
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return
-    r = reference_cpu(steps=max(1, args.steps), tokens_per_thread=64)
+    r = reference_cpu(steps=max(1, min(args.steps, 10)), tokens_per_thread=64)  # bounded: a few minutes at most
     line = {"metric": METRIC, "value": r["value"], "unit": r["unit"], "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -360,9 +369,12 @@ def main():
         # one untimed step enqueued ahead of ev0: its device barriers re-align the ranks' GPUs after any host skew
         layer.step(x, y, params)
         ev0.record(stream)
-        for _ in range(args.steps):
+        for i in range(args.steps):
             layer.step(x, y, params)
+            if i == args.steps // 2:
+                clk.sample_now()
         ev1.record(stream)
+        clk.sample_now()
         torch.cuda.synchronize()
     barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
