@@ -16,7 +16,7 @@ namespace tamoe {
 
 namespace {
 
-constexpr int kCombWarps = 8;
+constexpr int kCombWarps = 4;
 
 __device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
   const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
