@@ -94,6 +94,16 @@ int tamoe_smooth_profile(const int* levels, int n_levels, const double* alpha, c
 int tamoe_p2p_sweep(const void* nccl_id128, int world, int rank, const double* sizes_mb, int nsizes, int reps,
                     int warmup, double* time_us);
 
+/* The same sweep with the external (NCCL-free) bootstrap of tamoe_layer_create_ep_begin: create, exchange
+ * the blobs, connect, sweep.  time_us is filled for the rows this rank timed (src == rank), zero elsewhere:
+ * the caller sums the ranks' arrays. */
+typedef struct tamoe_p2p_probe tamoe_p2p_probe;
+int tamoe_p2p_probe_create(int world, int rank, double max_mb, tamoe_p2p_probe** out, void* blob_out);
+int tamoe_p2p_probe_connect(tamoe_p2p_probe* p, const void* blobs, int world);
+int tamoe_p2p_probe_sweep(tamoe_p2p_probe* p, const double* sizes_mb, int nsizes, int reps, int warmup,
+                          double* time_us);
+int tamoe_p2p_probe_destroy(tamoe_p2p_probe* p);
+
 /* Heterogeneous-topology emulation (BASELINE config 5): ranks in different groups of `group_size` consecutive
  * ranks exchange over a link throttled `repeat` times -- every payload store to such a peer (dispatch, expert
  * output return, dO, dX return, and the p2p sweep's copies) is issued `repeat` times, so the link delivers
@@ -250,6 +260,17 @@ int tamoe_layer_create(const tamoe_layer_config* cfg, const double* c_hat, tamoe
 int tamoe_nccl_unique_id(void* out128);
 int tamoe_layer_create_ep(const tamoe_layer_config* cfg, const double* c_hat, const void* nccl_id128,
                           tamoe_layer** out);
+
+/* Expert parallelism without NCCL (ranks may share a device: several ranks per GPU emulate a larger world).
+ * Phase 1 creates this rank's layer and writes its TAMOE_EP_BLOB_BYTES blob (the CUDA IPC handle of its
+ * workspace plus a fingerprint of the configuration / layout); the caller exchanges the blobs with any
+ * transport (TCP store, MPI, gloo all-gather); phase 2 hands every rank's blob (world x 128 bytes, in rank
+ * order) back and maps the peers.  A rank created with a different configuration is a validation error.
+ * tamoe_layer_create_ep performs both phases over NCCL. */
+#define TAMOE_EP_BLOB_BYTES 128
+int tamoe_layer_create_ep_begin(const tamoe_layer_config* cfg, const double* c_hat, tamoe_layer** out,
+                                void* blob_out);
+int tamoe_layer_ep_connect(tamoe_layer* l, const void* blobs);
 /* Off-rank payload bytes of the last step: out[4] = dispatch, expert-output return, dO, dX return. */
 int tamoe_layer_a2a_bytes(tamoe_layer* l, long long* out4);
 /* Host-side receive plan (CPU-testable): recv[P x E] rows per (source rank, local expert) -> the receive
@@ -301,7 +322,14 @@ int tamoe_train(const tamoe_layer_config* cfg, const double* c_hat, const tamoe_
 int tamoe_train_f64(const tamoe_layer_config* cfg, const double* c_hat, const tamoe_train_opts* opts,
                     const double* x, const double* y, double* gates, double* experts, tamoe_train_report* report,
                     void* stream);
+/* One layer step, stream-ordered, no host synchronisation.  A non-finite gate logit (the reference's
+ * ValidationError, gate.cpp:16-17) cannot be reported by the call that enqueues the step: the device router
+ * routes such a token to experts 0..k-1 with NaN gate values (indices stay in range, outputs and losses come
+ * out NaN) and raises a flag that the next tamoe_layer_step (once the earlier step has completed) or
+ * tamoe_layer_status returns as status 2. */
 int tamoe_layer_step(tamoe_layer* l, const tamoe_layer_io* io, void* stream);
+/* Waits for the last step; status 2 ("non-finite gate logit") if it saw a non-finite logit (reported once). */
+int tamoe_layer_status(tamoe_layer* l);
 int tamoe_layer_read(tamoe_layer* l, int what, void* dst, long long bytes, void* stream);
 int tamoe_layer_n_pad(int N);
 /* Kernel launches of libtamoe per step (memsets excluded). */

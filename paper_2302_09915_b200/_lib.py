@@ -51,6 +51,10 @@ SIGNATURES = {
     "tamoe_exchange_cost": [_D, _D, _D, c_int, c_int, c_int, c_int, c_int, _D, _D],
     "tamoe_p2p_sweep": [_P, c_int, c_int, _D, c_int, c_int, c_int, _D],
     "tamoe_set_link_emulation": [c_int, c_int],
+    "tamoe_p2p_probe_create": [c_int, c_int, c_double, POINTER(c_void_p), _P],
+    "tamoe_p2p_probe_connect": [_P, _P, c_int],
+    "tamoe_p2p_probe_sweep": [_P, _D, c_int, c_int, c_int, _D],
+    "tamoe_p2p_probe_destroy": [_P],
     "tamoe_grouped_fwd": [_P, _P, c_int, c_int, c_int, c_int, _P, _P, _P, _P, c_int, _P],
     "tamoe_grouped_dgrad": [_P, _P, c_int, c_int, c_int, c_int, _P, _P, _P, _P, c_int, _P],
     "tamoe_grouped_wgrad": [_P, _P, c_int, c_int, c_int, c_int, _P, _P, _P, _P],

@@ -31,6 +31,10 @@ struct tamoe_layer {
   tamoe_layer(const LayerConfig& c, const double* ch, std::unique_ptr<EpComm> ep = nullptr)
       : impl(c, ch, std::move(ep)) {}
 };
+struct tamoe_p2p_probe {
+  P2PProbe impl;
+  tamoe_p2p_probe(std::unique_ptr<EpComm> c, size_t bytes) : impl(std::move(c), bytes) {}
+};
 
 namespace {
 
@@ -447,7 +451,8 @@ int tamoe_p2p_sweep(const void* nccl_id128, int world, int rank, const double* s
     std::memcpy(&id, nccl_id128, sizeof(id));
     double max_mb = 0.0;
     for (int i = 0; i < nsizes; ++i) max_mb = std::max(max_mb, sizes_mb[i]);
-    P2PProbe probe(world, rank, id, (static_cast<size_t>(max_mb * 1e6) + 4095) & ~static_cast<size_t>(4095));
+    P2PProbe probe(std::make_unique<EpComm>(world, rank, id),
+                   (static_cast<size_t>(max_mb * 1e6) + 4095) & ~static_cast<size_t>(4095));
     const std::vector<double> t = probe.sweep(sizes_mb, nsizes, reps, warmup);
     std::memcpy(time_us, t.data(), sizeof(double) * t.size());
   });
@@ -486,6 +491,63 @@ int tamoe_layer_create_ep(const tamoe_layer_config* cfg, const double* c_hat, co
   });
 }
 
+int tamoe_layer_create_ep_begin(const tamoe_layer_config* cfg, const double* c_hat, tamoe_layer** out,
+                                void* blob_out) {
+  return guarded([&] {
+    require(cfg && out && blob_out, "layer_create_ep_begin: null argument");
+    LayerConfig c{cfg->P, cfg->S, cfg->d, cfg->d_out, cfg->N, cfg->k, cfg->f, cfg->act, cfg->cap_mode,
+                  cfg->capacity_factor, cfg->aux_kind, cfg->aux_weight, cfg->penalty_norm, cfg->temperature,
+                  cfg->need_dx, cfg->world_size, cfg->rank};
+    auto l = std::make_unique<tamoe_layer>(c, c_hat, std::make_unique<EpComm>(c.world_size, c.rank));
+    const PeerBlob b = l->impl.blob();
+    std::memcpy(blob_out, &b, sizeof(b));
+    *out = l.release();
+  });
+}
+
+int tamoe_layer_ep_connect(tamoe_layer* l, const void* blobs) {
+  return guarded([&] {
+    require(l && blobs, "layer_ep_connect: null argument");
+    const int W = l->impl.cfg().world_size;
+    std::vector<PeerBlob> all(static_cast<size_t>(W));
+    std::memcpy(all.data(), blobs, sizeof(PeerBlob) * all.size());
+    l->impl.connect(all.data());
+  });
+}
+
+int tamoe_p2p_probe_create(int world, int rank, double max_mb, tamoe_p2p_probe** out, void* blob_out) {
+  return guarded([&] {
+    require(out && blob_out && max_mb > 0.0, "p2p_probe_create: bad argument");
+    auto p = std::make_unique<tamoe_p2p_probe>(std::make_unique<EpComm>(world, rank),
+                                               (static_cast<size_t>(max_mb * 1e6) + 4095) & ~static_cast<size_t>(4095));
+    const PeerBlob b = p->impl.blob();
+    std::memcpy(blob_out, &b, sizeof(b));
+    *out = p.release();
+  });
+}
+
+int tamoe_p2p_probe_connect(tamoe_p2p_probe* p, const void* blobs, int world) {
+  return guarded([&] {
+    require(p && blobs && world >= 1 && world <= kMaxRanks, "p2p_probe_connect: bad argument");
+    std::vector<PeerBlob> all(static_cast<size_t>(world));
+    std::memcpy(all.data(), blobs, sizeof(PeerBlob) * all.size());
+    p->impl.connect(all.data());
+  });
+}
+
+int tamoe_p2p_probe_sweep(tamoe_p2p_probe* p, const double* sizes_mb, int nsizes, int reps, int warmup,
+                          double* time_us) {
+  return guarded([&] {
+    require(p && sizes_mb && time_us, "p2p_probe_sweep: null argument");
+    const std::vector<double> t = p->impl.sweep(sizes_mb, nsizes, reps, warmup);
+    std::memcpy(time_us, t.data(), sizeof(double) * t.size());
+  });
+}
+
+int tamoe_p2p_probe_destroy(tamoe_p2p_probe* p) {
+  return guarded([&] { delete p; });
+}
+
 int tamoe_layer_a2a_bytes(tamoe_layer* l, long long* out4) {
   return guarded([&] {
     require(l && out4, "a2a_bytes: null argument");
@@ -513,6 +575,13 @@ int tamoe_layer_step(tamoe_layer* l, const tamoe_layer_io* io, void* stream) {
               static_cast<__nv_bfloat16*>(io->dw2), static_cast<__nv_bfloat16*>(io->dx),
               static_cast<__nv_bfloat16*>(io->y_hat), io->losses};
     l->impl.step(x, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int tamoe_layer_status(tamoe_layer* l) {
+  return guarded([&] {
+    require(l != nullptr, "status: null layer");
+    l->impl.status();
   });
 }
 

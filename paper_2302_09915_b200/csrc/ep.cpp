@@ -1,5 +1,7 @@
 #include "ep.hpp"
 
+#include <unistd.h>
+
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -30,6 +32,10 @@ EpComm::EpComm(int world, int rank, const ncclUniqueId& id) : world_(world), ran
   TAMOE_NCCL(ncclCommInitRank(&comm_, world, id, rank));
 }
 
+EpComm::EpComm(int world, int rank) : world_(world), rank_(rank) {
+  require(world >= 1 && world <= kMaxRanks && rank >= 0 && rank < world, "bad expert-parallel world / rank");
+}
+
 EpComm::~EpComm() {
   close_peers();
   if (comm_) ncclCommDestroy(comm_);
@@ -41,69 +47,128 @@ void EpComm::close_peers() {
 }
 
 void EpComm::allgather_counts(const int* my_counts, int* all_counts, int N, cudaStream_t s) {
+  require(comm_ != nullptr, "NCCL barriers need the NCCL bootstrap (tamoe_layer_create_ep)");
   TAMOE_NCCL(ncclAllGather(my_counts, all_counts, N, ncclInt32, comm_, s));
 }
 
 void EpComm::barrier(int* flag, cudaStream_t s) {
+  require(comm_ != nullptr, "NCCL barriers need the NCCL bootstrap (tamoe_layer_create_ep)");
   TAMOE_NCCL(ncclAllReduce(flag, flag, 1, ncclInt32, ncclSum, comm_, s));
 }
 
 void EpComm::allreduce_sum(double* buf, size_t n, cudaStream_t s) {
+  require(comm_ != nullptr, "NCCL all-reduce needs the NCCL bootstrap");
   TAMOE_NCCL(ncclAllReduce(buf, buf, n, ncclFloat64, ncclSum, comm_, s));
 }
 
-void EpComm::map_peers(void* local_base, std::vector<char*>& bases) {
-  cudaIpcMemHandle_t h;
-  TAMOE_CUDA(cudaIpcGetMemHandle(&h, local_base));
+PeerBlob EpComm::make_blob(void* local_base, long long bytes, unsigned long long fingerprint) const {
+  PeerBlob b;
+  std::memset(&b, 0, sizeof(b));
+  TAMOE_CUDA(cudaIpcGetMemHandle(&b.handle, local_base));
+  b.bytes = bytes;
+  b.fingerprint = fingerprint;
+  b.world = world_;
+  b.rank = rank_;
+  b.pid = static_cast<int>(getpid());
+  TAMOE_CUDA(cudaGetDevice(&b.device));
+  return b;
+}
+
+std::vector<PeerBlob> EpComm::allgather_blobs(const PeerBlob& mine) {
+  require(comm_ != nullptr, "blob all-gather needs the NCCL bootstrap");
+  const size_t hs = sizeof(PeerBlob);
   char* d_buf = nullptr;
-  const size_t hs = sizeof(cudaIpcMemHandle_t);
   TAMOE_CUDA(cudaMalloc(&d_buf, hs * (world_ + 1)));
-  TAMOE_CUDA(cudaMemcpy(d_buf + hs * world_, &h, hs, cudaMemcpyHostToDevice));
+  TAMOE_CUDA(cudaMemcpy(d_buf + hs * world_, &mine, hs, cudaMemcpyHostToDevice));
   TAMOE_NCCL(ncclAllGather(d_buf + hs * world_, d_buf, hs, ncclChar, comm_, nullptr));
   TAMOE_CUDA(cudaStreamSynchronize(nullptr));
-  std::vector<cudaIpcMemHandle_t> all(world_);
+  std::vector<PeerBlob> all(world_);
   TAMOE_CUDA(cudaMemcpy(all.data(), d_buf, hs * world_, cudaMemcpyDeviceToHost));
   TAMOE_CUDA(cudaFree(d_buf));
+  return all;
+}
+
+void EpComm::open_peers(const PeerBlob* all, void* local_base, std::vector<char*>& bases) {
+  require(opened_.empty(), "expert-parallel peers are already mapped");
+  const PeerBlob& me = all[rank_];
+  for (int j = 0; j < world_; ++j) {
+    const PeerBlob& b = all[j];
+    require(b.world == world_ && b.rank == j,
+            "expert-parallel bootstrap: blob " + std::to_string(j) + " is not rank " + std::to_string(j) + " of " +
+                std::to_string(world_));
+    require(b.bytes == me.bytes && b.fingerprint == me.fingerprint,
+            "expert-parallel bootstrap: rank " + std::to_string(j) +
+                " was created with a different configuration / workspace layout than rank " +
+                std::to_string(rank_));
+  }
   bases.assign(world_, nullptr);
   for (int j = 0; j < world_; ++j) {
     if (j == rank_) {
       bases[j] = static_cast<char*>(local_base);
     } else {
       void* p = nullptr;
-      TAMOE_CUDA(cudaIpcOpenMemHandle(&p, all[j], cudaIpcMemLazyEnablePeerAccess));
+      TAMOE_CUDA(cudaIpcOpenMemHandle(&p, all[j].handle, cudaIpcMemLazyEnablePeerAccess));
       opened_.push_back(p);
       bases[j] = static_cast<char*>(p);
     }
   }
 }
 
-P2PProbe::P2PProbe(int world, int rank, const ncclUniqueId& id, size_t max_bytes)
-    : comm_(world, rank, id), max_bytes_(max_bytes) {
+namespace {
+constexpr size_t kProbeSig = 256;  // signal slots [kMaxRanks] + epoch at the head of the probe buffer
+}
+
+P2PProbe::P2PProbe(std::unique_ptr<EpComm> comm, size_t max_bytes) : comm_(std::move(comm)), max_bytes_(max_bytes) {
   require(max_bytes >= 16, "p2p probe buffer too small");
-  TAMOE_CUDA(cudaMalloc(&buf_, 2 * max_bytes_));
-  TAMOE_CUDA(cudaMemset(buf_, 1, 2 * max_bytes_));
-  TAMOE_CUDA(cudaMalloc(&flag_, sizeof(int)));
+  TAMOE_CUDA(cudaMalloc(&buf_, kProbeSig + 2 * max_bytes_));
+  TAMOE_CUDA(cudaMemset(buf_, 0, kProbeSig));
+  TAMOE_CUDA(cudaMemset(buf_ + kProbeSig, 1, 2 * max_bytes_));
+  TAMOE_CUDA(cudaDeviceSynchronize());  // slots zeroed before any peer can see the handle
   TAMOE_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-  comm_.map_peers(buf_, bases_);
+  if (comm_->has_nccl()) {
+    const std::vector<PeerBlob> all = comm_->allgather_blobs(blob());
+    connect(all.data());
+  }
+}
+
+PeerBlob P2PProbe::blob() const {
+  return comm_->make_blob(buf_, static_cast<long long>(kProbeSig + 2 * max_bytes_), 0x70327050726f6265ull);
+}
+
+void P2PProbe::connect(const PeerBlob* all) {
+  comm_->open_peers(all, buf_, bases_);
+  sig_.P = comm_->world();
+  sig_.me = comm_->rank();
+  sig_.N = 0;
+  sig_.my_counts = nullptr;
+  sig_.epoch = reinterpret_cast<unsigned int*>(buf_ + sizeof(unsigned int) * kMaxRanks);
+  for (int j = 0; j < sig_.P; ++j) sig_.sig[j] = reinterpret_cast<unsigned int*>(bases_[static_cast<size_t>(j)]);
+  connected_ = true;
+}
+
+void P2PProbe::barrier(bool soft) {
+  EpSignal a = sig_;
+  a.soft = soft ? 1 : 0;
+  ep_signal_barrier(a, stream_);
 }
 
 P2PProbe::~P2PProbe() {
-  // every rank unmaps the others' buffers before anybody frees its own
-  comm_.close_peers();
-  if (flag_ && stream_) {
+  // nobody unmaps or frees before every rank finished its last transfer
+  if (connected_ && stream_) {
     try {
-      comm_.barrier(flag_, stream_);
+      barrier(true);
+      cudaStreamSynchronize(stream_);
     } catch (...) {
     }
-    cudaStreamSynchronize(stream_);
   }
+  comm_->close_peers();
   if (stream_) cudaStreamDestroy(stream_);
-  if (flag_) cudaFree(flag_);
   if (buf_) cudaFree(buf_);
 }
 
 std::vector<double> P2PProbe::sweep(const double* sizes_mb, int nsizes, int reps, int warmup) {
-  const int W = comm_.world(), me = comm_.rank();
+  require(connected_, "p2p sweep: peers not connected (tamoe_p2p_probe_connect)");
+  const int W = comm_->world(), me = comm_->rank();
   require(nsizes >= 1 && reps >= 1 && warmup >= 0, "p2p sweep: bad sizes / reps");
   for (int s = 0; s < nsizes; ++s)
     require(sizes_mb[s] > 0.0 && sizes_mb[s] * 1e6 <= static_cast<double>(max_bytes_),
@@ -112,15 +177,16 @@ std::vector<double> P2PProbe::sweep(const double* sizes_mb, int nsizes, int reps
   cudaEvent_t e0, e1;
   TAMOE_CUDA(cudaEventCreate(&e0));
   TAMOE_CUDA(cudaEventCreate(&e1));
+  char* src_buf = buf_ + kProbeSig;
   for (int src = 0; src < W; ++src)
     for (int dst = 0; dst < W; ++dst)
       for (int si = 0; si < nsizes; ++si) {
         const size_t bytes = (static_cast<size_t>(sizes_mb[si] * 1e6) + 15) & ~static_cast<size_t>(15);
         for (int r = -warmup; r < reps; ++r) {
-          comm_.barrier(flag_, stream_);  // everybody idle, previous transfer done
+          barrier();  // everybody idle, previous transfer done
           if (me == src) {
             TAMOE_CUDA(cudaEventRecord(e0, stream_));
-            p2p_copy(bases_[static_cast<size_t>(dst)] + max_bytes_, buf_, bytes, stream_,
+            p2p_copy(bases_[static_cast<size_t>(dst)] + kProbeSig + max_bytes_, src_buf, bytes, stream_,
                      link_emulation().factor(src, dst));
             TAMOE_CUDA(cudaEventRecord(e1, stream_));
             TAMOE_CUDA(cudaEventSynchronize(e1));
@@ -130,17 +196,20 @@ std::vector<double> P2PProbe::sweep(const double* sizes_mb, int nsizes, int reps
           }
         }
       }
+  barrier();
   TAMOE_CUDA(cudaStreamSynchronize(stream_));
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  // every entry was written by exactly one rank: a sum all-reduce gathers them
-  double* d = nullptr;
-  TAMOE_CUDA(cudaMalloc(&d, sizeof(double) * out.size()));
-  TAMOE_CUDA(cudaMemcpy(d, out.data(), sizeof(double) * out.size(), cudaMemcpyHostToDevice));
-  comm_.allreduce_sum(d, out.size(), stream_);
-  TAMOE_CUDA(cudaStreamSynchronize(stream_));
-  TAMOE_CUDA(cudaMemcpy(out.data(), d, sizeof(double) * out.size(), cudaMemcpyDeviceToHost));
-  cudaFree(d);
+  if (comm_->has_nccl()) {
+    // every entry was written by exactly one rank: a sum all-reduce gathers them
+    double* d = nullptr;
+    TAMOE_CUDA(cudaMalloc(&d, sizeof(double) * out.size()));
+    TAMOE_CUDA(cudaMemcpy(d, out.data(), sizeof(double) * out.size(), cudaMemcpyHostToDevice));
+    comm_->allreduce_sum(d, out.size(), stream_);
+    TAMOE_CUDA(cudaStreamSynchronize(stream_));
+    TAMOE_CUDA(cudaMemcpy(out.data(), d, sizeof(double) * out.size(), cudaMemcpyDeviceToHost));
+    cudaFree(d);
+  }
   return out;
 }
 

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <memory>
 #include <vector>
 
 #include "route.hpp"
@@ -48,6 +49,9 @@ struct EpSignal {
   int* counts_dst[kMaxRanks];    // every rank's all_counts [P x N]
   const int* my_counts;          // null: plain barrier
   int P, me, N;
+  // teardown barrier: give up after ~5 s instead of trapping (a peer that exits without destroying its
+  // layer must not kill this rank's context)
+  int soft = 0;
 };
 void ep_signal_barrier(const EpSignal& a, cudaStream_t s);
 
@@ -59,20 +63,40 @@ struct PeerWords {
 void peer_broadcast_words(const PeerWords& dst, long long dst_off_words, const void* src, long long words, int P,
                           cudaStream_t s);
 
+// What one rank publishes so the others can map its workspace: the CUDA IPC handle of the allocation plus a
+// fingerprint of the layout (bytes, configuration hash) that every rank must agree on -- every peer pointer
+// is this rank's offset applied to the peer's base, so a mismatching peer would be written out of bounds.
+struct PeerBlob {
+  cudaIpcMemHandle_t handle;    // 64 bytes
+  long long bytes;              // size of the mapped allocation
+  unsigned long long fingerprint;
+  int world, rank, pid, device;
+  char pad[128 - 64 - 16 - 16];
+};
+static_assert(sizeof(PeerBlob) == 128, "PeerBlob is the 128-byte tamoe_ep_blob");
+
+// Communicator of the expert-parallel ranks.  Two bootstraps:
+//   * NCCL (one process per GPU): the blobs are all-gathered over NCCL;
+//   * external (no NCCL, ranks may share a device): the caller exchanges the 128-byte blobs with any transport
+//     (a TCP store, MPI, a gloo all-gather) and hands all of them back.
 class EpComm {
  public:
   EpComm(int world, int rank, const ncclUniqueId& id);
+  EpComm(int world, int rank);  // external bootstrap
   ~EpComm();
   int world() const { return world_; }
   int rank() const { return rank_; }
+  bool has_nccl() const { return comm_ != nullptr; }
+  PeerBlob make_blob(void* local_base, long long bytes, unsigned long long fingerprint) const;
+  // validate every rank's blob against this rank's and map the peers' allocations; bases[j] = rank j's
+  void open_peers(const PeerBlob* all, void* local_base, std::vector<char*>& bases);
+  std::vector<PeerBlob> allgather_blobs(const PeerBlob& mine);  // NCCL bootstrap only
   // my kept counts [N] -> everybody's [P x N] (stream-ordered; doubles as the step-start barrier)
   void allgather_counts(const int* my_counts, int* all_counts, int N, cudaStream_t s);
   // all ranks' streams reach this point before any proceeds (1-int all-reduce)
   void barrier(int* flag, cudaStream_t s);
   void allreduce_sum(double* buf, size_t n, cudaStream_t s);
-  void close_peers();  // unmap every peer allocation opened by map_peers
-  // map every rank's `local_base` allocation (cudaMalloc'd) into this process; bases[j] = rank j's
-  void map_peers(void* local_base, std::vector<char*>& bases);
+  void close_peers();  // unmap every peer allocation opened by open_peers
 
  private:
   int world_, rank_;
@@ -85,19 +109,25 @@ class EpComm {
 // copy -- the mechanism the dispatch uses -- with CUDA events on the source rank while the other ranks idle
 // between stream barriers.  Result on every rank: time_us[src][dst][size][rep] (the reference's
 // TransferSample rows, profile_io.hpp:8-13; alpha then absorbs the launch latency).
+// Phases are separated by the device signal barrier over the mapped buffers; with NCCL the sweep's rows are
+// summed over ranks at the end, with the external bootstrap each rank returns the rows it timed (src == rank).
 class P2PProbe {
  public:
-  P2PProbe(int world, int rank, const ncclUniqueId& id, size_t max_bytes);
+  P2PProbe(std::unique_ptr<EpComm> comm, size_t max_bytes);  // NCCL comm: maps the peers at once
   ~P2PProbe();
+  PeerBlob blob() const;
+  void connect(const PeerBlob* all);  // external bootstrap
   std::vector<double> sweep(const double* sizes_mb, int nsizes, int reps, int warmup);
 
  private:
-  EpComm comm_;
+  void barrier(bool soft = false);
+  std::unique_ptr<EpComm> comm_;
   size_t max_bytes_;
-  char* buf_ = nullptr;  // [src half | dst half]
+  char* buf_ = nullptr;  // [signal slots + epoch (256 B) | src half | dst half]
   std::vector<char*> bases_;
   cudaStream_t stream_ = nullptr;
-  int* flag_ = nullptr;
+  EpSignal sig_{};
+  bool connected_ = false;
 };
 
 void p2p_copy(void* dst, const void* src, size_t bytes, cudaStream_t s, int rep = 1);

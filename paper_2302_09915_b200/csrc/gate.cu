@@ -88,7 +88,10 @@ __global__ void __launch_bounds__(kRouteGroupWarps * 32) route_logits_kernel(con
   const int proc = b / groups;
   const int tok0 = (b % groups) * 32 + warp * RPW;
   const int N = d.N, k = d.k;
-  bool finite = true;
+  // rows with a non-finite logit (the reference throws ValidationError, gate.cpp:16-17): the bad flag is
+  // raised and the row is routed to experts 0..k-1 with NaN gate values, so every index stays in range and
+  // the step's outputs and losses come out NaN (poisoned) instead of faulting on a garbage index
+  unsigned okmask = 0;
 #pragma unroll 2
   for (int r = 0; r < RPW; ++r) {
     const int tok = tok0 + r;
@@ -96,6 +99,7 @@ __global__ void __launch_bounds__(kRouteGroupWarps * 32) route_logits_kernel(con
     const float* row = logits + (static_cast<long long>(proc) * d.S + tok) * N;
     float v[EPL];
     float mx = -INFINITY;
+    bool finite = true;
 #pragma unroll
     for (int j = 0; j < EPL; ++j) {
       const int c = j * 32 + lane;
@@ -103,6 +107,7 @@ __global__ void __launch_bounds__(kRouteGroupWarps * 32) route_logits_kernel(con
       if (valid && c < N) finite &= isfinite(v[j]);
       mx = fmaxf(mx, v[j]);
     }
+    if (__all_sync(0xffffffffu, finite)) okmask |= 1u << r;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
     const double dmx = valid ? static_cast<double>(mx) : 0.0;
@@ -131,13 +136,15 @@ __global__ void __launch_bounds__(kRouteGroupWarps * 32) route_logits_kernel(con
     const bool valid = tok < d.S;
     const long long gtok = static_cast<long long>(proc) * d.S + tok;
     const double dn = den[warp][r];
+    const bool ok = (okmask >> r) & 1u;
     double p[EPL];
 #pragma unroll
     for (int j = 0; j < EPL; ++j) {
       const int c = j * 32 + lane;
-      p[j] = (valid && c < N) ? E[warp][r][c] / dn : 0.0;
+      p[j] = (valid && c < N) ? (ok ? E[warp][r][c] / dn : __longlong_as_double(0x7ff8000000000000ll)) : 0.0;
       if (valid && c < N && o.probs) o.probs[gtok * N + c] = p[j];
       msum[j] += p[j];
+      if (!ok) p[j] = -static_cast<double>(c) / 2048.0;  // selection order of a bad row: experts 0, 1, ...
     }
     if (!valid) continue;
     // top-k: k rounds of a warp arg-max under (p desc, expert asc)
@@ -188,15 +195,19 @@ __global__ void __launch_bounds__(kRouteGroupWarps * 32) route_logits_kernel(con
         if (t < k) {
           const long long a = gtok * k + t;
           o.idx[a] = pe[t];
-          o.score[a] = pp[t];
-          const double g = k == 1 ? pp[t] : pp[t] / mass;
+          o.score[a] = ok ? pp[t] : 0.0;
+          const double g = !ok ? __longlong_as_double(0x7ff8000000000000ll) : (k == 1 ? pp[t] : pp[t] / mass);
           o.gate[a] = static_cast<float>(g);
           if (o.gate64) o.gate64[a] = g;
         }
       }
     }
   }
-  if (__any_sync(0xffffffffu, !finite) && lane == 0) atomicOr(o.bad, 1);
+  if (okmask != (1u << RPW) - 1u && lane == 0) {
+    bool any_bad = false;
+    for (int r = 0; r < RPW; ++r) any_bad |= !((okmask >> r) & 1u) && tok0 + r < d.S;
+    if (any_bad) atomicOr(o.bad, 1);
+  }
   __syncthreads();  // every warp is done with E
 #pragma unroll
   for (int j = 0; j < EPL; ++j) {

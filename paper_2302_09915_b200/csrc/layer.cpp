@@ -161,7 +161,10 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
   const int E = c.N / c.world_size;
   const long long T = static_cast<long long>(c.P) * c.S;
   // receive side: worst case every token of every rank picks this rank's experts
-  r_max_ = static_cast<int>(static_cast<long long>(c.world_size) * (T * c.k + 16LL * E));
+  const long long r_max = static_cast<long long>(c.world_size) * (T * c.k + 16LL * E);
+  require(r_max <= INT_MAX, "layer: world_size * (P*S*k + 16*E) rows exceed the int32 row index");
+  require(T * c.k < (1LL << 27), "layer: P*S*k must be < 2^27 (row field of the expert-parallel return codes)");
+  r_max_ = static_cast<int>(r_max);
   rw_.reserve(arena_, c.P, c.S, c.N, c.k);
   global_ep_ = ep_ != nullptr && c.cap_mode == 1;
   if (global_ep_) gw_.reserve(arena_, c.world_size, c.S, c.N, c.k);
@@ -205,14 +208,54 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
   n_loss_part_ = combine_blocks(T);
   arena_.reserve(loss_part_, n_loss_part_);
   arena_.commit();
+  TAMOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&bad_host_), sizeof(int), cudaHostAllocDefault));
+  *bad_host_ = 0;
+  TAMOE_CUDA(cudaEventCreateWithFlags(&step_done_, cudaEventDisableTiming));
   if (!ep_) ret_codes_.p[0] = ret_code_;
   if (ep_) {
-    // barrier slots start at zero on every rank before any peer can signal: the memset is stream-ordered
-    // before this rank's contribution to the handle all-gather that every peer waits for
+    // barrier slots start at zero on every rank before any peer can signal: zeroed (and synchronised)
+    // before this rank's handle leaves the process
     TAMOE_CUDA(cudaMemset(sig_slots_, 0, sizeof(unsigned int) * kMaxRanks));
     TAMOE_CUDA(cudaMemset(sig_epoch_, 0, sizeof(unsigned int)));
-    // every rank's arena has the same layout: map them all into this process (CUDA IPC over NVLink)
-    ep_->map_peers(arena_.base(), bases_);
+    if (global_ep_)
+      TAMOE_CUDA(cudaMemset(gw_.buf.msum4, 0, sizeof(double) * static_cast<size_t>(gw_.dims.tiles()) * 4 * c.N));
+    TAMOE_CUDA(cudaDeviceSynchronize());
+    if (ep_->has_nccl()) {
+      const std::vector<PeerBlob> all = ep_->allgather_blobs(blob());
+      connect(all.data());
+    }
+  }
+  init_topology(c_hat);
+}
+
+unsigned long long Layer::fingerprint() const {
+  // FNV-1a over everything that shapes the workspace layout (not the rank)
+  const LayerConfig& c = cfg_;
+  const long long f[] = {c.P, c.S, c.d, c.d_out, c.N, c.k, c.f, c.act, c.cap_mode, c.aux_kind, c.need_dx,
+                         c.world_size, static_cast<long long>(c.cf * 1e9), r_max_, dw_splits_};
+  unsigned long long h = 1469598103934665603ull;
+  for (long long v : f)
+    for (int b = 0; b < 8; ++b) {
+      h ^= static_cast<unsigned long long>(v >> (8 * b)) & 0xffull;
+      h *= 1099511628211ull;
+    }
+  return h;
+}
+
+PeerBlob Layer::blob() const {
+  require(ep_ != nullptr, "blob: not an expert-parallel layer");
+  return ep_->make_blob(arena_.base(), arena_.bytes(), fingerprint());
+}
+
+// Map every rank's workspace (identical layouts: every peer pointer is this rank's offset applied to the
+// peer's base) and derive the peer views of the exchange buffers and barrier slots.
+void Layer::connect(const PeerBlob* all) {
+  const LayerConfig& c = cfg_;
+  require(ep_ != nullptr, "connect: not an expert-parallel layer");
+  require(!connected_, "connect: peers already mapped");
+  const int E = c.N / c.world_size;
+  {
+    ep_->open_peers(all, arena_.base(), bases_);
     for (int j = 0; j < c.world_size; ++j) link_rep_[j] = link_emulation().factor(c.rank, j);
     sig_.P = c.world_size;
     sig_.me = c.rank;
@@ -238,14 +281,17 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
         gw_score_.p[j] = peer_of(gw_.buf.score, j);
         gw_hist_.p[j] = peer_of(gw_.buf.hist4, j);
       }
-      TAMOE_CUDA(cudaMemset(gw_.buf.msum4, 0, sizeof(double) * static_cast<size_t>(gw_.dims.tiles()) * 4 * c.N));
     }
     map_.P = c.world_size;
     map_.E = E;
     map_.local_start = rw_.buf.seg_start;
     map_.dst_off = plan_.dst_off;
   }
+  connected_ = true;
+}
 
+void Layer::init_topology(const double* c_hat) {
+  const LayerConfig& c = cfg_;
   // host-side, once per topology: penalties p = Norm(1/c_hat) and capacities (gate.cpp:151-180, 222-246)
   std::vector<double> pen(static_cast<size_t>(c.P) * c.N, 1.0 / c.N);
   if (c.aux_kind == 1) {
@@ -279,7 +325,42 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
   if (global_ep_) gw_.upload_caps(caps.data(), nullptr);  // one global cap per expert, every rank's row
 }
 
-Layer::~Layer() = default;
+Layer::~Layer() {
+  if (step_done_) {
+    cudaEventSynchronize(step_done_);
+    cudaEventDestroy(step_done_);
+  }
+  if (bad_host_) cudaFreeHost(bad_host_);
+  if (ep_ && connected_ && stepped_) {
+    // nobody unmaps or frees its workspace while a peer may still store into it: a (soft) device barrier,
+    // then unmap the peers, then the arena is freed (member destruction)
+    try {
+      EpSignal a = sig_;
+      a.my_counts = nullptr;
+      a.soft = 1;
+      ep_signal_barrier(a, nullptr);
+      cudaStreamSynchronize(nullptr);
+    } catch (...) {
+    }
+  }
+  if (ep_) ep_->close_peers();
+}
+
+void Layer::check_deferred(bool wait) {
+  if (!step_pending_) return;
+  if (wait) TAMOE_CUDA(cudaEventSynchronize(step_done_));
+  else if (cudaEventQuery(step_done_) != cudaSuccess) {
+    (void)cudaGetLastError();  // cudaErrorNotReady is not sticky; clear it
+    return;
+  }
+  step_pending_ = false;
+  if (*bad_host_ != 0) {
+    *bad_host_ = 0;
+    throw ValidationError("non-finite gate logit");
+  }
+}
+
+void Layer::status() { check_deferred(true); }
 
 PeerBufs Layer::peers(__nv_bfloat16* local) const {
   PeerBufs pb{};
@@ -405,6 +486,15 @@ void Layer::step(const LayerIO& io, cudaStream_t s) {
   require(io.x && io.y && io.wg && io.w1 && io.dwg && io.dw1 && io.losses, "layer step: missing buffer");
   require(c.f == 0 || (io.w2 && io.dw2), "layer step: FFN experts need w2 / dw2");
   require(!c.need_dx || io.dx, "layer step: need_dx set but dx is null");
+  require(!ep_ || connected_, "layer step: expert-parallel peers not connected (tamoe_layer_ep_connect)");
+  check_deferred(false);  // a completed earlier step that saw a non-finite logit raises here
+  stepped_ = true;
+  step_graph(io, s);
+  TAMOE_CUDA(cudaEventRecord(step_done_, s));
+  step_pending_ = true;
+}
+
+void Layer::step_graph(const LayerIO& io, cudaStream_t s) {
   StepGraph& g = graph_;
   if (timer_.enabled || !graphs_enabled() || !g.warm || g.disabled) {
     run_step(io, s);
@@ -465,6 +555,7 @@ void Layer::route_front(const LayerIO& io, cudaStream_t s) {
   const bool compulsory = cfg_.aux_kind == 2;
   TAMOE_CUDA(cudaMemsetAsync(b.bad, 0, sizeof(int), s));
   gate_forward(io.x, io.wg, n_pad_, rw.dims, cfg_.d, rw.row_out(logits_, compulsory ? probs_ : nullptr), s);
+  TAMOE_CUDA(cudaMemcpyAsync(bad_host_, b.bad, sizeof(int), cudaMemcpyDeviceToHost, s));
   tm.mark("gate_fwd", s);
   if (compulsory) {  // quota claims replace the top-k / capacity outcome; every token is kept
     route_compulsory(rw.dims, b, probs_, quota_, comp_ws_, comp_ws_bytes_, s);

@@ -126,6 +126,15 @@ class Layer {
   const float* logits() const { return logits_; }
   PhaseTimer& timer() { return timer_; }
   int launches_per_step() const;
+  // Non-finite gate logits (the reference throws ValidationError, gate.cpp:16-17) are detected on the
+  // device without a host synchronisation inside the step: the flag is copied into pinned host memory at
+  // the end of every step and reported (ValidationError) by the next step() once that step has completed,
+  // or at once by status(), which waits for the last step.
+  void status();
+  // expert parallelism with the external bootstrap: this rank's 128-byte blob, then every rank's blobs
+  PeerBlob blob() const;
+  void connect(const PeerBlob* all);
+  bool connected() const { return connected_; }
 
  private:
   void step_local(const LayerIO& io, cudaStream_t s);
@@ -178,6 +187,13 @@ class Layer {
   char* comp_ws_ = nullptr;
   size_t comp_ws_bytes_ = 0;  // penalties p = Norm(1/c_hat) computed at creation (created with the topo loss)
   PhaseTimer timer_;
+  bool connected_ = false, stepped_ = false;
+  unsigned long long fingerprint() const;
+  void init_topology(const double* c_hat);
+  int* bad_host_ = nullptr;            // pinned: the last step's non-finite-logit flag
+  cudaEvent_t step_done_ = nullptr;    // recorded on the caller's stream after every step
+  bool step_pending_ = false;
+  void check_deferred(bool wait);
   // CUDA graphs of one step keyed by the step's buffers (LayerIO), a few cached (double-buffered inputs
   // alternate), captured and launched on a private stream joined to the caller's with two events.
   // TAMOE_GRAPHS=0 or phase timing: eager.
@@ -195,6 +211,7 @@ class Layer {
     ~StepGraph();
   } graph_;
   void run_step(const LayerIO& io, cudaStream_t s);
+  void step_graph(const LayerIO& io, cudaStream_t s);
   void route_front(const LayerIO& io, cudaStream_t s);
 };
 

@@ -199,6 +199,7 @@ TrainReport train_layer(LayerConfig cfg, const double* c_hat, const TrainOptions
                    [&](int step, double* losses, int* counts_i, int* dropped_i) {
                      if (o.kind == 1 && o.switch_step != INT_MIN && step > o.switch_step) layer.set_aux_kind(0);
                      layer.step(io, s);
+                     layer.status();  // non-finite logit: ValidationError before the update (gate.cpp:16-17)
                      const size_t pn = static_cast<size_t>(cfg.P) * cfg.N;
                      TAMOE_CUDA(cudaMemcpyAsync(losses, io.losses, sizeof(double) * 2, cudaMemcpyDeviceToHost, s));
                      TAMOE_CUDA(cudaMemcpyAsync(counts_i, rb.counts, sizeof(int) * pn, cudaMemcpyDeviceToHost, s));

@@ -53,7 +53,13 @@ _lib.lib.tamoe_layer_enable_timing.argtypes = [ctypes.c_void_p, ctypes.c_int]
 _lib.lib.tamoe_layer_timing.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_char_p),
                                         ctypes.POINTER(ctypes.c_double), ctypes.c_int, ctypes.POINTER(ctypes.c_int),
                                         ctypes.POINTER(ctypes.c_int)]
-for _n in ("tamoe_layer_create", "tamoe_layer_destroy", "tamoe_layer_step", "tamoe_layer_read",
+_lib.lib.tamoe_layer_status.argtypes = [ctypes.c_void_p]
+_lib.lib.tamoe_layer_create_ep_begin.argtypes = [ctypes.POINTER(_Cfg), ctypes.POINTER(ctypes.c_double),
+                                                 ctypes.POINTER(ctypes.c_void_p), ctypes.c_void_p]
+_lib.lib.tamoe_layer_ep_connect.argtypes = [ctypes.c_void_p, ctypes.c_char_p]
+_lib.lib.tamoe_layer_create_ep_begin.restype = ctypes.c_int
+_lib.lib.tamoe_layer_ep_connect.restype = ctypes.c_int
+for _n in ("tamoe_layer_status", "tamoe_layer_create", "tamoe_layer_destroy", "tamoe_layer_step", "tamoe_layer_read",
            "tamoe_layer_launches_per_step", "tamoe_layer_enable_timing", "tamoe_layer_timing", "tamoe_layer_create_ep",
            "tamoe_nccl_unique_id", "tamoe_layer_a2a_bytes", "tamoe_ep_plan"):
     getattr(_lib.lib, _n).restype = ctypes.c_int
@@ -115,7 +121,11 @@ def ep_plan(recv):
 
 
 class TAMoELayer:
-    def __init__(self, cfg: LayerConfig, c_hat=None, device="cuda", nccl_id: bytes = None):
+    """world_size > 1: expert parallelism.  With `nccl_id` (nccl_unique_id() broadcast from one rank) the
+    ranks bootstrap over NCCL (one process per GPU); without it the workspace handles are all-gathered over
+    torch.distributed (`group`, any backend -- gloo lets several ranks share one GPU)."""
+
+    def __init__(self, cfg: LayerConfig, c_hat=None, device="cuda", nccl_id: bytes = None, group=None):
         self.cfg = cfg
         self.device = torch.device(device)
         c = _Cfg(cfg.P, cfg.S, cfg.d, cfg.d_out, cfg.N, cfg.k, cfg.f, cfg.act, cfg.cap_mode, cfg.capacity_factor,
@@ -124,10 +134,20 @@ class TAMoELayer:
         self._c_hat = np.ascontiguousarray(c_hat, np.float64) if c_hat is not None else None
         h = ctypes.c_void_p()
         chp = self._c_hat.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if self._c_hat is not None else None
-        if cfg.world_size > 1:
-            if nccl_id is None or len(nccl_id) != 128:
+        if cfg.world_size > 1 and nccl_id is not None:
+            if len(nccl_id) != 128:
                 raise ValueError("expert parallelism needs the 128-byte NCCL id from nccl_unique_id()")
             _lib.check(_lib.lib.tamoe_layer_create_ep(ctypes.byref(c), chp, nccl_id, ctypes.byref(h)))
+        elif cfg.world_size > 1:
+            from .ops import allgather_blobs
+            blob = ctypes.create_string_buffer(128)
+            _lib.check(_lib.lib.tamoe_layer_create_ep_begin(ctypes.byref(c), chp, ctypes.byref(h), blob))
+            try:
+                blobs = allgather_blobs(blob.raw, group)
+                _lib.check(_lib.lib.tamoe_layer_ep_connect(h, blobs))
+            except BaseException:
+                _lib.lib.tamoe_layer_destroy(h)
+                raise
         else:
             _lib.check(_lib.lib.tamoe_layer_create(ctypes.byref(c), chp, ctypes.byref(h)))
         self._h = h
@@ -172,6 +192,11 @@ class TAMoELayer:
         s = stream if stream is not None else torch.cuda.current_stream()
         _lib.check(_lib.lib.tamoe_layer_step(self._h, ctypes.byref(io), ctypes.c_void_p(s.cuda_stream)))
         return self.losses
+
+    def status(self):
+        """Wait for the last step; raise ValidationError("non-finite gate logit") if it saw one
+        (gate.cpp:16-17).  The next step() raises it too, once the failing step has completed."""
+        _lib.check(_lib.lib.tamoe_layer_status(self._h))
 
     def read(self, what, shape):
         out = np.zeros(shape, dtype=_R_DTYPES[what])

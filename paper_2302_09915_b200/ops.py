@@ -156,6 +156,41 @@ def p2p_sweep(nccl_id: bytes, world: int, rank: int, sizes_mb=(1.0, 4.0, 16.0, 6
             for s in range(sz.size) for r in range(reps)]
 
 
+def allgather_blobs(blob: bytes, group=None) -> bytes:
+    """All-gather every rank's 128-byte expert-parallel blob over torch.distributed (any backend; gloo needs
+    no GPU and lets several ranks share one device) -> world x 128 bytes in rank order."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, bytes(blob), group=group)
+    assert all(len(b) == 128 for b in out)
+    return b"".join(out)
+
+
+def p2p_sweep_store(world: int, rank: int, sizes_mb=(1.0, 4.0, 16.0, 64.0, 128.0), reps: int = 5,
+                    warmup: int = 2, group=None):
+    """p2p_sweep with the NCCL-free bootstrap: the probe buffers' IPC handles are exchanged over
+    torch.distributed (gloo works; ranks may share a device) and the per-rank rows summed the same way."""
+    import torch
+    import torch.distributed as dist
+    sz = _f64(list(sizes_mb))
+    h = ctypes.c_void_p()
+    blob = ctypes.create_string_buffer(128)
+    _lib.call("tamoe_p2p_probe_create", world, rank, float(sz.max()), ctypes.byref(h), blob)
+    try:
+        allb = ctypes.create_string_buffer(allgather_blobs(blob.raw, group), 128 * world)
+        _lib.call("tamoe_p2p_probe_connect", h, allb, world)
+        out = np.zeros((world, world, sz.size, reps))
+        _lib.call("tamoe_p2p_probe_sweep", h, sz.ctypes.data_as(_D), int(sz.size), reps, warmup,
+                  out.ctypes.data_as(_D))
+    finally:
+        _lib.call("tamoe_p2p_probe_destroy", h)
+    t = torch.from_numpy(out)
+    dist.all_reduce(t, group=group)  # every entry was written by exactly one rank
+    out = t.numpy()
+    return [(i, j, float(sz[s]), float(out[i, j, s, r])) for i in range(world) for j in range(world)
+            for s in range(sz.size) for r in range(reps)]
+
+
 def set_link_emulation(group_size: int, repeat: int) -> None:
     """Emulated heterogeneous topology (BASELINE C5): links between ranks in different groups of `group_size`
     consecutive ranks carry every payload store `repeat` times (1/repeat of the bandwidth).  (0, 1) = off."""

@@ -1,4 +1,6 @@
-"""Expert-parallel parity on W GPUs (torchrun --nproc-per-node W tests/ep_worker.py [case]).
+"""Expert-parallel parity on W ranks (torchrun --nproc-per-node W tests/ep_worker.py [case] [steps]).
+With fewer GPUs than ranks (or TAMOE_EP_BOOTSTRAP=store) the ranks bootstrap over gloo and share devices
+round-robin -- the same kernels, peer stores and device barriers, several ranks per GPU.
 
 Every rank owns one logical process (its gate replica and S tokens) and E = N/W experts; the
 layer exchanges tokens, expert outputs and gradients over NCCL.  Rank 0 gathers losses and
@@ -37,11 +39,21 @@ def rel(a, b):
 
 def main():
     case = sys.argv[1] if len(sys.argv) > 1 else "ffn_prop"
+    # optional second argument: number of steps; > 2 turns the run into a determinism stress loop (every
+    # step's losses and gradients must be bitwise identical to the first step's: same inputs, same weights)
+    steps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
     c = CASES[case]
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ndev = torch.cuda.device_count()
+    # store bootstrap (no NCCL): the workspace handles go over gloo, so several ranks may share one GPU
+    shared = os.environ.get("TAMOE_EP_BOOTSTRAP") == "store" or ndev < world
+    dev = local % ndev
+    torch.cuda.set_device(dev)
+    if shared:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     import oracle
     from paper_2302_09915_b200 import ops
     from paper_2302_09915_b200.layer import LayerConfig, TAMoELayer, nccl_unique_id
@@ -66,8 +78,10 @@ def main():
     beta = np.array([[0.1 if i == j else (1.0 if i // 2 == j // 2 else 4.0) for j in range(P)] for i in range(P)])
     c_hat = ops.target_closed_form(beta, N, k, S)
 
-    obj = [nccl_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(obj, src=0)
+    obj = [None]
+    if not shared:
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
     cfg = LayerConfig(P=1, S=S, d=d, d_out=dout, N=N, k=k, f=f, act=1, cap_mode=c["cap"], capacity_factor=c.get("cf", 1.25),
                       aux_kind=c["kind"], need_dx=c["need_dx"], world_size=world, rank=rank)
     layer = TAMoELayer(cfg, c_hat, nccl_id=obj[0])
@@ -80,11 +94,22 @@ def main():
         params["w2"] = torch.tensor(W2[lo:hi], dtype=torch.float32).transpose(1, 2).contiguous().bfloat16().cuda()
     xt = torch.tensor(x[rank], dtype=torch.float32).bfloat16().cuda()
     yt = torch.tensor(y[rank], dtype=torch.float32).bfloat16().cuda()
-    for _ in range(2):  # second step re-uses every buffer
+    first = None
+    for it in range(steps):  # the second step re-uses every buffer (graph replay from then on)
         layer.step(xt, yt, params)
+        if steps > 2:
+            cur = [layer.losses, layer.dwg, layer.dw1] + ([layer.dw2] if f else []) + ([layer.dx] if c["need_dx"] else [])
+            if first is None:
+                first = [t.clone() for t in cur]
+            else:
+                for a, b in zip(first, cur):
+                    assert torch.equal(a, b), f"rank {rank}: step {it} differs from step 0 (non-deterministic)"
+    layer.status()
     torch.cuda.synchronize()
 
     def gather(t):
+        if shared:  # gloo: CPU tensors
+            t = t.contiguous().cpu()
         out = [torch.empty_like(t) for _ in range(world)]
         dist.all_gather(out, t.contiguous())
         return [o.cpu() for o in out]
@@ -122,9 +147,12 @@ def main():
         if dx is not None:
             gx = np.stack([t.float().numpy() for t in dx])
             assert rel(gx, o["dx"]) < 2e-2, rel(gx, o["dx"])
-        print(f"EP_PARITY_OK case={case} world={world} task={task:.6f} oracle={o['task_loss']:.6f} "
-              f"aux={aux:.6f} a2a_bytes_rank0={a2a} routing_mismatch={mism}", flush=True)
+        print(f"EP_PARITY_OK case={case} world={world} devices={min(ndev, world)} "
+              f"bootstrap={'store' if shared else 'nccl'} steps={steps} task={task:.6f} "
+              f"oracle={o['task_loss']:.6f} aux={aux:.6f} a2a_bytes_rank0={a2a} routing_mismatch={mism}",
+              flush=True)
     dist.barrier()
+    del layer  # teardown barrier: every rank unmaps its peers before any workspace is freed
     dist.destroy_process_group()
 
 

@@ -238,3 +238,41 @@ def test_layer_all_tokens_on_one_expert(cap, cf):
     layer, o, extra = run_case(P, S, d, dout, N, k, f, cap, 1, True, seed=5, cf=cf, hot_expert=5)
     assert (o["expert"][:, :, 0] == 5).all()
     check(layer, o, extra, P, S, N, k, f, True)
+
+
+@pytest.mark.parametrize("k,bad", [(1, float("inf")), (2, float("nan"))])
+def test_layer_non_finite_logit_raises(k, bad):
+    """gate.cpp:16-17 throws ValidationError("non-finite gate logit").  The stream-ordered step reports it
+    deferred: tamoe_layer_status (and the next step, once the bad step completed) returns status 2 through
+    the C ABI and the Python mirror raises ValidationError.  The bad row is routed in range (no fault) and
+    poisons the step's losses with NaN; a later clean step is unaffected."""
+    import ctypes
+    from paper_2302_09915_b200 import _lib, ops
+    from paper_2302_09915_b200.layer import LayerConfig, TAMoELayer
+    P, S, d, dout, N, f = 1, 256, 256, 128, 8, 256
+    cfg = LayerConfig(P=P, S=S, d=d, d_out=dout, N=N, k=k, f=f, act=1, cap_mode=2, aux_kind=0, need_dx=True)
+    layer = TAMoELayer(cfg)
+    params = layer.init_params(seed=2)
+    g = torch.Generator(device="cuda").manual_seed(9)
+    x = torch.randn(S, d, generator=g, device="cuda").bfloat16()
+    y = torch.randn(S, dout, generator=g, device="cuda").bfloat16()
+    layer.step(x, y, params)
+    layer.status()  # clean
+    clean = layer.losses.cpu().clone()
+    xb = x.clone()
+    xb[37, 5] = bad
+    layer.step(xb, y, params)
+    torch.cuda.synchronize()
+    assert _lib.lib.tamoe_layer_status(layer._h) == 2  # C ABI: status 2 = ValidationError
+    assert b"non-finite gate logit" in _lib.lib.tamoe_last_error()
+    assert not np.isfinite(layer.losses.cpu().numpy()).all()  # poisoned, not silently finite
+    idx = layer.read(ops.R_IDX, (S, k))
+    assert idx.min() >= 0 and idx.max() < N and list(idx[37]) == list(range(k))
+    # the next step reports a completed bad step before running
+    layer.step(xb, y, params)
+    torch.cuda.synchronize()
+    with pytest.raises(ops.ValidationError, match="non-finite gate logit"):
+        layer.step(x, y, params)
+    layer.step(x, y, params)
+    layer.status()
+    assert torch.equal(layer.losses.cpu(), clean)
