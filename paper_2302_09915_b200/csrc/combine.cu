@@ -10,6 +10,8 @@
 
 #include "combine.hpp"
 #include "common.hpp"
+#include "gate_dz.cuh"
+#include "ptx.cuh"
 #include "route.hpp"
 
 namespace tamoe {
@@ -37,16 +39,35 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
 
 // KT = compile-time top-k (0: runtime k <= kMaxTopK).  Each lane keeps kU 16-byte vectors of every
 // slot in flight before computing, so the warp has (k + 1) * kU * 512 B of loads outstanding.
-template <int KT>
+// NPL > 0: the gate dz pass is fused in (experts per lane, N <= 32 * NPL).
+template <int KT, int NPL>
 __global__ void __launch_bounds__(kCombWarps * 32) combine_loss_kernel(const __grid_constant__ CombineArgs a) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   constexpr int KM = KT > 0 ? KT : kMaxTopK;
   constexpr int kU = 4;
   __shared__ double wsum[kCombWarps];
+  extern __shared__ double coeff[];  // [P*N] aux-loss coefficients (fused dz)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long t = static_cast<long long>(blockIdx.x) * kCombWarps + warp;
+  if constexpr (NPL > 0) {
+    dz_coeff_smem(a.gz, coeff);
+    __syncthreads();
+  }
   double lsum = 0.0;
   if (t < a.T) {
     const int k = KT > 0 ? KT : a.k;
+    float lg[NPL > 0 ? NPL : 1];
+    int ex_in[KM];
+    double sc_in[KM];
+    if constexpr (NPL > 0) {  // the dz pass's inputs, loaded up front so their latency overlaps the combine
+      dz_load_logits<NPL>(a.gz, t, lane, lg);
+#pragma unroll
+      for (int j = 0; j < KM; ++j) {
+        ex_in[j] = j < k ? a.idx[t * k + j] : -1;
+        sc_in[j] = (k > 1 && j < k) ? a.gz.score[t * k + j] : 0.0;
+      }
+    }
     int rows[KM];
     float g[KM], dot[KM];
     const __nv_bfloat16* osrc[KM];
@@ -122,15 +143,19 @@ __global__ void __launch_bounds__(kCombWarps * 32) combine_loss_kernel(const __g
         }
       }
     }
+    float dl[KM];
 #pragma unroll
     for (int j = 0; j < KM; ++j) {
+      dl[j] = 0.f;
       if (j < k) {
         float s = dot[j];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) a.dldg[t * k + j] = rows[j] >= 0 ? a.mse_scale * s : 0.f;
+        dl[j] = rows[j] >= 0 ? a.mse_scale * s : 0.f;
+        if (lane == 0) a.dldg[t * k + j] = dl[j];
       }
     }
+    if constexpr (NPL > 0) dz_token<KM, NPL>(a.gz, coeff, t, k, lane, lg, ex_in, dl, sc_in);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
@@ -147,13 +172,28 @@ __global__ void __launch_bounds__(kCombWarps * 32) combine_loss_kernel(const __g
 
 int combine_blocks(long long T) { return static_cast<int>((T + kCombWarps - 1) / kCombWarps); }
 
+template <int KT>
+static void launch_combine(const CombineArgs& a, int blocks, cudaStream_t s) {
+  if (!a.fuse_dz) {
+    launch_pdl(combine_loss_kernel<KT, 0>, blocks, kCombWarps * 32, 0, s, a);
+    return;
+  }
+  const size_t smem = sizeof(double) * a.gz.P * a.gz.N;
+  const int N = a.gz.N;
+  if (N <= 32) launch_pdl(combine_loss_kernel<KT, 1>, blocks, kCombWarps * 32, smem, s, a);
+  else if (N <= 64) launch_pdl(combine_loss_kernel<KT, 2>, blocks, kCombWarps * 32, smem, s, a);
+  else if (N <= 128) launch_pdl(combine_loss_kernel<KT, 4>, blocks, kCombWarps * 32, smem, s, a);
+  else launch_pdl(combine_loss_kernel<KT, 8>, blocks, kCombWarps * 32, smem, s, a);
+}
+
 void combine_loss(const CombineArgs& a, cudaStream_t s) {
   require(a.dout % 8 == 0, "combine: d_out must be a multiple of 8");
   require(a.k >= 1 && a.k <= kMaxTopK, "combine: k out of range");
+  require(!a.fuse_dz || (a.gz.N <= 256 && a.gz.P * a.gz.N <= 4096), "combine: fused dz needs N <= 256");
   const int blocks = combine_blocks(a.T);
-  if (a.k == 1) combine_loss_kernel<1><<<blocks, kCombWarps * 32, 0, s>>>(a);
-  else if (a.k == 2) combine_loss_kernel<2><<<blocks, kCombWarps * 32, 0, s>>>(a);
-  else combine_loss_kernel<0><<<blocks, kCombWarps * 32, 0, s>>>(a);
+  if (a.k == 1) launch_combine<1>(a, blocks, s);
+  else if (a.k == 2) launch_combine<2>(a, blocks, s);
+  else launch_combine<0>(a, blocks, s);
   TAMOE_CUDA(cudaGetLastError());
 }
 

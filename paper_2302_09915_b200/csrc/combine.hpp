@@ -2,6 +2,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "gate_bwd.hpp"
 #include "route.hpp"
 
 namespace tamoe {
@@ -21,6 +22,10 @@ struct CombineArgs {
   RowMap map;
   float* dldg;                   // [T*k]
   double* loss_part;             // [combine_blocks(T)] sum of squared residuals per block
+  // fuse_dz: the gate's softmax backward (gate_dz) runs per token right after the combine, in the same warp
+  // (the loss finalisation then moves to gate_dw's reduction); gz.dldg is not read
+  int fuse_dz;
+  GateDzArgs gz;
 };
 
 int combine_blocks(long long T);

@@ -2,7 +2,9 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <stdexcept>
+#include <utility>
 #include <string>
 
 namespace tamoe {
@@ -22,6 +24,33 @@ inline void cuda_check(cudaError_t e, const char* what) {
 
 inline void require(bool cond, const std::string& msg) {
   if (!cond) throw ValidationError(msg);
+}
+
+// Programmatic dependent launch between the step's kernels (TAMOE_PDL=0: plain stream order).  Every kernel
+// launched this way calls griddepcontrol.launch_dependents / .wait (ptx::pdl_trigger / pdl_wait) before it
+// touches memory the previous kernel writes or reads.
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("TAMOE_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+// kernel<<<grid, block, smem, s>>>(args...) with the programmatic-serialization attribute
+template <class... KArgs, class... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TAMOE_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
 }
 
 inline int num_sms() {

@@ -3,6 +3,7 @@
 
 #include "common.hpp"
 #include "ep.hpp"
+#include "ptx.cuh"
 
 namespace tamoe {
 
@@ -13,6 +14,8 @@ __device__ __forceinline__ int pad16(int c) { return (c + 15) & ~15; }
 // expert-major receive layouts: at rank j, local expert e_l owns rows
 //   [ sum_{e' < e_l} sum_src pad16(c[src][jE+e']) , ... ) split into per-source segments in rank order.
 __global__ void ep_plan_kernel(EpPlanDev p, int P, int E, int me) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int N = P * E;
   // one thread per global expert: where do my rows for it start at its owner?
   for (int ge = threadIdx.x; ge < N; ge += blockDim.x) {
@@ -37,6 +40,8 @@ __global__ void ep_plan_kernel(EpPlanDev p, int P, int E, int me) {
 // Return map of the receive layout: block (local expert el, source i) fills its segment's rows with
 // (i, row of the same pick in source i's local layout = expert-major, 16-padded, global expert order).
 __global__ void ep_push_map_kernel(EpPlanDev p, int P, int E, int me) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int N = P * E;
   const int el = blockIdx.x / P, i = blockIdx.x % P;
   const int ge = me * E + el;
@@ -71,6 +76,8 @@ __device__ __forceinline__ unsigned long long global_ns() {
 }
 
 __global__ void ep_barrier_kernel(const __grid_constant__ EpSignal a) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   if (a.my_counts) {
     for (int i = threadIdx.x; i < a.P * a.N; i += blockDim.x) {
       const int r = i / a.N, e = i - r * a.N;
@@ -129,6 +136,8 @@ __global__ void __launch_bounds__(512) p2p_copy_kernel(uint4* __restrict__ dst, 
 
 __global__ void peer_broadcast_kernel(const __grid_constant__ PeerWords dst, long long off,
                                       const unsigned int* __restrict__ src, long long words, int P) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < words; i += stride) {
     const unsigned int v = src[i];
@@ -143,7 +152,7 @@ void peer_broadcast_words(const PeerWords& dst, long long dst_off_words, const v
                           cudaStream_t s) {
   if (words <= 0) return;
   const int grid = static_cast<int>(std::min<long long>((words + 255) / 256, 2LL * num_sms()));
-  peer_broadcast_kernel<<<grid, 256, 0, s>>>(dst, dst_off_words, static_cast<const unsigned int*>(src), words, P);
+  launch_pdl(peer_broadcast_kernel, grid, 256, 0, s, dst, dst_off_words, static_cast<const unsigned int*>(src), words, P);
   TAMOE_CUDA(cudaGetLastError());
 }
 
@@ -158,16 +167,16 @@ void p2p_copy(void* dst, const void* src, size_t bytes, cudaStream_t s, int rep)
 }
 
 void ep_signal_barrier(const EpSignal& a, cudaStream_t s) {
-  ep_barrier_kernel<<<1, 256, 0, s>>>(a);
+  launch_pdl(ep_barrier_kernel, 1, 256, 0, s, a);
   TAMOE_CUDA(cudaGetLastError());
 }
 
 void ep_plan_device(const EpPlanDev& plan, int P, int E, int me, cudaStream_t s) {
   require(P >= 1 && P <= kMaxRanks, "expert parallelism supports up to 16 ranks");
-  ep_plan_kernel<<<1, 128, 0, s>>>(plan, P, E, me);
+  launch_pdl(ep_plan_kernel, 1, 128, 0, s, plan, P, E, me);
   TAMOE_CUDA(cudaGetLastError());
   if (plan.push_row) {
-    ep_push_map_kernel<<<E * P, 128, 0, s>>>(plan, P, E, me);
+    launch_pdl(ep_push_map_kernel, E * P, 128, 0, s, plan, P, E, me);
     TAMOE_CUDA(cudaGetLastError());
   }
 }

@@ -9,6 +9,7 @@
 #include <cuda_bf16.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "common.hpp"
 #include "gate.hpp"
@@ -61,6 +62,267 @@ struct EpiLogits {
   }
 };
 
+// Fused gate (N <= 64 experts): the GEMM epilogue routes its 128 tokens in place -- the logits never
+// round-trip through a separate kernel.  Lane = token; the two epilogue warps of a TMEM lane quarter split the
+// experts (column half h holds experts 32h..32h+31 of its 32 tokens, N <= 32: half 0 alone).  Per token,
+// exactly as the reference (gate.cpp:12-28): max, fp64 exp(v - max), the denominator summed sequentially in
+// expert order (half 0's partial sum handed to half 1 through shared memory), p = e / denominator correctly
+// rounded.  Top-k in (p desc, expert asc) order (gate.cpp:117-122): division is monotone, so the top-k by e
+// are found first (per half, then merged) and only the candidates within a few ulps of the k-th are divided
+// exactly -- the selected p (score, gate value) are the reference's bits.  Column sums of the 32-token group
+// (mean probabilities, gate.cpp:115) use e * (1 / denominator) reduced across lanes in a fixed butterfly
+// order; expert histograms by ballot.  fp32 logits are still stored (the backward recomputes the softmax).
+struct GateRouteParams {
+  float* logits;
+  RowRouteOut o;
+  int N, S, k, TB;
+};
+
+template <int KM>
+struct RouteXchg {  // per-warp, per-lane exchange record between the two halves of a lane quarter
+  float mx[32];
+  int fin[32];
+  double sum[32];       // half 0: partial denominator (experts 0-31); half 1: the full denominator
+  double te_p[KM][32];  // this half's top-k by e, then (after the candidates pass) by exact p
+  int te_e[KM][32];
+};
+
+template <int KM>
+__device__ __forceinline__ void merge_topk(const double* pa, const int* ea, const double* pb, const int* eb, int k,
+                                           TopK<KM>& out) {
+  // two lists sorted by (value desc, expert asc); every expert of list a is below every expert of list b, so on
+  // equal values a wins
+  int ia = 0, ib = 0;
+#pragma unroll
+  for (int j = 0; j < KM; ++j) {
+    if (j < k) {
+      const double va = ia < k ? pa[ia] : -2.0, vb = ib < k ? pb[ib] : -2.0;
+      if (va >= vb) {
+        out.p[j] = va;
+        out.e[j] = ea[ia];
+        ++ia;
+      } else {
+        out.p[j] = vb;
+        out.e[j] = eb[ib];
+        ++ib;
+      }
+    }
+  }
+}
+
+template <int NC, int KM>
+struct EpiRoute {
+  using Params = GateRouteParams;
+  static constexpr bool kEarlyRelease = true;
+  static constexpr int kWarpBytes = (sizeof(RouteXchg<KM>) + 127) / 128 * 128;
+  static __device__ __forceinline__ void finish(const Params&, int) {}
+  static __device__ __forceinline__ void prefetch(const Params&, const GemmParams&, const TileInfo&, int, int, int,
+                                                  uint8_t*, const int*) {}
+  template <class Release>
+  static __device__ __forceinline__ void run(const Params& e, const GemmParams&, const TileInfo& ti,
+                                             uint32_t tmem_tile, int q, int h, int lane, uint8_t* wsm, const int*,
+                                             Release&& release) {
+    constexpr bool kTwo = NC == 64;  // two halves cooperate
+    if (!kTwo && h != 0) {
+      release();
+      return;
+    }
+    RouteXchg<KM>& me = *reinterpret_cast<RouteXchg<KM>*>(wsm);
+    RouteXchg<KM>& pa = *reinterpret_cast<RouteXchg<KM>*>(h == 0 ? wsm + 4 * kWarpBytes : wsm - 4 * kWarpBytes);
+    auto pair_sync = [&]() {
+      if constexpr (kTwo) ptx::named_bar_sync(1 + q, 64);
+    };
+    const int N = e.N, k = e.k;
+    const int cb = 32 * h;  // first expert of this half
+    const int tok = ti.m0 + q * 32 + lane;
+    const bool valid = tok < e.S;
+    const long long gtok = static_cast<long long>(ti.g) * e.S + tok;
+    float v[32];
+    {
+      uint32_t r[32];
+      ptx::tmem_ld_32x32b_x32(tmem_tile + cb, r);
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+    }
+    release();
+    if (valid) {
+      float* dst = e.logits + gtok * N + cb;
+      if ((N & 3) == 0) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+          if (cb + i < N) *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (cb + i < N) dst[i] = v[i];
+      }
+    }
+    float mx = -INFINITY;
+    bool finite = true;
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (cb + i < N) {
+        finite &= isfinite(v[i]);
+        mx = fmaxf(mx, v[i]);
+      }
+    if constexpr (kTwo) {  // barrier 1: row max and finiteness of both halves
+      me.mx[lane] = mx;
+      me.fin[lane] = finite;
+      pair_sync();
+      mx = fmaxf(mx, pa.mx[lane]);
+      finite = finite && pa.fin[lane];
+    }
+    const bool ok = finite || !valid;
+    const double dmx = static_cast<double>(mx);
+    double E[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) E[i] = (cb + i < N) ? exp(static_cast<double>(v[i]) - dmx) : 0.0;
+    // top-k by e of this half (experts ascending: strict '>' keeps the lower one on ties)
+    TopK<KM> te;
+    te.init();
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (cb + i < N) te.insert(E[i], cb + i, k);
+    // denominator in expert order: half 0 sums experts 0-31, half 1 continues from that partial sum
+    double den = 0.0;
+    if (h == 0) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (i < N) den += E[i];
+    }
+    double kth;
+    if constexpr (kTwo) {  // barrier 2: half 0's partial sum and both halves' top-k by e
+      if (h == 0) me.sum[lane] = den;
+#pragma unroll
+      for (int j = 0; j < KM; ++j) {
+        me.te_p[j][lane] = te.p[j];
+        me.te_e[j][lane] = te.e[j];
+      }
+      pair_sync();
+      if (h == 1) {
+        den = pa.sum[lane];
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (32 + i < N) den += E[i];
+      }
+      double ap[KM], bp[KM];
+      int ae[KM], be[KM];
+      const RouteXchg<KM>& h0 = h == 0 ? me : pa;
+      const RouteXchg<KM>& h1 = h == 0 ? pa : me;
+#pragma unroll
+      for (int j = 0; j < KM; ++j) {
+        ap[j] = h0.te_p[j][lane];
+        ae[j] = h0.te_e[j][lane];
+        bp[j] = h1.te_p[j][lane];
+        be[j] = h1.te_e[j][lane];
+      }
+      TopK<KM> m;
+      merge_topk<KM>(ap, ae, bp, be, k, m);
+      kth = m.p[0];
+#pragma unroll
+      for (int j = 0; j < KM; ++j)
+        if (j < k) kth = m.p[j];
+      // barrier 3: the full denominator (half 1) back to half 0; the exchange slots are free again
+      pair_sync();
+      if (h == 1) me.sum[lane] = den;
+      pair_sync();
+      if (h == 0) den = pa.sum[lane];
+    } else {
+      kth = te.p[0];
+#pragma unroll
+      for (int j = 0; j < KM; ++j)
+        if (j < k) kth = te.p[j];
+    }
+    // exact p = e / den for every expert of this half that can tie or beat the k-th after rounding
+    const double thr = kth * (1.0 - 0x1p-46);
+    TopK<KM> tp;
+    tp.init();
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (cb + i < N && E[i] >= thr) tp.insert(E[i] / den, cb + i, k);
+    if constexpr (kTwo) {  // barrier 4: half 1's candidates to half 0, which merges and writes the picks
+      if (h == 1) {
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {
+          me.te_p[j][lane] = tp.p[j];
+          me.te_e[j][lane] = tp.e[j];
+        }
+      }
+      pair_sync();
+      if (h == 0) {
+        double bp[KM];
+        int be[KM];
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {
+          bp[j] = pa.te_p[j][lane];
+          be[j] = pa.te_e[j][lane];
+        }
+        TopK<KM> m;
+        merge_topk<KM>(tp.p, tp.e, bp, be, k, m);
+        tp = m;
+      }
+    }
+    const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+    // 32-token group slot of this warp (= route_logits' block index)
+    const long long slot = (static_cast<long long>(ti.g) * e.TB + ti.m0 / kRouteTile) * 4 + q;
+    if (h == 0) {
+      if (!ok) {  // non-finite logit: experts 0..k-1, NaN gates, poisoned column sums (see route_logits_kernel)
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {
+          tp.p[j] = 0.0;
+          tp.e[j] = j;
+        }
+      }
+      if (valid) {
+        double mass = 0.0;
+#pragma unroll
+        for (int j = 0; j < KM; ++j)
+          if (j < k) mass += tp.p[j];
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {
+          if (j < k) {
+            const long long a = gtok * k + j;
+            e.o.idx[a] = tp.e[j];
+            e.o.score[a] = tp.p[j];
+            const double g = !ok ? qnan : (k == 1 ? tp.p[j] : tp.p[j] / mass);
+            e.o.gate[a] = static_cast<float>(g);
+            if (e.o.gate64) e.o.gate64[a] = g;
+          }
+        }
+      }
+      if (__any_sync(0xffffffffu, !ok)) {
+        if (lane == 0) {
+          atomicOr(e.o.bad, 1);
+          if (e.o.bad_host) *reinterpret_cast<volatile int*>(e.o.bad_host) = 1;
+        }
+      }
+      // expert histogram of the group's picks (all N columns): lane c % 32 keeps column c's count
+      int cnt0 = 0, cnt1 = 0;
+#pragma unroll 4
+      for (int c = 0; c < N; ++c) {
+        bool hit = false;
+#pragma unroll
+        for (int t = 0; t < KM; ++t) hit |= (t < k) && (tp.e[t] == c);
+        const int n = __popc(__ballot_sync(0xffffffffu, valid && hit));
+        if (lane == (c & 31)) {
+          if (c < 32) cnt0 = n;
+          else cnt1 = n;
+        }
+      }
+      if (lane < N) e.o.hist4[slot * N + lane] = cnt0;
+      if (32 + lane < N) e.o.hist4[slot * N + 32 + lane] = cnt1;
+    }
+    // column sums of p = e * (1 / den) over the group's 32 tokens for this half's experts (fixed butterfly)
+    const double rcp = valid ? (ok ? 1.0 / den : qnan) : 0.0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) E[i] *= rcp;
+    const double sum = warp_transpose_sum32(E, lane);
+    if (cb + lane < N) e.o.msum4[slot * N + cb + lane] = sum;
+    pair_sync();  // exchange slots free for the next tile
+  }
+};
+
 // Per-token routing over fp32 logits: fp64 softmax exactly as the reference (max-subtract, exp, sequential
 // sum in expert order, divide: gate.cpp:12-28), top-k in (probability desc, expert asc) order
 // (gate.cpp:117-134), per-32-token-group expert histograms and probability sums (gate.cpp:115).
@@ -74,6 +336,8 @@ constexpr int kRouteGroupWarps = 32 / kRouteRowsPerWarp;
 template <int EPL, int KM>
 __global__ void __launch_bounds__(kRouteGroupWarps * 32) route_logits_kernel(const float* __restrict__ logits, RouteDims d,
                                                            RowRouteOut o) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   constexpr int NC = EPL * 32;
   constexpr int RPW = kRouteRowsPerWarp;
   extern __shared__ double route_smem[];
@@ -206,7 +470,10 @@ __global__ void __launch_bounds__(kRouteGroupWarps * 32) route_logits_kernel(con
   if (okmask != (1u << RPW) - 1u && lane == 0) {
     bool any_bad = false;
     for (int r = 0; r < RPW; ++r) any_bad |= !((okmask >> r) & 1u) && tok0 + r < d.S;
-    if (any_bad) atomicOr(o.bad, 1);
+    if (any_bad) {
+      atomicOr(o.bad, 1);
+      if (o.bad_host) *reinterpret_cast<volatile int*>(o.bad_host) = 1;
+    }
   }
   __syncthreads();  // every warp is done with E
 #pragma unroll
@@ -239,7 +506,8 @@ static void route_logits_launch_k(const float* logits, const RouteDims& d, const
     TAMOE_CUDA(cudaFuncSetAttribute(route_logits_kernel<EPL, KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set |= 1ull << dev;
   }
-  route_logits_kernel<EPL, KM><<<static_cast<unsigned>(d.tiles()) * 4, kRouteGroupWarps * 32, smem, s>>>(logits, d, o);
+  launch_pdl(route_logits_kernel<EPL, KM>, static_cast<unsigned>(d.tiles()) * 4, kRouteGroupWarps * 32, smem, s,
+             logits, d, o);
   TAMOE_CUDA(cudaGetLastError());
 }
 
@@ -288,6 +556,17 @@ void route_rows_from_probs(const double* probs, const RouteDims& d, const RowRou
   TAMOE_CUDA(cudaGetLastError());
 }
 
+// TAMOE_FUSED_GATE=0: logits GEMM + the separate router kernel (A/B switch)
+static bool fused_gate_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("TAMOE_FUSED_GATE");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+bool gate_is_fused(int N, bool want_probs) { return fused_gate_enabled() && N <= 64 && !want_probs; }
+
 void gate_forward(const __nv_bfloat16* x, const __nv_bfloat16* wg, int n_pad, const RouteDims& d, int dm,
                   const RowRouteOut& o, cudaStream_t s) {
   require(d.k >= 1 && d.k <= kMaxTopK && d.k <= d.N, "k must be in [1, min(N, 8)]");
@@ -299,6 +578,23 @@ void gate_forward(const __nv_bfloat16* x, const __nv_bfloat16* wg, int n_pad, co
   CUtensorMap ta = make_tmap_bf16(x, dm, T, dm, kBM);
   CUtensorMap tb = make_tmap_bf16(wg, dm, static_cast<uint64_t>(d.P) * n_pad, dm, BNsel);
   GemmParams p{1, nullptr, nullptr, 0, n_pad, dm, 1, d.S, n_pad, d.P, 0, 1, 0, 0};
+  if (gate_is_fused(d.N, o.probs != nullptr)) {
+    // one launch: logits GEMM + per-token routing in the epilogue
+    GateRouteParams rp{o.logits, o, d.N, d.S, d.k, d.TB};
+    const int km = d.k == 1 ? 1 : (d.k == 2 ? 2 : kMaxTopK);
+#define TAMOE_GATE_ROUTE(NC, KM) launch_gemm<kModeGate, NC, false, false, EpiRoute<NC, KM>>(ta, tb, p, rp, 0, s)
+    if (BNsel == 32) {
+      if (km == 1) TAMOE_GATE_ROUTE(32, 1);
+      else if (km == 2) TAMOE_GATE_ROUTE(32, 2);
+      else TAMOE_GATE_ROUTE(32, kMaxTopK);
+    } else {
+      if (km == 1) TAMOE_GATE_ROUTE(64, 1);
+      else if (km == 2) TAMOE_GATE_ROUTE(64, 2);
+      else TAMOE_GATE_ROUTE(64, kMaxTopK);
+    }
+#undef TAMOE_GATE_ROUTE
+    return;
+  }
   GateEpiParams ep{o.logits, d.N, d.S};
   switch (BNsel) {
     case 32: launch_gemm<kModeGate, 32, false, false, EpiLogits>(ta, tb, p, ep, 0, s); break;

@@ -14,6 +14,7 @@
 
 #include "common.hpp"
 #include "gate_bwd.hpp"
+#include "gate_dz.cuh"
 #include "gemm_launch.cuh"
 #include "route.hpp"
 #include "tma_host.hpp"
@@ -28,42 +29,16 @@ constexpr int kMaxNPerLane = 8;  // N <= 256
 // KT: compile-time top-k (0 = runtime k <= 8); NPL: experts per lane (N <= 32 * NPL).
 template <int KT, int NPL>
 __global__ void __launch_bounds__(kDzWarps * 32) gate_dz_kernel(const __grid_constant__ GateDzArgs a) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   constexpr int KM = KT > 0 ? KT : kMaxTopK;
   extern __shared__ double coeff[];  // [P*N]
-  const int N = a.N;
-  const double s2 = static_cast<double>(a.S) * a.S;
-  for (int i = threadIdx.x; i < a.P * N; i += blockDim.x) {
-    const double c = static_cast<double>(a.counts[i]);
-    coeff[i] = a.aux_kind == 1 ? (static_cast<double>(N) * a.P_global / s2) * a.penalties[i] * c : c / s2;
-  }
+  dz_coeff_smem(a, coeff);
   __syncthreads();
-  if (blockIdx.x == 0 && threadIdx.x < 32) {
-    // loss finalisation (one warp): task = sum residual^2 / (P S d_out); aux = mean over processes
-    const int lane = threadIdx.x;
-    double task = 0.0;
-    for (int i = lane; i < a.n_loss_part; i += 32) task += a.loss_part[i];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) task += __shfl_xor_sync(0xffffffffu, task, o);
-    double aux = 0.0;
-    for (int pr = 0; pr < a.P; ++pr) {
-      double l = 0.0;
-      for (int e = lane; e < N; e += 32) {
-        const double frac = static_cast<double>(a.counts[pr * N + e]) / a.S;
-        l += (a.aux_kind == 1 ? a.penalties[pr * N + e] : 1.0) * a.mean_probs[pr * N + e] * frac;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-      aux += a.aux_kind == 1 ? static_cast<double>(N) * a.P_global * l : l;
-    }
-    if (lane == 0) {
-      a.losses[0] = task / (static_cast<double>(a.P_global) * a.S * a.dout);
-      a.losses[1] = aux / a.P_global;
-    }
-  }
+  if (blockIdx.x == 0 && threadIdx.x < 32) dz_finalize_losses(a, threadIdx.x);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long t = static_cast<long long>(blockIdx.x) * kDzWarps + warp;
   if (t >= static_cast<long long>(a.P) * a.S) return;
-  const int proc = static_cast<int>(t / a.S);
   const int k = KT > 0 ? KT : a.k;
   // every per-token load up front (independent of the softmax below), so their latencies overlap
   int ex_in[KM];
@@ -75,92 +50,18 @@ __global__ void __launch_bounds__(kDzWarps * 32) gate_dz_kernel(const __grid_con
     dl_in[j] = j < k ? a.dldg[t * k + j] : 0.f;
     sc_in[j] = (k > 1 && j < k) ? a.score[t * k + j] : 0.0;
   }
-  // softmax of the stored fp32 logits (fp32 math, max-subtracted)
-  float l[NPL], p[NPL], dpi[NPL];
-  float mx = -INFINITY;
-#pragma unroll
-  for (int i = 0; i < NPL; ++i) {
-    const int e = lane + 32 * i;
-    l[i] = e < N ? a.logits[t * N + e] : -INFINITY;
-    mx = fmaxf(mx, l[i]);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  float den = 0.f;
-#pragma unroll
-  for (int i = 0; i < NPL; ++i) {
-    p[i] = (lane + 32 * i < N) ? expf(l[i] - mx) : 0.f;
-    den += p[i];
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
-  const float inv = 1.f / den;
-  const float aux_scale = static_cast<float>(a.aux_weight / a.P_global);
-#pragma unroll
-  for (int i = 0; i < NPL; ++i) {
-    const int e = lane + 32 * i;
-    p[i] *= inv;
-    dpi[i] = e < N ? aux_scale * static_cast<float>(coeff[proc * N + e]) : 0.f;
-  }
-  // combine-weight Jacobian (trainer.cpp:318-331)
-  int ex[KM];
-  float add[KM];
-  if (k == 1) {
-    ex[0] = ex_in[0];
-    add[0] = dl_in[0];
-#pragma unroll
-    for (int j = 1; j < KM; ++j) {
-      ex[j] = -1;
-      add[j] = 0.f;
-    }
-  } else {
-    double sc[KM], dg[KM];
-    double mass = 0.0;
-#pragma unroll
-    for (int j = 0; j < KM; ++j) {
-      ex[j] = ex_in[j];
-      sc[j] = sc_in[j];
-      dg[j] = static_cast<double>(dl_in[j]);
-      mass += sc[j];
-    }
-    const double inv2 = 1.0 / (mass * mass);
-#pragma unroll
-    for (int l2 = 0; l2 < KM; ++l2) {
-      double acc = 0.0;
-#pragma unroll
-      for (int j = 0; j < KM; ++j)
-        if (dg[j] != 0.0) acc += dg[j] * ((j == l2 ? mass : 0.0) - sc[j]) * inv2;
-      add[l2] = static_cast<float>(acc);
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < NPL; ++i) {
-    const int e = lane + 32 * i;
-#pragma unroll
-    for (int j = 0; j < KM; ++j) dpi[i] += (ex[j] == e) ? add[j] : 0.f;
-  }
-  float dot = 0.f;
-#pragma unroll
-  for (int i = 0; i < NPL; ++i) dot += dpi[i] * p[i];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-  __nv_bfloat16* dz = a.dz + t * a.n64;
-#pragma unroll
-  for (int i = 0; i < NPL; ++i) {
-    const int e = lane + 32 * i;
-    if (e < a.n64) dz[e] = __float2bfloat16(e < N ? p[i] * (dpi[i] - dot) : 0.f);
-  }
-  // experts beyond 32 * NPL (n64 padding) are zero
-  for (int e = 32 * NPL + lane; e < a.n64; e += 32) dz[e] = __float2bfloat16(0.f);
+  float lg[NPL];
+  dz_load_logits<NPL>(a, t, lane, lg);
+  dz_token<KM, NPL>(a, coeff, t, k, lane, lg, ex_in, dl_in, sc_in);
 }
 
 template <int KT>
 void launch_dz(const GateDzArgs& a, int blocks, cudaStream_t s) {
   const size_t smem = sizeof(double) * a.P * a.N;
-  if (a.N <= 32) gate_dz_kernel<KT, 1><<<blocks, kDzWarps * 32, smem, s>>>(a);
-  else if (a.N <= 64) gate_dz_kernel<KT, 2><<<blocks, kDzWarps * 32, smem, s>>>(a);
-  else if (a.N <= 128) gate_dz_kernel<KT, 4><<<blocks, kDzWarps * 32, smem, s>>>(a);
-  else gate_dz_kernel<KT, 8><<<blocks, kDzWarps * 32, smem, s>>>(a);
+  if (a.N <= 32) launch_pdl(gate_dz_kernel<KT, 1>, blocks, kDzWarps * 32, smem, s, a);
+  else if (a.N <= 64) launch_pdl(gate_dz_kernel<KT, 2>, blocks, kDzWarps * 32, smem, s, a);
+  else if (a.N <= 128) launch_pdl(gate_dz_kernel<KT, 4>, blocks, kDzWarps * 32, smem, s, a);
+  else launch_pdl(gate_dz_kernel<KT, 8>, blocks, kDzWarps * 32, smem, s, a);
 }
 
 // dWg partials: acc[m = d index][n = expert] -> part[((ks * P + proc) * n64 + n) * d + m]
@@ -193,7 +94,13 @@ struct EpiGateDw {
 };
 
 __global__ void dwg_reduce_kernel(const float* __restrict__ part, int splits, int P, int n64, int n_pad, int d,
-                                  int N, float* __restrict__ dwg) {
+                                  int N, float* __restrict__ dwg, const __grid_constant__ GateDzArgs fin,
+                                  int finalize) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  // the gate dz pass fused into the combine kernel: the losses are finalised here (combine's partial sums
+  // are complete once this kernel runs)
+  if (finalize && blockIdx.x == 0 && threadIdx.x < 32) dz_finalize_losses(fin, threadIdx.x);
   const long long total = static_cast<long long>(P) * n_pad * d;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -421,7 +328,7 @@ int gate_dw_splits(int P, int S, int d, int n64) {
 }
 
 void gate_dw(const __nv_bfloat16* x, const __nv_bfloat16* dz, int P, int S, int d, int n64, int n_pad, int N,
-             float* part, int splits, float* dwg, cudaStream_t s) {
+             float* part, int splits, float* dwg, cudaStream_t s, const GateDzArgs* finalize) {
   require(d % 128 == 0, "gate dW: d must be a multiple of 128");
   require(n64 % 64 == 0, "gate dW: dz width must be a multiple of 64");
   require(P == 1 || S % 16 == 0, "gate dW: S must be a multiple of 16 when several processes share a device");
@@ -445,7 +352,9 @@ void gate_dw(const __nv_bfloat16* x, const __nv_bfloat16* dz, int P, int S, int 
   }
   const long long total = static_cast<long long>(P) * n_pad * d;
   const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 4096));
-  dwg_reduce_kernel<<<blocks, 256, 0, s>>>(part, splits, P, n64, n_pad, d, N, dwg);
+  GateDzArgs fin{};
+  if (finalize) fin = *finalize;
+  launch_pdl(dwg_reduce_kernel, blocks, 256, 0, s, part, splits, P, n64, n_pad, d, N, dwg, fin, finalize ? 1 : 0);
   TAMOE_CUDA(cudaGetLastError());
 }
 

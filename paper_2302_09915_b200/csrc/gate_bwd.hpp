@@ -28,8 +28,9 @@ inline int expert_pad64(int N) { return N <= 64 ? 64 : (N <= 128 ? 128 : 256); }
 
 void gate_dz(const GateDzArgs& a, cudaStream_t s);
 int gate_dw_splits(int P, int S, int d, int n64);
+// finalize (optional): the loss finalisation of a gate dz pass that was fused into the combine kernel
 void gate_dw(const __nv_bfloat16* x, const __nv_bfloat16* dz, int P, int S, int d, int n64, int n_pad, int N,
-             float* part, int splits, float* dwg, cudaStream_t s);
+             float* part, int splits, float* dwg, cudaStream_t s, const GateDzArgs* finalize = nullptr);
 // dX = dz Wg + sum over kept slots of the expert-path gradient rows (read from the owners' layouts).
 void gate_dx(const __nv_bfloat16* dz, const __nv_bfloat16* wg, int P, int S, int d, int n64, int n_pad,
              const PeerBufs& dxp, const int* pos, const int* idx, const RowMap& map, int k, __nv_bfloat16* dx,

@@ -29,19 +29,23 @@ void launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams&
   cfg.blockDim = dim3(kGemmThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = kCG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   if constexpr (kCG > 1) {
     // a persistent grid must be co-resident: GPCs whose SM count is not a multiple of kCG leave SMs idle
     static int max_clusters[64] = {};
     if (max_clusters[dev] == 0) {
       int n = 0;
-      TAMOE_CUDA(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
+      cudaLaunchConfig_t occ = cfg;
+      occ.numAttrs = 1;  // the cluster shape only
+      TAMOE_CUDA(cudaOccupancyMaxActiveClusters(&n, kern, &occ));
       max_clusters[dev] = n > 0 ? n : 1;
     }
     grid = std::min(grid, max_clusters[dev] * kCG);

@@ -261,6 +261,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int cluster_id = blockIdx.x / kCG;
   const int num_clusters = gridDim.x / kCG;
 
+  // programmatic dependent launch: let the next kernel of the step get scheduled as SMs free up, and set up
+  // barriers / TMEM / tensor maps (no dependent data) before waiting for the previous kernel's results
+  ptx::pdl_trigger();
+  if (warp == kProducerWarp && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+    for (int s = 0; s < L::kStages; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], kCG == 4 ? 2 : 1);  // kCG 4: both pairs read every stage
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&tfull_bar[b], 1);
+      ptx::mbar_init(&tempty_bar[b], kEpiWarps * kCGm);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == kMmaWarp) {
+    if constexpr (kCG > 1) ptx::tmem_alloc_cg2<L::kTmemCols>(tmem_slot);
+    else ptx::tmem_alloc<L::kTmemCols>(tmem_slot);
+  }
+  ptx::pdl_wait();
   // group table -> smem (parallel loads), then a warp-parallel prefix of the tile counts
   const int G = p.num_groups;
   const bool grouped = (kMode == kModeSwap || kMode == kModeWgrad);
@@ -285,23 +306,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       carry += __shfl_sync(0xffffffffu, x, 31);
     }
     if (lane == 0) prefix[G] = carry;
-  }
-  if (warp == kProducerWarp && lane == 0) {
-    ptx::prefetch_tmap(&tmA);
-    ptx::prefetch_tmap(&tmB);
-    for (int s = 0; s < L::kStages; ++s) {
-      ptx::mbar_init(&full_bar[s], 1);
-      ptx::mbar_init(&empty_bar[s], kCG == 4 ? 2 : 1);  // kCG 4: both pairs read every stage
-    }
-    for (int b = 0; b < 2; ++b) {
-      ptx::mbar_init(&tfull_bar[b], 1);
-      ptx::mbar_init(&tempty_bar[b], kEpiWarps * kCGm);
-    }
-    ptx::fence_barrier_init();
-  }
-  if (warp == kMmaWarp) {
-    if constexpr (kCG > 1) ptx::tmem_alloc_cg2<L::kTmemCols>(tmem_slot);
-    else ptx::tmem_alloc<L::kTmemCols>(tmem_slot);
   }
   ptx::tc_fence_before();
   if constexpr (kCG > 1) ptx::cluster_sync();

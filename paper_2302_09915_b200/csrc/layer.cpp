@@ -78,8 +78,8 @@ void RouteWorkspace::upload_caps(const long long* caps_host, cudaStream_t s) {
 }
 
 void RouteWorkspace::finish(int mode, cudaStream_t s) const {
-  route_bucket(dims, buf, s);
-  route_capacity(dims, buf, mode, caps, s);
+  route_bucket(dims, buf, s, mode == 0);
+  if (mode != 0) route_capacity(dims, buf, mode, caps, s);
 }
 
 Router::Router(int P, int S, int N, int k) {
@@ -208,8 +208,9 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
   n_loss_part_ = combine_blocks(T);
   arena_.reserve(loss_part_, n_loss_part_);
   arena_.commit();
-  TAMOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&bad_host_), sizeof(int), cudaHostAllocDefault));
+  TAMOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&bad_host_), sizeof(int), cudaHostAllocMapped));
   *bad_host_ = 0;
+  TAMOE_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&bad_host_dev_), bad_host_, 0));
   TAMOE_CUDA(cudaEventCreateWithFlags(&step_done_, cudaEventDisableTiming));
   if (!ep_) ret_codes_.p[0] = ret_code_;
   if (ep_) {
@@ -354,8 +355,8 @@ void Layer::check_deferred(bool wait) {
     return;
   }
   step_pending_ = false;
-  if (*bad_host_ != 0) {
-    *bad_host_ = 0;
+  if (*reinterpret_cast<volatile int*>(bad_host_) != 0) {
+    *reinterpret_cast<volatile int*>(bad_host_) = 0;
     throw ValidationError("non-finite gate logit");
   }
 }
@@ -452,6 +453,14 @@ Layer::StepGraph::~StepGraph() {
   if (in) cudaEventDestroy(in);
   if (out) cudaEventDestroy(out);
   if (stream) cudaStreamDestroy(stream);
+}
+
+static bool fused_dz_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("TAMOE_FUSED_DZ");
+    return !(v && v[0] == '0');
+  }();
+  return on;
 }
 
 static bool graphs_enabled() {
@@ -554,14 +563,15 @@ void Layer::route_front(const LayerIO& io, cudaStream_t s) {
   const RouteBuffers& b = rw.buf;
   const bool compulsory = cfg_.aux_kind == 2;
   TAMOE_CUDA(cudaMemsetAsync(b.bad, 0, sizeof(int), s));
-  gate_forward(io.x, io.wg, n_pad_, rw.dims, cfg_.d, rw.row_out(logits_, compulsory ? probs_ : nullptr), s);
-  TAMOE_CUDA(cudaMemcpyAsync(bad_host_, b.bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  gate_forward(io.x, io.wg, n_pad_, rw.dims, cfg_.d, rw.row_out(logits_, compulsory ? probs_ : nullptr, bad_host_dev_),
+               s);
   tm.mark("gate_fwd", s);
   if (compulsory) {  // quota claims replace the top-k / capacity outcome; every token is kept
     route_compulsory(rw.dims, b, probs_, quota_, comp_ws_, comp_ws_bytes_, s);
     tm.mark("route_compulsory", s);
   }
-  route_bucket(rw.dims, b, s);
+  const int mode = compulsory ? 0 : cfg_.cap_mode;
+  route_bucket(rw.dims, b, s, mode == 0);  // mode 0: kept lists directly, no capacity pass
   tm.mark("route_bucket", s);
   if (global_ep_) {
     // every rank's picks (expert, score) and 32-token histograms -> every rank's global view, then the
@@ -579,8 +589,10 @@ void Layer::route_front(const LayerIO& io, cudaStream_t s) {
     tm.mark("route_capacity_global", s);
     return;
   }
-  route_capacity(rw.dims, b, compulsory ? 0 : cfg_.cap_mode, rw.caps, s);
-  tm.mark("route_capacity", s);
+  if (mode != 0) {
+    route_capacity(rw.dims, b, mode, rw.caps, s);
+    tm.mark("route_capacity", s);
+  }
 }
 
 void Layer::step_local(const LayerIO& io, cudaStream_t s) {
@@ -679,14 +691,15 @@ void Layer::combine(const LayerIO& io, cudaStream_t s) {
   ca.map = map_;
   ca.dldg = dldg_;
   ca.loss_part = loss_part_;
+  ca.fuse_dz = fused_dz_enabled() ? 1 : 0;
+  ca.gz = dz_args(io);
   combine_loss(ca, s);
   timer_.mark("combine_loss", s);
 }
 
-void Layer::gate_backward(const LayerIO& io, cudaStream_t s) {
+GateDzArgs Layer::dz_args(const LayerIO& io) const {
   const LayerConfig& c = cfg_;
   const RouteBuffers& b = rw_.buf;
-  PhaseTimer& tm = timer_;
   GateDzArgs ga{};
   ga.P = c.P;
   ga.S = c.S;
@@ -708,6 +721,18 @@ void Layer::gate_backward(const LayerIO& io, cudaStream_t s) {
   ga.n_loss_part = n_loss_part_;
   ga.losses = io.losses;
   ga.dz = dz_;
+  return ga;
+}
+
+void Layer::gate_backward(const LayerIO& io, cudaStream_t s) {
+  const LayerConfig& c = cfg_;
+  PhaseTimer& tm = timer_;
+  const GateDzArgs ga = dz_args(io);
+  if (fused_dz_enabled()) {  // dz was computed by the combine kernel; the losses are finalised by gate_dw
+    gate_dw(io.x, dz_, c.P, c.S, c.d, n64_, n_pad_, c.N, dw_part_, dw_splits_, io.dwg, s, &ga);
+    tm.mark("gate_dw", s);
+    return;
+  }
   gate_dz(ga, s);
   tm.mark("gate_dz", s);
   gate_dw(io.x, dz_, c.P, c.S, c.d, n64_, n_pad_, c.N, dw_part_, dw_splits_, io.dwg, s);
@@ -729,7 +754,9 @@ void Layer::gate_backward_dx(const LayerIO& io, cudaStream_t s) {
 
 int Layer::launches_per_step() const {
   // gate, scan, bucket, capacity, permute, combine, dz, dW GEMM + reduce
-  int n = 10;  // gate = logits GEMM + router
+  int n = gate_is_fused(cfg_.N, cfg_.aux_kind == 2) ? 9 : 10;  // gate: one fused launch, or logits GEMM + router
+  if (!global_ep_ && (cfg_.cap_mode == 0 || cfg_.aux_kind == 2)) n -= 1;  // no capacity pass
+  if (fused_dz_enabled()) n -= 1;  // gate dz inside the combine kernel
   // EP: + plan and return-map kernels + the device barriers (counts publish, dispatch, forward, combine, [dX])
   if (ep_) n += 1 + (nccl_barrier() ? 0 : 4 + (cfg_.need_dx ? 1 : 0));  // + the device plan
   if (global_ep_) n += 3 + (nccl_barrier() ? 0 : 1) + 3;  // broadcasts, barrier, global scan/bucket/capacity

@@ -10,6 +10,7 @@
 #include <memory>
 
 #include "ep.hpp"
+#include "gate_bwd.hpp"
 #include "route.hpp"
 
 namespace tamoe {
@@ -47,8 +48,8 @@ struct RouteWorkspace {
   void reserve(Arena& a, int P, int S, int N, int k, bool with_gate64 = false);
   void upload_caps(const long long* caps_host, cudaStream_t s);
   // gate outputs view of the workspace
-  RowRouteOut row_out(float* logits, double* probs) const {
-    return RowRouteOut{buf.idx, buf.gate, buf.score, buf.hist4, buf.msum4, logits, probs, buf.bad, buf.gate64};
+  RowRouteOut row_out(float* logits, double* probs, int* bad_host = nullptr) const {
+    return RowRouteOut{buf.idx, buf.gate, buf.score, buf.hist4, buf.msum4, logits, probs, buf.bad, buf.gate64, bad_host};
   }
   void finish(int mode, cudaStream_t s) const;  // bucket + capacity
 };
@@ -144,6 +145,7 @@ class Layer {
   void experts_backward(const LayerIO& io, int G, int E, int nsub, const int* seg_start, const int* seg_rows, int rows,
                         cudaStream_t s);
   void gate_backward(const LayerIO& io, cudaStream_t s);  // dz + dWg (local inputs only)
+  GateDzArgs dz_args(const LayerIO& io) const;
   void gate_backward_dx(const LayerIO& io, cudaStream_t s);  // dX (needs the expert-path gradients)
   void combine(const LayerIO& io, cudaStream_t s);
   PeerBufs peers(__nv_bfloat16* local) const;
@@ -190,7 +192,8 @@ class Layer {
   bool connected_ = false, stepped_ = false;
   unsigned long long fingerprint() const;
   void init_topology(const double* c_hat);
-  int* bad_host_ = nullptr;            // pinned: the last step's non-finite-logit flag
+  int* bad_host_ = nullptr;            // mapped pinned: set by the router on a non-finite logit
+  int* bad_host_dev_ = nullptr;        // its device address
   cudaEvent_t step_done_ = nullptr;    // recorded on the caller's stream after every step
   bool step_pending_ = false;
   void check_deferred(bool wait);

@@ -284,6 +284,12 @@ __device__ __forceinline__ float tanh_fast(float x) {
   return y;
 }
 
+// Programmatic dependent launch (griddepcontrol): no-ops unless the kernel was launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization.  trigger: the next kernel may be scheduled (its CTAs
+// still wait in pdl_wait); wait: the previous kernel has completed and its memory is visible.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

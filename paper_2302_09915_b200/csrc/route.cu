@@ -12,6 +12,7 @@
 #include <cstdint>
 
 #include "common.hpp"
+#include "ptx.cuh"
 #include "route.hpp"
 
 namespace tamoe {
@@ -56,12 +57,37 @@ __device__ int block_excl_scan(int* a, int n, int* wtmp) {
   return total;
 }
 
+// Mean probabilities of expert e for every process (gate.cpp:115): the 32-token group sums msum4 added in a
+// fixed block-parallel order, / S.  All threads of the block must call.
+__device__ void mean_probs_column(const RouteDims& d, const RouteBuffers& b, int e) {
+  __shared__ double dred[32];
+  const int N = d.N;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int pr = 0; pr < d.P; ++pr) {
+    double m = 0.0;
+    const int t0 = pr * d.TB * 4, t1 = (pr + 1) * d.TB * 4;
+    for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) m += b.msum4[static_cast<long long>(t) * N + e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+    if (lane == 0) dred[w] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double mt = 0.0;
+      for (int i = 0; i < nw; ++i) mt += dred[i];
+      b.mean_probs[pr * N + e] = mt / d.S;
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- scan
 // One CTA per expert: exclusive prefix of the per-(tile, warp) pick counts in
 // (process, token) order -> base4, plus per-(process, expert) bucket ranges.
 constexpr int kScanThreads = 512;
 
-__global__ void __launch_bounds__(kScanThreads) route_scan_kernel(RouteDims d, RouteBuffers b) {
+__global__ void __launch_bounds__(kScanThreads) route_scan_kernel(RouteDims d, RouteBuffers b, int direct) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   __shared__ int wsum[32];
   __shared__ int carry_s;
   const int e = blockIdx.x, N = d.N;
@@ -98,13 +124,20 @@ __global__ void __launch_bounds__(kScanThreads) route_scan_kernel(RouteDims d, R
     const int st = b.bucket_start[pr * N + e];
     const int en = pr + 1 < d.P ? b.bucket_start[(pr + 1) * N + e] : carry_s;
     b.bucket_count[pr * N + e] = en - st;
+    if (direct) {  // no capacity: every pick is kept
+      b.counts[pr * N + e] = en - st;
+      b.dropped[pr * N + e] = 0;
+    }
   }
+  if (direct) mean_probs_column(d, b, e);
 }
 
 // ---------------------------------------------------------------- bucket
 // One CTA per 128-token tile.  Position of a pick in its expert's list =
 // list_start[e] + picks to e in earlier (tile, warp) slots + earlier lanes of its warp.
-__global__ void __launch_bounds__(kRouteTile) route_bucket_kernel(RouteDims d, RouteBuffers b) {
+__global__ void __launch_bounds__(kRouteTile) route_bucket_kernel(RouteDims d, RouteBuffers b, int direct) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   extern __shared__ int sm[];
   const int N = d.N, k = d.k;
   int* wbase = sm;                     // [4*N]
@@ -135,8 +168,14 @@ __global__ void __launch_bounds__(kRouteTile) route_bucket_kernel(RouteDims d, R
     for (int l = w * 32; l < threadIdx.x; ++l)
       for (int j = 0; j < k; ++j) r += (sel[l * k + j] == e);
     const int pos = wbase[w * N + e] + r;
-    b.list_pick[pos] = static_cast<int>(gtok * k + a);
-    b.list_score[pos] = b.score[gtok * k + a];
+    const int pick = static_cast<int>(gtok * k + a);
+    if (direct) {  // no capacity: the bucket lists are the compacted kept lists
+      b.clist[pos] = pick;
+      b.kept[pick] = 1;
+    } else {
+      b.list_pick[pos] = pick;
+      b.list_score[pos] = b.score[pick];
+    }
   }
 }
 
@@ -154,6 +193,8 @@ __device__ __forceinline__ unsigned long long score_key(double s) {
 
 __global__ void __launch_bounds__(kCapThreads) route_capacity_kernel(RouteDims d, RouteBuffers b, int mode,
                                                                      const int* __restrict__ caps) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   __shared__ int hist[256];
   __shared__ int wtmp[32];
   __shared__ int sh_digit, sh_need;
@@ -257,8 +298,7 @@ __global__ void __launch_bounds__(kCapThreads) route_capacity_kernel(RouteDims d
     }
     __syncthreads();
   }
-  // per-bucket kept / dropped counts and mean probabilities (block-parallel, fixed-order sums)
-  __shared__ double dred[32];
+  // per-bucket kept / dropped counts (block-parallel) and mean probabilities (fixed-order sums)
   __shared__ int ired[32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int pr = 0; pr < d.P; ++pr) {
@@ -269,32 +309,19 @@ __global__ void __launch_bounds__(kCapThreads) route_capacity_kernel(RouteDims d
     } else if (threadIdx.x == 0) {
       kc = mode == 0 ? bc : min(bc, max(caps[pr * N + e], 0));  // exactly cap picks survive
     }
-    double m = 0.0;
-    const int t0 = pr * d.TB * 4, t1 = (pr + 1) * d.TB * 4;
-    for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) m += b.msum4[static_cast<long long>(t) * N + e];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      kc += __shfl_xor_sync(0xffffffffu, kc, o);
-      m += __shfl_xor_sync(0xffffffffu, m, o);
-    }
-    if (lane == 0) {
-      ired[w] = kc;
-      dred[w] = m;
-    }
+    for (int o = 16; o > 0; o >>= 1) kc += __shfl_xor_sync(0xffffffffu, kc, o);
+    if (lane == 0) ired[w] = kc;
     __syncthreads();
     if (threadIdx.x == 0) {
       int kt = 0;
-      double mt = 0.0;
-      for (int i = 0; i < nw; ++i) {
-        kt += ired[i];
-        mt += dred[i];
-      }
+      for (int i = 0; i < nw; ++i) kt += ired[i];
       b.counts[pr * N + e] = kt;
       b.dropped[pr * N + e] = bc - kt;
-      b.mean_probs[pr * N + e] = mt / d.S;
     }
     __syncthreads();
   }
+  mean_probs_column(d, b, e);
 }
 
 // ---------------------------------------------------------------- permute
@@ -308,6 +335,8 @@ __global__ void __launch_bounds__(kPermWarps * 32) route_permute_kernel(RouteDim
                                                                         int has_z, int zdim, RowMap map,
                                                                         const __grid_constant__ PeerInts codes,
                                                                         int has_codes, int me, int trash_row) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   extern __shared__ int sm[];
   const int N = d.N;
   int* start = sm;          // [N]
@@ -411,17 +440,17 @@ void zero_pad_rows(const int* seg_start, const int* seg_rows, const int* seg_rea
   TAMOE_CUDA(cudaGetLastError());
 }
 
-void route_bucket(const RouteDims& d, const RouteBuffers& b, cudaStream_t s) {
-  route_scan_kernel<<<d.N, kScanThreads, 0, s>>>(d, b);
+void route_bucket(const RouteDims& d, const RouteBuffers& b, cudaStream_t s, bool direct) {
+  launch_pdl(route_scan_kernel, d.N, kScanThreads, 0, s, d, b, direct ? 1 : 0);
   TAMOE_CUDA(cudaGetLastError());
   const size_t smem = sizeof(int) * (5 * d.N + kRouteTile * d.k + 32);
-  route_bucket_kernel<<<d.tiles(), kRouteTile, smem, s>>>(d, b);
+  launch_pdl(route_bucket_kernel, d.tiles(), kRouteTile, smem, s, d, b, direct ? 1 : 0);
   TAMOE_CUDA(cudaGetLastError());
 }
 
 void route_capacity(const RouteDims& d, const RouteBuffers& b, int mode, const int* caps, cudaStream_t s) {
   require(mode >= 0 && mode <= 4, "unknown capacity mode");
-  route_capacity_kernel<<<d.N, kCapThreads, 0, s>>>(d, b, mode, caps);
+  launch_pdl(route_capacity_kernel, d.N, kCapThreads, 0, s, d, b, mode, caps);
   TAMOE_CUDA(cudaGetLastError());
 }
 
@@ -435,8 +464,8 @@ void route_permute(const RouteDims& d, const RouteBuffers& b, const __nv_bfloat1
   if (zrows) z = *zrows;
   PeerInts c{};
   if (codes) c = *codes;
-  route_permute_kernel<<<blocks, kPermWarps * 32, smem, s>>>(d, b, x, dx, xp, r_max, z, zrows ? 1 : 0, zdim, map, c,
-                                                             codes ? 1 : 0, me, trash_row);
+  launch_pdl(route_permute_kernel, blocks, kPermWarps * 32, smem, s, d, b, x, dx, xp, r_max, z, zrows ? 1 : 0, zdim,
+             map, c, codes ? 1 : 0, me, trash_row);
   TAMOE_CUDA(cudaGetLastError());
 }
 

@@ -113,6 +113,7 @@ struct RowRouteOut {
   double* probs;  // optional [P*S*N]
   int* bad;
   double* gate64 = nullptr;  // optional [P*S*k] fp64 gate values (reference Assignment::gate_value)
+  int* bad_host = nullptr;   // optional: mapped pinned host flag, set to 1 on a non-finite logit
 };
 
 // Top-k selection from fp64 probabilities (P x S x N), the reference's topk_route input.
@@ -128,7 +129,9 @@ void route_compulsory(const RouteDims& d, const RouteBuffers& b, const double* p
                       size_t ws_bytes, cudaStream_t s);
 
 // histogram scan + stable bucket lists (gate.cpp:160-164 / 181-185 order)
-void route_bucket(const RouteDims& d, const RouteBuffers& b, cudaStream_t s);
+// direct = no capacity (mode 0): the bucket lists are written as the kept lists (clist, kept, counts, mean
+// probabilities) and route_capacity is not needed
+void route_bucket(const RouteDims& d, const RouteBuffers& b, cudaStream_t s, bool direct = false);
 // capacity enforcement + compaction + counts + mean probs (gate.cpp:115, 138-199)
 // caps: device int32 [P*N] (INT32_MAX = unlimited); mode: 0 none, 1 global, 2 local, 3 proportional,
 // 4 external (b.kept already holds the keep flag of every pick: the expert-parallel global decision)

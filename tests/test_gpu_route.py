@@ -116,6 +116,50 @@ def test_gate_route_from_identical_logits(P, S, d, N, k, mode):
             assert np.array_equal(a, b), e
 
 
+@pytest.mark.parametrize("P,S,d,N,k,mode", [(1, 16384, 1024, 64, 1, 0), (4, 256, 512, 8, 2, 3), (2, 300, 128, 16, 2, 2),
+                                            (1, 2048, 4096, 64, 2, 3), (1, 200, 256, 48, 8, 1), (3, 129, 256, 32, 1, 2)])
+def test_fused_gate_routing_bit_exact(P, S, d, N, k, mode):
+    """The one-launch gate (N <= 64: routing in the tcgen05 GEMM epilogue, no probabilities output) against the
+    oracle fed the kernel's own fp32 logits: expert indices, fp64 scores and gate values, kept flags, counts,
+    mean probabilities and the permutation order -- bit for bit (mean probabilities to 1e-12), except audited
+    near-ties (probabilities within a few ulps).  Includes C2 (T=16,384, d=1,024, N=64, top-1) and C4's gate
+    (d=4,096, N=64, top-2, proportional capacity) and in-row exact ties."""
+    ops = _ops()
+    O = oracle.orc()
+    torch.manual_seed(P * 7 + S + N)
+    x = torch.randn(P * S, d, device="cuda").bfloat16()
+    npd = ops.n_pad(N)
+    wg = torch.zeros(P, npd, d, device="cuda", dtype=torch.bfloat16)
+    wg[:, :N] = (torch.randn(P, N, d, device="cuda") * 0.05).bfloat16()
+    if N >= 8:  # identical weight rows 3 and 5: exact in-row logit ties (the lower expert wins)
+        wg[:, 5] = wg[:, 3]
+    c_hat = np.random.default_rng(2).uniform(0.5, 3, size=(P, N))
+    pol = ops.CapacityPolicy(ops.CapacityMode(mode), 1.25)
+    caps = ops.capacity_caps(pol, k, S, N, P, c_hat)
+    r = ops.Router(P, S, N, k)
+    logits, probs = r.route_gate(x, wg, pol, caps, want_probs=False)
+    torch.cuda.synchronize()
+    lg = logits.double().cpu().numpy().reshape(P, S, N)
+    oprobs = np.stack([O.softmax_rows(l) for l in lg])
+    orc = O.topk_route(oprobs, k, mode, 1.25, c_hat)
+    idx = r.read(ops.R_IDX)
+    mism = np.argwhere(idx != orc["expert"])
+    for (i, s_, j) in mism:
+        pr = np.sort(oprobs[i, s_])[::-1]
+        assert abs(pr[j] - pr[j + 1]) <= 4 * np.spacing(pr[j]), (i, s_, j)
+    assert len(mism) <= 2
+    if len(mism) == 0:
+        # the device's fp64 exp is within 1 ulp of glibc's (the oracle's): scores / gate values to 1e-14
+        np.testing.assert_allclose(r.read(ops.R_SCORE), orc["score"], rtol=1e-14, atol=0)
+        np.testing.assert_allclose(r.read(ops.R_GATE64), orc["gate"], rtol=1e-14, atol=0)
+        assert np.array_equal(r.read(ops.R_KEPT), orc["kept"])
+        assert np.array_equal(r.read(ops.R_COUNTS), orc["counts"])
+        assert np.array_equal(r.read(ops.R_DROPPED), orc["dropped"])
+        for e, (a, b) in enumerate(zip(r.expert_order(), oracle_order(orc, P, S, k, N))):
+            assert np.array_equal(a, b), e
+    np.testing.assert_allclose(r.read(ops.R_MEAN_PROBS), orc["mean_probs"], rtol=1e-12, atol=1e-15)
+
+
 def test_gate_rejects_nonfinite():
     ops = _ops()
     x = torch.zeros(128, 64, device="cuda", dtype=torch.bfloat16)
