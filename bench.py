@@ -154,6 +154,45 @@ class ClockSampler:
                 "samples": len(self.rows), "source": "nvml, 1 ms period, timed region only"}
 
 
+class NvlinkCounters:
+    """NVLink data-payload byte counters of this GPU (NVML field values NVLINK_THROUGHPUT_DATA_TX / _RX, per link,
+    cumulative KiB), read around the timed region: hardware evidence for the exchange's off-rank bytes, without a
+    profiler on the multi-rank run."""
+
+    def __init__(self, cuda_index, links=18):
+        self.h = None
+        self.err = None
+        try:
+            import pynvml as nv
+            import torch
+            nv.nvmlInit()
+            self.nv = nv
+            pr = torch.cuda.get_device_properties(cuda_index)
+            self.h = nv.nvmlDeviceGetHandleByPciBusId(
+                f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0")
+            self.fields = [(f, l) for l in range(links)
+                           for f in (nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX)]
+            self.read()
+        except Exception as e:  # noqa: BLE001
+            self.h, self.err = None, f"nvml nvlink counters unavailable: {e}"
+
+    def read(self):
+        """(tx_bytes, rx_bytes) summed over the links."""
+        if self.h is None:
+            return None
+        vals = self.nv.nvmlDeviceGetFieldValues(self.h, self.fields)
+        tx = rx = 0
+        for i, v in enumerate(vals):
+            if v.nvmlReturn != 0:
+                continue
+            x = v.value.ullVal * 1024
+            if i % 2 == 0:
+                tx += x
+            else:
+                rx += x
+        return tx, rx
+
+
 # ------------------------------------------------------------------------------------------ CPU baseline
 def host_threads(bytes_per_thread=1.6e9):
     """The host cores this process may use (up to 64), bounded by memory: each concurrent reference train() at the C2
@@ -371,18 +410,22 @@ def main():
     # NVML set-up and events before the barrier: any host work between the barrier and the first timed launch
     # on one rank is time the other ranks' GPUs spend in the step's device barrier (max over ranks)
     clk = ClockSampler(local)
+    nvl = NvlinkCounters(local) if world > 1 else None
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()
     with clk:
         # one untimed step enqueued ahead of ev0: its device barriers re-align the ranks' GPUs after any host skew
         layer.step(x, y, params)
+        torch.cuda.synchronize()
+        nvl0 = nvl.read() if nvl else None
         ev0.record(stream)
         for _ in range(args.steps):
             layer.step(x, y, params)
         ev1.record(stream)
         clk.sample_now()  # after ev1 is enqueued: an NVML call between launches stalls this rank's stream
         torch.cuda.synchronize()
+        nvl1 = nvl.read() if nvl else None
     barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     clocks = clk.summary()
@@ -421,6 +464,21 @@ def main():
         for kk in ("dispatch", "combine"):
             a2a[kk + "_frac_of_nvlink_peak"] = a2a[kk + "_bus_gbs"] / 900.0
             a2a[kk + "_frac_of_measured_a2a"] = a2a[kk + "_bus_gbs"] / A2A_CEILING_GBS
+        ok = bool(nvl0 and nvl1)
+        tx = (nvl1[0] - nvl0[0]) / args.steps if ok else -1.0
+        rx = (nvl1[1] - nvl0[1]) / args.steps if ok else -1.0
+        txm, rxm = max_over_ranks(tx), max_over_ranks(rx)  # collective on every rank
+        if txm >= 0:
+            algo = float(sum(nbytes))
+            a2a["nvlink_counters"] = {
+                "source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX field values, all links, read around the timed "
+                          "region (payload bytes; max over ranks)",
+                "tx_bytes_per_step": txm, "rx_bytes_per_step": rxm,
+                "algorithmic_offrank_bytes_per_step": algo,
+                "tx_over_algorithmic": txm / algo if algo else None,
+                "tx_gbs_over_step": txm / (ms / 1e3) / 1e9}
+        else:
+            a2a["nvlink_counters"] = {"unavailable": nvl.err if nvl else "no NVML"}
     losses = layer.losses.cpu().tolist()
     value = world * S / (ms / 1e3)
 

@@ -309,6 +309,9 @@ typedef struct {
   /* tv_initial_mean, tv_final_mean, col_balance_max_dev, min_expert_load, intra_share, final_task_loss,
    * final_aux_loss, final_comm_us, dropped_total_rate */
   double summary[9];
+  double* comm_measured_us;  /* [steps] optional: the step's measured exchange in us (CUDA events, max over ranks):
+                                counts exchange + dispatch phases under expert parallelism, the permute otherwise --
+                                next to comm_us, the alpha-beta model of the same dispatch (comm_cost.cpp:24-55) */
 } tamoe_train_report;
 
 int tamoe_train(const tamoe_layer_config* cfg, const double* c_hat, const tamoe_train_opts* opts, const void* x,
@@ -328,6 +331,13 @@ int tamoe_train_f64(const tamoe_layer_config* cfg, const double* c_hat, const ta
  * out NaN) and raises a flag that the next tamoe_layer_step (once the earlier step has completed) or
  * tamoe_layer_status returns as status 2. */
 int tamoe_layer_step(tamoe_layer* l, const tamoe_layer_io* io, void* stream);
+/* train() on an existing layer (any world size; trainer.cpp:183-452).  Under expert parallelism every rank calls it
+ * with the same opts and c_hat [P_global x N], its own process' x / y, its gate replica wg and its E local experts
+ * w1 / w2 (layer layouts, updated in place); each step the ranks exchange their losses, kept / dropped counts and
+ * measured exchange time through the mapped workspaces, so the report (all P_global processes) is identical on
+ * every rank.  opts->kind must match the layer's aux kind (topo -> balance switch allowed). */
+int tamoe_layer_train(tamoe_layer* l, const double* c_hat, const tamoe_train_opts* opts, const void* x, const void* y,
+                      void* wg, void* w1, void* w2, tamoe_train_report* report, void* stream);
 /* Waits for the last step; status 2 ("non-finite gate logit") if it saw a non-finite logit (reported once). */
 int tamoe_layer_status(tamoe_layer* l);
 int tamoe_layer_read(tamoe_layer* l, int what, void* dst, long long bytes, void* stream);

@@ -406,6 +406,7 @@ void fill_report(const TrainReport& r, tamoe_train_report* report) {
   put(report->initial_dispatch, r.initial_dispatch);
   put(report->final_dispatch, r.final_dispatch);
   put(report->tv_rows, r.tv_rows);
+  put(report->comm_measured_us, r.comm_measured_us);
   const double sm[9] = {r.tv_initial_mean, r.tv_final_mean, r.col_balance_max_dev, r.min_expert_load,
                         r.intra_share, r.final_task_loss, r.final_aux_loss, r.final_comm_us, r.dropped_total_rate};
   std::memcpy(report->summary, sm, sizeof(sm));
@@ -425,6 +426,19 @@ int tamoe_train(const tamoe_layer_config* cfg, const double* c_hat, const tamoe_
                                       static_cast<const __nv_bfloat16*>(y), static_cast<__nv_bfloat16*>(wg),
                                       static_cast<__nv_bfloat16*>(w1), static_cast<__nv_bfloat16*>(w2),
                                       static_cast<cudaStream_t>(stream));
+    fill_report(r, report);
+  });
+}
+
+int tamoe_layer_train(tamoe_layer* l, const double* c_hat, const tamoe_train_opts* opts, const void* x, const void* y,
+                      void* wg, void* w1, void* w2, tamoe_train_report* report, void* stream) {
+  return guarded([&] {
+    require(l && opts && x && y && wg && w1 && report, "layer_train: null argument");
+    require(l->impl.cfg().f == 0 || w2, "layer_train: FFN experts need w2");
+    const TrainReport r = train_on_layer(l->impl, c_hat, train_options(opts), static_cast<const __nv_bfloat16*>(x),
+                                         static_cast<const __nv_bfloat16*>(y), static_cast<__nv_bfloat16*>(wg),
+                                         static_cast<__nv_bfloat16*>(w1), static_cast<__nv_bfloat16*>(w2),
+                                         static_cast<cudaStream_t>(stream));
     fill_report(r, report);
   });
 }

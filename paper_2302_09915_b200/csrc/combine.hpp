@@ -23,7 +23,7 @@ struct CombineArgs {
   float* dldg;                   // [T*k]
   double* loss_part;             // [combine_blocks(T)] sum of squared residuals per block
   // fuse_dz: the gate's softmax backward (gate_dz) runs per token right after the combine, in the same warp
-  // (the loss finalisation then moves to gate_dw's reduction); gz.dldg is not read
+  // (the loss finalisation then moves into the gate dW GEMM); gz.dldg is not read
   int fuse_dz;
   GateDzArgs gz;
 };

@@ -76,6 +76,7 @@ struct GateRouteParams {
   float* logits;
   RowRouteOut o;
   int N, S, k, TB;
+  int probe;  // A/B probe (TAMOE_GATE_PROBE): 1 = release TMEM and stop, 2 = skip the fp64 exp
 };
 
 template <int KM>
@@ -108,6 +109,42 @@ __device__ __forceinline__ void merge_topk(const double* pa, const int* ea, cons
       }
     }
   }
+}
+
+// Branch-free fp64 exp for x <= 0 (the softmax's exp(v - max)): x clamped to >= -700 (exp(-700) ~ 1e-304 vanishes
+// against the denominator >= 1 either way), n = round(x / ln2) by the 1.5 * 2^52 shift, r = x - n ln2 with a
+// 32-bit-exact high part of ln2 (|r| <= ln2 / 2), Taylor to degree 13 (truncation < 5e-18 relative), and 2^n
+// applied to the exponent field.  Within 1 ulp of the correctly rounded value, like CUDA's exp(), but with no
+// special-case branch, so the 32 exponentials of a lane interleave.
+template <int W>
+__device__ __forceinline__ void exp_nonpos_x(double (&x)[W]) {
+  // W independent evaluations written in lockstep, so the dependent DFMA chains interleave
+  const double shift = 6755399441055744.0;  // 1.5 * 2^52
+  double n[W], r[W], p[W];
+  int ni[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    const double xc = fmax(x[w], -700.0);
+    const double t = fma(xc, 0x1.71547652b82fep+0, shift);
+    n[w] = t - shift;
+    ni[w] = __double2loint(t);
+    r[w] = fma(n[w], -0x1.62e42fee00000p-1, xc);
+  }
+#pragma unroll
+  for (int w = 0; w < W; ++w) r[w] = fma(n[w], -0x1.a39ef35793c76p-33, r[w]);
+  constexpr double c[13] = {0x1.1eed8eff8d898p-29, 0x1.ae64567f544e4p-26, 0x1.27e4fb7789f5cp-22,
+                            0x1.71de3a556c734p-19, 0x1.a01a01a01a01ap-16, 0x1.a01a01a01a01ap-13,
+                            0x1.6c16c16c16c17p-10, 0x1.1111111111111p-7,  0x1.5555555555555p-5,
+                            0x1.5555555555555p-3,  0.5,                   1.0,
+                            1.0};
+#pragma unroll
+  for (int w = 0; w < W; ++w) p[w] = fma(0x1.6124613a86d09p-33, r[w], c[0]);
+#pragma unroll
+  for (int j = 1; j < 13; ++j)
+#pragma unroll
+    for (int w = 0; w < W; ++w) p[w] = fma(p[w], r[w], c[j]);
+#pragma unroll
+  for (int w = 0; w < W; ++w) x[w] = __hiloint2double(__double2hiint(p[w]) + (ni[w] << 20), __double2loint(p[w]));
 }
 
 template <int NC, int KM>
@@ -146,6 +183,7 @@ struct EpiRoute {
       for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
     }
     release();
+    if (e.probe == 1) return;
     if (valid) {
       float* dst = e.logits + gtok * N + cb;
       if ((N & 3) == 0) {
@@ -177,7 +215,21 @@ struct EpiRoute {
     const double dmx = static_cast<double>(mx);
     double E[32];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) E[i] = (cb + i < N) ? exp(static_cast<double>(v[i]) - dmx) : 0.0;
+    for (int i0 = 0; i0 < 32; i0 += 4) {
+      double xs[4];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) xs[w] = static_cast<double>(cb + i0 + w < N ? v[i0 + w] : mx) - dmx;
+      exp_nonpos_x<4>(xs);
+#pragma unroll
+      for (int w = 0; w < 4; ++w) E[i0 + w] = (cb + i0 + w < N && ok) ? xs[w] : 0.0;
+    }
+    if (e.probe == 3) {  // stop after the exps
+      double acc = 0.0;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) acc += E[i];
+      if (valid) e.o.msum4[gtok] = acc;
+      return;
+    }
     // top-k by e of this half (experts ascending: strict '>' keeps the lower one on ties)
     TopK<KM> te;
     te.init();
@@ -191,7 +243,8 @@ struct EpiRoute {
       for (int i = 0; i < 32; ++i)
         if (i < N) den += E[i];
     }
-    double kth;
+    // merged top-k by e (both halves hold it after barrier 2)
+    TopK<KM> m;
     if constexpr (kTwo) {  // barrier 2: half 0's partial sum and both halves' top-k by e
       if (h == 0) me.sum[lane] = den;
 #pragma unroll
@@ -217,51 +270,87 @@ struct EpiRoute {
         bp[j] = h1.te_p[j][lane];
         be[j] = h1.te_e[j][lane];
       }
-      TopK<KM> m;
       merge_topk<KM>(ap, ae, bp, be, k, m);
-      kth = m.p[0];
+    } else {
+      m = te;
+    }
+    double kth = m.p[0];
 #pragma unroll
-      for (int j = 0; j < KM; ++j)
-        if (j < k) kth = m.p[j];
-      // barrier 3: the full denominator (half 1) back to half 0; the exchange slots are free again
-      pair_sync();
+    for (int j = 0; j < KM; ++j)
+      if (j < k) kth = m.p[j];
+    // Division is monotone, so the top-k by p is the top-k by e unless an expert with a smaller e rounds to the
+    // same p as a selected one and has the lower index (the reference breaks p ties by index).  Only experts with
+    // e within a few ulps of the k-th can: flag them (no division on the common path).
+    const double thr = kth * (1.0 - 0x1p-46);
+    bool extra = false;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      bool sel = false;
+#pragma unroll
+      for (int j = 0; j < KM; ++j) sel |= (j < k) && (m.e[j] == cb + i);
+      extra |= (cb + i < N) && !sel && E[i] >= thr;
+    }
+    bool any_extra = __any_sync(0xffffffffu, extra);
+    if constexpr (kTwo) {  // barrier 3: the full denominator (half 1) and the extra flags to both halves
+      pair_sync();  // both halves are done reading the top-k lists
       if (h == 1) me.sum[lane] = den;
+      me.fin[lane] = any_extra;
       pair_sync();
       if (h == 0) den = pa.sum[lane];
-    } else {
-      kth = te.p[0];
+      any_extra = any_extra || pa.fin[lane];
+    }
+    TopK<KM> tp;
+    if (!any_extra) {
+      // common path: exactly the k selected are divided (warp-uniform, no divergence)
+      tp = m;
 #pragma unroll
       for (int j = 0; j < KM; ++j)
-        if (j < k) kth = te.p[j];
+        if (j < k) tp.p[j] = m.p[j] / den;
+      // two selected e may round to the same p: restore (p desc, expert asc) among the selected
+#pragma unroll
+      for (int j = 1; j < KM; ++j)
+#pragma unroll
+        for (int i = j; i > 0; --i)
+          if (i < k && (tp.p[i] > tp.p[i - 1] || (tp.p[i] == tp.p[i - 1] && tp.e[i] < tp.e[i - 1]))) {
+            const double tpv = tp.p[i];
+            tp.p[i] = tp.p[i - 1];
+            tp.p[i - 1] = tpv;
+            const int tev = tp.e[i];
+            tp.e[i] = tp.e[i - 1];
+            tp.e[i - 1] = tev;
+          }
+    } else {
+      // near-tie path (pair-uniform): exact p for every candidate of this half in expert order, then merged
+      tp.init();
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (cb + i < N && E[i] >= thr) tp.insert(E[i] / den, cb + i, k);
+      if constexpr (kTwo) {  // barrier 4: half 1's candidates to half 0, which merges
+        if (h == 1) {
+#pragma unroll
+          for (int j = 0; j < KM; ++j) {
+            me.te_p[j][lane] = tp.p[j];
+            me.te_e[j][lane] = tp.e[j];
+          }
+        }
+        pair_sync();
+        if (h == 0) {
+          double bp[KM];
+          int be[KM];
+#pragma unroll
+          for (int j = 0; j < KM; ++j) {
+            bp[j] = pa.te_p[j][lane];
+            be[j] = pa.te_e[j][lane];
+          }
+          TopK<KM> mm;
+          merge_topk<KM>(tp.p, tp.e, bp, be, k, mm);
+          tp = mm;
+        }
+      }
     }
-    // exact p = e / den for every expert of this half that can tie or beat the k-th after rounding
-    const double thr = kth * (1.0 - 0x1p-46);
-    TopK<KM> tp;
-    tp.init();
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (cb + i < N && E[i] >= thr) tp.insert(E[i] / den, cb + i, k);
-    if constexpr (kTwo) {  // barrier 4: half 1's candidates to half 0, which merges and writes the picks
-      if (h == 1) {
-#pragma unroll
-        for (int j = 0; j < KM; ++j) {
-          me.te_p[j][lane] = tp.p[j];
-          me.te_e[j][lane] = tp.e[j];
-        }
-      }
-      pair_sync();
-      if (h == 0) {
-        double bp[KM];
-        int be[KM];
-#pragma unroll
-        for (int j = 0; j < KM; ++j) {
-          bp[j] = pa.te_p[j][lane];
-          be[j] = pa.te_e[j][lane];
-        }
-        TopK<KM> m;
-        merge_topk<KM>(tp.p, tp.e, bp, be, k, m);
-        tp = m;
-      }
+    if (e.probe == 5) {  // stop after the exact candidates / merge
+      if (valid) e.o.msum4[gtok] = tp.p[0] + tp.e[0];
+      return;
     }
     const double qnan = __longlong_as_double(0x7ff8000000000000ll);
     // 32-token group slot of this warp (= route_logits' block index)
@@ -313,6 +402,7 @@ struct EpiRoute {
       if (lane < N) e.o.hist4[slot * N + lane] = cnt0;
       if (32 + lane < N) e.o.hist4[slot * N + 32 + lane] = cnt1;
     }
+    if (e.probe == 6) return;  // stop before the column sums
     // column sums of p = e * (1 / den) over the group's 32 tokens for this half's experts (fixed butterfly)
     const double rcp = valid ? (ok ? 1.0 / den : qnan) : 0.0;
 #pragma unroll
@@ -580,7 +670,11 @@ void gate_forward(const __nv_bfloat16* x, const __nv_bfloat16* wg, int n_pad, co
   GemmParams p{1, nullptr, nullptr, 0, n_pad, dm, 1, d.S, n_pad, d.P, 0, 1, 0, 0};
   if (gate_is_fused(d.N, o.probs != nullptr)) {
     // one launch: logits GEMM + per-token routing in the epilogue
-    GateRouteParams rp{o.logits, o, d.N, d.S, d.k, d.TB};
+    static const int probe = [] {
+      const char* v = std::getenv("TAMOE_GATE_PROBE");
+      return v ? std::atoi(v) : 0;
+    }();
+    GateRouteParams rp{o.logits, o, d.N, d.S, d.k, d.TB, probe};
     const int km = d.k == 1 ? 1 : (d.k == 2 ? 2 : kMaxTopK);
 #define TAMOE_GATE_ROUTE(NC, KM) launch_gemm<kModeGate, NC, false, false, EpiRoute<NC, KM>>(ta, tb, p, rp, 0, s)
     if (BNsel == 32) {

@@ -69,10 +69,15 @@ struct EpiGateDw {
   struct Params {
     float* part;
     int d, n64, P;
+    int finalize;    // the loss finalisation of the gate dz pass fused into combine: one epilogue warp of CTA 0
+    GateDzArgs fin;  // runs it before its first accumulator is ready (hidden under the mainloop)
   };
   static __device__ __forceinline__ void finish(const Params&, int) {}
-  static __device__ __forceinline__ void prefetch(const Params&, const GemmParams&, const TileInfo&, int, int, int,
-                                                  uint8_t*, const int*) {}
+  static __device__ __forceinline__ void prefetch(const Params& e, const GemmParams&, const TileInfo& ti, int q, int h,
+                                                  int lane, uint8_t*, const int*) {
+    if (e.finalize && blockIdx.x == 0 && q == 0 && h == 0 && ti.g == 0 && ti.ks == 0 && ti.m0 == 0 && ti.n0 == 0)
+      dz_finalize_losses(e.fin, lane);
+  }
   static __device__ __forceinline__ void run(const Params& e, const GemmParams& p, const TileInfo& ti,
                                              uint32_t tmem_tile, int q, int h, int lane, uint8_t*, const int*) {
     const int m = ti.m0 + q * 32 + lane;
@@ -94,13 +99,9 @@ struct EpiGateDw {
 };
 
 __global__ void dwg_reduce_kernel(const float* __restrict__ part, int splits, int P, int n64, int n_pad, int d,
-                                  int N, float* __restrict__ dwg, const __grid_constant__ GateDzArgs fin,
-                                  int finalize) {
+                                  int N, float* __restrict__ dwg) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
-  // the gate dz pass fused into the combine kernel: the losses are finalised here (combine's partial sums
-  // are complete once this kernel runs)
-  if (finalize && blockIdx.x == 0 && threadIdx.x < 32) dz_finalize_losses(fin, threadIdx.x);
   const long long total = static_cast<long long>(P) * n_pad * d;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -337,7 +338,7 @@ void gate_dw(const __nv_bfloat16* x, const __nv_bfloat16* dz, int P, int S, int 
   CUtensorMap tb = make_tmap_bf16(dz, n64, T, n64, 64);  // B = dz   (MN-major)
   GemmParams p{1, nullptr, nullptr, d, 64, 0, splits, S, 0, P, 0, 1, 0, 0};
   // one 64-column N block per launch keeps BN = 64 (n64 > 64 loops over column blocks)
-  EpiGateDw::Params ep{part, d, n64, P};
+  EpiGateDw::Params ep{part, d, n64, P, finalize ? 1 : 0, finalize ? *finalize : GateDzArgs{}};
   if (n64 == 64) {
     launch_gemm<kModeGateDw, 64, true, true, EpiGateDw>(ta, tb, p, ep, 0, s);
   } else {
@@ -352,9 +353,7 @@ void gate_dw(const __nv_bfloat16* x, const __nv_bfloat16* dz, int P, int S, int 
   }
   const long long total = static_cast<long long>(P) * n_pad * d;
   const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 4096));
-  GateDzArgs fin{};
-  if (finalize) fin = *finalize;
-  launch_pdl(dwg_reduce_kernel, blocks, 256, 0, s, part, splits, P, n64, n_pad, d, N, dwg, fin, finalize ? 1 : 0);
+  launch_pdl(dwg_reduce_kernel, blocks, 256, 0, s, part, splits, P, n64, n_pad, d, N, dwg);
   TAMOE_CUDA(cudaGetLastError());
 }
 

@@ -58,6 +58,51 @@ __device__ __forceinline__ void dz_finalize_losses(const GateDzArgs& a, int lane
   }
 }
 
+// The same finalisation by a whole block (blockDim a multiple of 32, <= 1024): the task partials are split over
+// all threads (strided, eight loads in flight), reduced per warp and then across warps in a fixed order.
+__device__ __forceinline__ void dz_finalize_losses_block(const GateDzArgs& a) {
+  __shared__ double red[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double task = 0.0;
+  {
+    constexpr int kU = 8;
+    const int nt = blockDim.x;
+    int i = threadIdx.x;
+    for (; i + nt * (kU - 1) < a.n_loss_part; i += nt * kU) {
+      double v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) v[u] = a.loss_part[i + nt * u];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) task += v[u];
+    }
+    for (; i < a.n_loss_part; i += nt) task += a.loss_part[i];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) task += __shfl_xor_sync(0xffffffffu, task, o);
+  if (lane == 0) red[w] = task;
+  __syncthreads();
+  if (w == 0) {
+    double t = 0.0;
+    for (int i = 0; i < nw; ++i) t += red[i];
+    const int N = a.N;
+    double aux = 0.0;
+    for (int pr = 0; pr < a.P; ++pr) {
+      double l = 0.0;
+      for (int e = lane; e < N; e += 32) {
+        const double frac = static_cast<double>(a.counts[pr * N + e]) / a.S;
+        l += (a.aux_kind == 1 ? a.penalties[pr * N + e] : 1.0) * a.mean_probs[pr * N + e] * frac;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+      aux += a.aux_kind == 1 ? static_cast<double>(N) * a.P_global * l : l;
+    }
+    if (lane == 0) {
+      a.losses[0] = t / (static_cast<double>(a.P_global) * a.S * a.dout);
+      a.losses[1] = aux / a.P_global;
+    }
+  }
+}
+
 template <int NPL>
 __device__ __forceinline__ void dz_load_logits(const GateDzArgs& a, long long t, int lane, float (&l)[NPL]) {
 #pragma unroll

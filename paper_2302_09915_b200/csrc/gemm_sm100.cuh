@@ -46,9 +46,17 @@ struct GemmParams {
   int procs;             // logical processes (gate modes)
   int w_mod;             // kModeSwap: weight of group g is g % w_mod (0: g) -- (source, expert) segments
   int nsub;              // kModeWgrad: K of group g = sub-segments s*num_groups + g, s < nsub
-  int pf_dist;           // kModeSwap: k-blocks of A/B prefetched into L2 ahead of the TMA loads (0: off)
-  int pf_b;              // also prefetch B
+  int pf_dist;           // unused (an L2 prefetch experiment, measured no gain)
+  int pf_b;              // unused
+  int lpt;               // kModeSwap: groups in descending token-tile size, tiles dealt to the CTA pairs in
+                         // boustrophedon order (largest first, alternating direction per round) -- evens out
+                         // the last round of the persistent schedule
 };
+
+// i-th tile of persistent cluster c out of nc (>= the tile count: done).  Snake: rounds alternate direction.
+__device__ __forceinline__ int sched_tile(int i, int c, int nc, bool snake) {
+  return i * nc + ((snake && (i & 1)) ? nc - 1 - c : c);
+}
 
 struct TileInfo {
   int g;       // group
@@ -102,7 +110,7 @@ struct GemmSmem {
   static constexpr int kBBytes = (BN / (kCG == 1 ? 1 : 2)) * kBK * 2;  // a CTA pair splits B's N between its CTAs
   static constexpr int kStageBytes = kABytes + kBBytes;
   // barriers: full[S], empty[S], tfull[2], tempty[2]; tmem addr; tile prefix; group starts / rows
-  static constexpr int kMiscBytes = (2 * 8 + 4) * 8 + 16 + (3 * kMaxGroups + 1) * 4;
+  static constexpr int kMiscBytes = (2 * 8 + 4) * 8 + 16 + (4 * kMaxGroups + 1) * 4;
   static constexpr int kBudget = 227 * 1024 - ((kEpiBytes + 1023) / 1024) * 1024 - kMiscBytes - 2048;
 #ifdef TAMOE_MAX_STAGES
   static constexpr int kMaxStages = TAMOE_MAX_STAGES;  // A/B experiments only
@@ -147,7 +155,7 @@ __device__ __forceinline__ int group_tiles(const GemmParams& p, int rows) {
 
 template <int kMode, int BN, int kCG = 1>
 __device__ __forceinline__ void decode_tile(const GemmParams& p, const int* prefix, const int* s_start,
-                                            const int* s_rows, int t, TileInfo& ti) {
+                                            const int* s_rows, const int* s_gid, int t, TileInfo& ti) {
   // find group: prefix[g] <= t < prefix[g+1]
   int lo = 0, hi = p.num_groups - 1;
   while (lo < hi) {
@@ -163,7 +171,8 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, const int* pref
     const int nb = swap_ntiles<BN>(rows);
     const int ns = swap_nsize<BN>(rows);
     const int mb = r / nb, nbk = r % nb;
-    ti.wg = p.w_mod > 0 ? g % p.w_mod : g;
+    const int gg = s_gid[g];  // the group's weight (groups may be visited in size order)
+    ti.wg = p.w_mod > 0 ? gg % p.w_mod : gg;
     ti.m0 = mb * kBM * kCG;
     ti.n0 = nbk * ns;
     ti.n = min(ns, rows - ti.n0);
@@ -252,6 +261,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   int* prefix = reinterpret_cast<int*>(tmem_slot + 4);
   int* s_start = prefix + kMaxGroups + 1;
   int* s_rows = s_start + kMaxGroups;
+  int* s_gid = s_rows + kMaxGroups;
 
   const int warp = ptx::warp_id();
   const int lane = ptx::lane_id();
@@ -289,8 +299,40 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   for (int g = threadIdx.x; g < nseg; g += blockDim.x) {
     s_start[g] = grouped ? p.seg_start[g] : 0;
     s_rows[g] = grouped ? p.seg_rows[g] : 0;
+    s_gid[g] = g;
   }
   __syncthreads();
+  const bool snake = kMode == kModeSwap && p.lpt != 0;
+  if (snake) {
+    // stable order by token-tile size, descending: rank of every group, then the table permuted into it
+    constexpr int kPer = (kMaxGroups + kGemmThreads - 1) / kGemmThreads;
+    int rk[kPer], st[kPer], rw[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int g = threadIdx.x + j * kGemmThreads;
+      rk[j] = -1;
+      if (g < G) {
+        const int ns = swap_nsize<BN>(s_rows[g]);
+        int r = 0;
+        for (int h = 0; h < G; ++h) {
+          const int nh = swap_nsize<BN>(s_rows[h]);
+          r += (nh > ns) || (nh == ns && h < g);
+        }
+        rk[j] = r;
+        st[j] = s_start[g];
+        rw[j] = s_rows[g];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kPer; ++j)
+      if (rk[j] >= 0) {
+        s_start[rk[j]] = st[j];
+        s_rows[rk[j]] = rw[j];
+        s_gid[rk[j]] = threadIdx.x + j * kGemmThreads;
+      }
+    __syncthreads();
+  }
   if (warp == 0) {
     int carry = 0;
     for (int g0 = 0; g0 < G; g0 += 32) {
@@ -331,36 +373,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           ti.bx += static_cast<int>(rank) * (BN / kCG);
         }
       };
-      // Swap mode streams every expert's weights once from HBM: keep kPfDist k-blocks of A (weights) and
-      // B (tokens) prefetched into L2 ahead of the TMA loads, across tile boundaries, so DRAM latency is
-      // not bounded by the shared-memory pipeline depth.
-      const int kPfDist = p.pf_dist;
-      int pf_t = cluster_id, pf_kb = 0;
-      TileInfo pf_ti;
-      bool pf_ok = (kMode == kModeSwap) && kPfDist > 0 && pf_t < total_tiles;
-      if (pf_ok) { decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, pf_t, pf_ti); localize(pf_ti); }
-      auto pf_step = [&]() {
-        if constexpr (kMode == kModeSwap) {
-          if (!pf_ok) return;
-          if constexpr (A_MN) {
-            ptx::tma_prefetch_2d(&tmA, pf_ti.ax, pf_ti.ay + pf_kb * kBK);
-            ptx::tma_prefetch_2d(&tmA, pf_ti.ax + 64, pf_ti.ay + pf_kb * kBK);
-          } else {
-            ptx::tma_prefetch_2d(&tmA, pf_ti.ax + pf_kb * kBK, pf_ti.ay);
-          }
-          if (p.pf_b) ptx::tma_prefetch_2d(&tmB, pf_ti.bx + pf_kb * kBK, pf_ti.by);
-          if (++pf_kb >= ceil_div(pf_ti.k_len, kBK)) {
-            pf_kb = 0;
-            pf_t += num_clusters;
-            pf_ok = pf_t < total_tiles;
-            if (pf_ok) { decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, pf_t, pf_ti); localize(pf_ti); }
-          }
-        }
-      };
-      for (int i = 0; i < kPfDist; ++i) pf_step();
-      for (int t = cluster_id; t < total_tiles; t += num_clusters) {
+      for (int i = 0;; ++i) {
+        const int t = sched_tile(i, cluster_id, num_clusters, snake);
+        if (t >= total_tiles) break;
         TileInfo ti;
-        decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, t, ti);
+        decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, s_gid, t, ti);
         localize(ti);
         // K ranges: wgrad walks the group's (source) sub-segments; every other mode has one range
         const int nsub = (kMode == kModeWgrad) ? p.nsub : 1;
@@ -415,7 +432,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               }
             }
             if (++stage == L::kStages) { stage = 0; phase ^= 1; }
-            pf_step();
           }
         }
       }
@@ -426,9 +442,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = cluster_id; t < total_tiles; t += num_clusters, ++it) {
+      for (;; ++it) {
+        const int t = sched_tile(it, cluster_id, num_clusters, snake);
+        if (t >= total_tiles) break;
         TileInfo ti;
-        decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, t, ti);
+        decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, s_gid, t, ti);
         const int buf = it & 1;
         const uint32_t use = static_cast<uint32_t>(it >> 1);
         ptx::mbar_wait(&tempty_bar[buf], (use & 1) ^ 1);
@@ -492,16 +510,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if constexpr (EpiAhead<Epi>::value) {
       static_assert(!EpiEarly<Epi>::value, "tile-ahead epilogues release TMEM after run()");
       TileInfo nx;
-      if (cluster_id < total_tiles) {
-        decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, cluster_id, nx);
+      if (sched_tile(0, cluster_id, num_clusters, snake) < total_tiles) {
+        decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, s_gid, sched_tile(0, cluster_id, num_clusters, snake),
+                                    nx);
         nx.m0 += static_cast<int>(rank) * kBM;
         Epi::prefetch(ep, p, nx, q, h, lane, wsm, s_start);
       }
-      for (int t = cluster_id; t < total_tiles; t += num_clusters, ++it) {
+      for (;; ++it) {
+        if (sched_tile(it, cluster_id, num_clusters, snake) >= total_tiles) break;
         const TileInfo ti = nx;
-        const int tn = t + num_clusters;
+        const int tn = sched_tile(it + 1, cluster_id, num_clusters, snake);
         if (tn < total_tiles) {
-          decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, tn, nx);
+          decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, s_gid, tn, nx);
           nx.m0 += static_cast<int>(rank) * kBM;
           Epi::prefetch(ep, p, nx, q, h, lane, wsm + ((it + 1) & 1) * Epi::kBufBytes, s_start);
         } else {
@@ -521,9 +541,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
     } else
-    for (int t = cluster_id; t < total_tiles; t += num_clusters, ++it) {
+    for (;; ++it) {
+      const int t = sched_tile(it, cluster_id, num_clusters, snake);
+      if (t >= total_tiles) break;
       TileInfo ti;
-      decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, t, ti);
+      decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, s_gid, t, ti);
       ti.m0 += static_cast<int>(rank) * kBM;  // this CTA's 128 accumulator rows
       const int buf = it & 1;
       const uint32_t use = static_cast<uint32_t>(it >> 1);

@@ -189,6 +189,9 @@ Layer::Layer(const LayerConfig& c, const double* c_hat, std::unique_ptr<EpComm> 
     arena_.reserve(plan_.push_row, r_max_);
     arena_.reserve(sig_slots_, kMaxRanks);
     arena_.reserve(sig_epoch_, 1);
+    gather_cap_ = 8 + 2 * c.P * c.N;
+    arena_.reserve(gather_buf_, static_cast<long long>(W) * gather_cap_);
+    arena_.reserve(gather_src_, gather_cap_);
   }
   if (c.aux_kind == 2) {
     arena_.reserve(quota_, static_cast<long long>(c.P) * c.N);
@@ -287,6 +290,8 @@ void Layer::connect(const PeerBlob* all) {
     map_.E = E;
     map_.local_start = rw_.buf.seg_start;
     map_.dst_off = plan_.dst_off;
+    const long long goff = reinterpret_cast<char*>(gather_buf_) - arena_.base();
+    for (int j = 0; j < c.world_size; ++j) gather_peers_.p[j] = reinterpret_cast<unsigned int*>(bases_[j] + goff);
   }
   connected_ = true;
 }
@@ -362,6 +367,24 @@ void Layer::check_deferred(bool wait) {
 }
 
 void Layer::status() { check_deferred(true); }
+
+void Layer::allgather_host(const double* mine, int n, double* all, cudaStream_t s) {
+  const int W = cfg_.world_size;
+  if (!ep_) {
+    std::copy(mine, mine + n, all);
+    return;
+  }
+  require(connected_, "allgather: expert-parallel peers not connected");
+  require(n >= 1 && n <= gather_cap_, "allgather: record larger than the gather buffer");
+  TAMOE_CUDA(cudaMemcpyAsync(gather_src_, mine, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  peer_broadcast_words(gather_peers_, static_cast<long long>(cfg_.rank) * gather_cap_ * 2, gather_src_, 2LL * n, W,
+                       s);
+  ep_barrier(s, false);
+  for (int r = 0; r < W; ++r)
+    TAMOE_CUDA(cudaMemcpyAsync(all + static_cast<size_t>(r) * n, gather_buf_ + static_cast<size_t>(r) * gather_cap_,
+                               sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  TAMOE_CUDA(cudaStreamSynchronize(s));
+}
 
 PeerBufs Layer::peers(__nv_bfloat16* local) const {
   PeerBufs pb{};
@@ -728,7 +751,7 @@ void Layer::gate_backward(const LayerIO& io, cudaStream_t s) {
   const LayerConfig& c = cfg_;
   PhaseTimer& tm = timer_;
   const GateDzArgs ga = dz_args(io);
-  if (fused_dz_enabled()) {  // dz was computed by the combine kernel; the losses are finalised by gate_dw
+  if (fused_dz_enabled()) {  // dz came from the combine kernel; the gate dW GEMM finalises the losses
     gate_dw(io.x, dz_, c.P, c.S, c.d, n64_, n_pad_, c.N, dw_part_, dw_splits_, io.dwg, s, &ga);
     tm.mark("gate_dw", s);
     return;

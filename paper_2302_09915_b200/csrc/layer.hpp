@@ -136,6 +136,11 @@ class Layer {
   PeerBlob blob() const;
   void connect(const PeerBlob* all);
   bool connected() const { return connected_; }
+  // Expert parallelism, outside the step: every rank's n doubles (host) -> all ranks' [world x n] (host, rank
+  // order), through peer stores into the mapped workspaces and one device barrier (train()'s per-step report).
+  // n <= gather_cap().  Synchronises the stream.
+  void allgather_host(const double* mine, int n, double* all, cudaStream_t s);
+  int gather_cap() const { return gather_cap_; }
 
  private:
   void step_local(const LayerIO& io, cudaStream_t s);
@@ -190,6 +195,10 @@ class Layer {
   size_t comp_ws_bytes_ = 0;  // penalties p = Norm(1/c_hat) computed at creation (created with the topo loss)
   PhaseTimer timer_;
   bool connected_ = false, stepped_ = false;
+  double* gather_buf_ = nullptr;  // [world x gather_cap_] (peer-mapped)
+  double* gather_src_ = nullptr;  // [gather_cap_]
+  int gather_cap_ = 0;
+  PeerWords gather_peers_{};
   unsigned long long fingerprint() const;
   void init_topology(const double* c_hat);
   int* bad_host_ = nullptr;            // mapped pinned: set by the router on a non-finite logit

@@ -8,6 +8,7 @@
 #include <limits>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "common.hpp"
 #include "host_topology.hpp"
@@ -73,7 +74,9 @@ TrainReport run_train(int P, int S, int N, int k, int d, int cap_mode, double au
   double losses[2];
 
   for (int step = 0; step < o.steps; ++step) {
-    step_fn(step, losses, counts_i.data(), dropped_i.data());
+    double measured = 0.0;
+    step_fn(step, losses, counts_i.data(), dropped_i.data(), &measured);
+    rep.comm_measured_us.push_back(measured);
     const double task = losses[0], aux = losses[1];
     if (!std::isfinite(task + aux_weight * aux))
       throw std::runtime_error("training diverged at step " + std::to_string(step) + " (task=" +
@@ -162,18 +165,32 @@ TrainReport run_train(int P, int S, int N, int k, int d, int cap_mode, double au
 TrainReport train_layer(LayerConfig cfg, const double* c_hat, const TrainOptions& o, const __nv_bfloat16* x,
                         const __nv_bfloat16* y, __nv_bfloat16* wg, __nv_bfloat16* w1, __nv_bfloat16* w2,
                         cudaStream_t s) {
-  require(cfg.world_size == 1, "train: single-device layer (P logical processes)");
+  require(cfg.world_size == 1, "train: single-device layer (P logical processes); expert parallelism: "
+                               "tamoe_layer_train on a layer created with tamoe_layer_create_ep[_begin]");
   require(o.kind >= 0 && o.kind <= 2, "train: unknown loss kind");
-  require(o.steps >= 0, "train: steps must be >= 0");
   require(o.kind == 0 || c_hat != nullptr, "topo and compulsory losses require a target pattern");
   cfg.aux_kind = o.kind;  // 2 = compulsory quota routing + balance loss
   require(cfg.N % cfg.P == 0, "N must be divisible by P");
-  const int P = cfg.P, S = cfg.S, N = cfg.N;
   Layer layer(cfg, cfg.aux_kind != 0 ? c_hat : nullptr);
+  return train_on_layer(layer, c_hat, o, x, y, wg, w1, w2, s);
+}
+
+TrainReport train_on_layer(Layer& layer, const double* c_hat, const TrainOptions& o, const __nv_bfloat16* x,
+                           const __nv_bfloat16* y, __nv_bfloat16* wg, __nv_bfloat16* w1, __nv_bfloat16* w2,
+                           cudaStream_t s) {
+  const LayerConfig& cfg = layer.cfg();
+  require(o.kind >= 0 && o.kind <= 2, "train: unknown loss kind");
+  require(o.steps >= 0, "train: steps must be >= 0");
+  require(o.kind == 0 || c_hat != nullptr, "topo and compulsory losses require a target pattern");
+  require(cfg.aux_kind == o.kind, "train: the layer was created with a different aux loss kind");
+  const int W = cfg.world_size, me = cfg.rank;
+  const int P = cfg.P, S = cfg.S, N = cfg.N, E = N / W;
+  const int Pg = P * W;  // processes of the report (one per rank under expert parallelism)
+  require(N % Pg == 0, "N must be divisible by the number of processes");
   const int n_pad = layer.n_pad();
   const long long n_wg = static_cast<long long>(P) * n_pad * cfg.d;
-  const long long n_w1 = static_cast<long long>(N) * (cfg.f == 0 ? cfg.d_out : cfg.f) * cfg.d;
-  const long long n_w2 = cfg.f == 0 ? 0 : static_cast<long long>(N) * cfg.d_out * cfg.f;
+  const long long n_w1 = static_cast<long long>(E) * (cfg.f == 0 ? cfg.d_out : cfg.f) * cfg.d;
+  const long long n_w2 = cfg.f == 0 ? 0 : static_cast<long long>(E) * cfg.d_out * cfg.f;
 
   DevBuf buf;
   float* m_wg = buf.get<float>(n_wg);
@@ -194,22 +211,75 @@ TrainReport train_layer(LayerConfig cfg, const double* c_hat, const TrainOptions
   io.dx = cfg.need_dx ? buf.get<__nv_bfloat16>(static_cast<long long>(P) * S * cfg.d) : nullptr;
   io.losses = buf.get<double>(2);
 
+  // per-step CUDA-event phase timing (eager steps): the measured exchange of each step = the counts exchange +
+  // dispatch phases under expert parallelism (a2a_counts, a2a_dispatch), the local permute otherwise
+  PhaseTimer& tm = layer.timer();
+  tm.reset();
+  tm.enabled = true;
+  std::vector<double> prev(PhaseTimer::kMax, 0.0);
   const RouteBuffers& rb = layer.route().buf;
-  return run_train(cfg.P, cfg.S, cfg.N, cfg.k, cfg.d, cfg.cap_mode, cfg.aux_weight, c_hat, o,
-                   [&](int step, double* losses, int* counts_i, int* dropped_i) {
-                     if (o.kind == 1 && o.switch_step != INT_MIN && step > o.switch_step) layer.set_aux_kind(0);
-                     layer.step(io, s);
-                     layer.status();  // non-finite logit: ValidationError before the update (gate.cpp:16-17)
-                     const size_t pn = static_cast<size_t>(cfg.P) * cfg.N;
-                     TAMOE_CUDA(cudaMemcpyAsync(losses, io.losses, sizeof(double) * 2, cudaMemcpyDeviceToHost, s));
-                     TAMOE_CUDA(cudaMemcpyAsync(counts_i, rb.counts, sizeof(int) * pn, cudaMemcpyDeviceToHost, s));
-                     TAMOE_CUDA(cudaMemcpyAsync(dropped_i, rb.dropped, sizeof(int) * pn, cudaMemcpyDeviceToHost, s));
-                     // synchronized update, fixed order (gates, then experts)
-                     sgd_step(m_wg, io.dwg, static_cast<float>(o.lr), wg, n_wg, s);
-                     sgd_step(m_w1, io.dw1, static_cast<float>(o.lr), w1, n_w1, s);
-                     if (n_w2) sgd_step(m_w2, io.dw2, static_cast<float>(o.lr), w2, n_w2, s);
-                     TAMOE_CUDA(cudaStreamSynchronize(s));
-                   });
+  const size_t pn = static_cast<size_t>(P) * N;
+  const size_t rec = 4 + 2 * pn;  // per rank: task, aux, measured exchange, pad, kept counts, dropped counts
+  std::vector<double> mine(rec), all(static_cast<size_t>(W) * rec);
+  std::vector<int> cnt_local(pn), drop_local(pn);
+  TrainReport rep = run_train(Pg, S, N, cfg.k, cfg.d, cfg.cap_mode, cfg.aux_weight, c_hat, o,
+                              [&](int step, double* losses, int* counts_i, int* dropped_i, double* measured) {
+    if (o.kind == 1 && o.switch_step != INT_MIN && step > o.switch_step) layer.set_aux_kind(0);
+    layer.step(io, s);
+    layer.status();  // non-finite logit: ValidationError before the update (gate.cpp:16-17)
+    double loc[2];
+    TAMOE_CUDA(cudaMemcpyAsync(loc, io.losses, sizeof(double) * 2, cudaMemcpyDeviceToHost, s));
+    TAMOE_CUDA(cudaMemcpyAsync(cnt_local.data(), rb.counts, sizeof(int) * pn, cudaMemcpyDeviceToHost, s));
+    TAMOE_CUDA(cudaMemcpyAsync(drop_local.data(), rb.dropped, sizeof(int) * pn, cudaMemcpyDeviceToHost, s));
+    // synchronized update, fixed order (gates, then experts)
+    sgd_step(m_wg, io.dwg, static_cast<float>(o.lr), wg, n_wg, s);
+    sgd_step(m_w1, io.dw1, static_cast<float>(o.lr), w1, n_w1, s);
+    if (n_w2) sgd_step(m_w2, io.dw2, static_cast<float>(o.lr), w2, n_w2, s);
+    TAMOE_CUDA(cudaStreamSynchronize(s));
+    tm.fold();
+    double comm = 0.0;
+    for (int i = 0; i < tm.n; ++i) {
+      const std::string nm = tm.names[i];
+      const double dt = tm.total_ms[i] - prev[static_cast<size_t>(i)];
+      prev[static_cast<size_t>(i)] = tm.total_ms[i];
+      if (W > 1 ? (nm == "a2a_counts" || nm == "a2a_dispatch") : nm == "permute") comm += dt * 1e3;
+    }
+    if (W == 1) {
+      losses[0] = loc[0];
+      losses[1] = loc[1];
+      std::copy(cnt_local.begin(), cnt_local.end(), counts_i);
+      std::copy(drop_local.begin(), drop_local.end(), dropped_i);
+      *measured = comm;
+      return;
+    }
+    // every rank's losses (its share), kept / dropped counts and measured exchange -> every rank (peer stores +
+    // device barrier over the mapped workspaces): the report covers all P processes, identically on every rank
+    mine[0] = loc[0];
+    mine[1] = loc[1];
+    mine[2] = comm;
+    mine[3] = 0.0;
+    for (size_t i = 0; i < pn; ++i) {
+      mine[4 + i] = cnt_local[i];
+      mine[4 + pn + i] = drop_local[i];
+    }
+    layer.allgather_host(mine.data(), static_cast<int>(rec), all.data(), s);
+    losses[0] = losses[1] = 0.0;
+    *measured = 0.0;
+    for (int r = 0; r < W; ++r) {  // rank order: the sums are identical on every rank
+      const double* row = all.data() + static_cast<size_t>(r) * rec;
+      losses[0] += row[0];
+      losses[1] += row[1];
+      *measured = std::max(*measured, row[2]);
+      for (size_t i = 0; i < pn; ++i) {
+        counts_i[static_cast<size_t>(r) * pn + i] = static_cast<int>(row[4 + i]);
+        dropped_i[static_cast<size_t>(r) * pn + i] = static_cast<int>(row[4 + pn + i]);
+      }
+    }
+    (void)me;
+  });
+  tm.enabled = false;
+  tm.reset();
+  return rep;
 }
 
 TrainReport train_f64(int P, int S, int d, int d_out, int N, int k, int cap_mode, double cf, double aux_weight,
@@ -235,7 +305,7 @@ TrainReport train_f64(int P, int S, int d, int d_out, int N, int k, int cap_mode
   double* eg = buf.get<double>(n_u);
   const RouteBuffers& rb = router.rw.buf;
   return run_train(P, S, N, k, d, cap_mode, aux_weight, c_hat, o,
-                   [&](int step, double* losses, int* counts_i, int* dropped_i) {
+                   [&](int step, double* losses, int* counts_i, int* dropped_i, double*) {
                      F64StepArgs a;
                      a.d = d;
                      a.d_out = d_out;

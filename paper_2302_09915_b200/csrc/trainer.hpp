@@ -23,6 +23,7 @@ struct TrainOptions {
 
 struct TrainReport {
   std::vector<double> task_loss, aux_loss, comm_us, dropped_rate;  // per step
+  std::vector<double> comm_measured_us;  // per step: the measured exchange (CUDA events; max over ranks)
   std::vector<double> initial_dispatch, final_dispatch;           // [P x N]
   std::vector<double> tv_rows;                                    // [P] (with c_hat)
   double tv_initial_mean = 0, tv_final_mean = 0, col_balance_max_dev = 0, min_expert_load = 0;
@@ -34,6 +35,13 @@ struct TrainReport {
 TrainReport train_layer(LayerConfig cfg, const double* c_hat, const TrainOptions& opts, const __nv_bfloat16* x,
                         const __nv_bfloat16* y, __nv_bfloat16* wg, __nv_bfloat16* w1, __nv_bfloat16* w2,
                         cudaStream_t s);
+
+// The loop on an existing layer -- any world size: under expert parallelism every rank passes its own process'
+// x / y, its gate replica wg and its E = N / world local experts; the report covers all world * P processes and
+// is identical on every rank (losses, counts and the measured exchange are gathered each step).
+TrainReport train_on_layer(Layer& layer, const double* c_hat, const TrainOptions& opts, const __nv_bfloat16* x,
+                           const __nv_bfloat16* y, __nv_bfloat16* wg, __nv_bfloat16* w1, __nv_bfloat16* w2,
+                           cudaStream_t s);
 
 // The same loop in the reference's own precision (BASELINE C1): fp64 device step (layer_step_f64, linear experts)
 // and fp64 SGD.  x [P*S x d], y [P*S x d_out], gates [P x d x N], experts [N x d x d_out]: device fp64 in the

@@ -40,13 +40,17 @@ class _Opts(ctypes.Structure):
 class _Report(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in ("task_loss", "aux_loss", "comm_us", "dropped_rate",
                                                "initial_dispatch", "final_dispatch", "tv_rows")] + \
-               [("summary", ctypes.c_double * 9)]
+               [("summary", ctypes.c_double * 9), ("comm_measured_us", ctypes.c_void_p)]
 
 
 _lib.lib.tamoe_train.argtypes = [ctypes.POINTER(_Cfg), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_Opts),
                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                  ctypes.POINTER(_Report), ctypes.c_void_p]
 _lib.lib.tamoe_train.restype = ctypes.c_int
+_lib.lib.tamoe_layer_train.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_Opts),
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.POINTER(_Report), ctypes.c_void_p]
+_lib.lib.tamoe_layer_train.restype = ctypes.c_int
 
 
 @dataclass
@@ -94,6 +98,7 @@ class TrainReport:
     final_comm_us: float
     dropped_total_rate: float
     weights: dict
+    comm_measured_us: np.ndarray = None  # per step: the measured exchange (CUDA events, max over ranks)
 
 
 def _dptr(a):
@@ -119,21 +124,7 @@ def train(cfg: TrainConfig, x, y, gates, experts=None, W1=None, W2=None, kind: L
     c = _Cfg(P, S, d, dout, N, k, f, ACT_NONE if f == 0 else ACT_GELU, int(cfg.capacity.mode),
              float(cfg.capacity.capacity_factor), int(kind == LossKind.topo), float(cfg.aux_weight), int(cfg.norm),
              float(cfg.temperature), 0, 1, 0)
-    ah = np.ascontiguousarray(cfg.alpha_hat, np.float64) if cfg.alpha_hat is not None else None
-    bh = np.ascontiguousarray(cfg.beta_hat, np.float64) if cfg.beta_hat is not None else None
-    ig = None
-    if cfg.intra_groups is not None:
-        ig = np.zeros((P, P), np.int32)
-        for i, members in enumerate(cfg.intra_groups):
-            ig[i, list(members)] = 1
-    o = _Opts(int(kind), cfg.steps, cfg.lr, int(cfg.switch_step is not None),
-              int(cfg.switch_step) if cfg.switch_step is not None else 0, cfg.report_window, cfg.bytes_per_element,
-              _dptr(ah), _dptr(bh), _dptr(ig))
-    steps = cfg.steps
-    arrs = {n: np.zeros(steps) for n in ("task_loss", "aux_loss", "comm_us", "dropped_rate")}
-    d0, d1, tv = np.zeros((P, N)), np.zeros((P, N)), np.zeros(P)
-    r = _Report(*[_dptr(arrs[n]) for n in ("task_loss", "aux_loss", "comm_us", "dropped_rate")], _dptr(d0), _dptr(d1),
-                _dptr(tv))
+    o, arrs, d0, d1, tv, r = _opts_report(cfg, kind, P)
     ch = np.ascontiguousarray(c_hat, np.float64) if c_hat is not None else None
     s = torch.cuda.current_stream(dev)
     _lib.check(_lib.lib.tamoe_train(ctypes.byref(c), ch.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
@@ -148,4 +139,49 @@ def train(cfg: TrainConfig, x, y, gates, experts=None, W1=None, W2=None, kind: L
         weights["W1"] = w1.float().transpose(1, 2).cpu().numpy()
         weights["W2"] = w2.float().transpose(1, 2).cpu().numpy()
     return TrainReport(kind, arrs["task_loss"], arrs["aux_loss"], arrs["comm_us"], arrs["dropped_rate"], d0, d1,
-                       tv if c_hat is not None else np.zeros(0), *sm, weights=weights)
+                       tv if c_hat is not None else np.zeros(0), *sm, weights=weights,
+                       comm_measured_us=arrs["comm_measured_us"])
+
+
+def _opts_report(cfg: "TrainConfig", kind, P: int):
+    """ctypes options + report buffers for P (global) processes."""
+    N = cfg.N
+    ah = np.ascontiguousarray(cfg.alpha_hat, np.float64) if cfg.alpha_hat is not None else None
+    bh = np.ascontiguousarray(cfg.beta_hat, np.float64) if cfg.beta_hat is not None else None
+    ig = None
+    if cfg.intra_groups is not None:
+        ig = np.zeros((P, P), np.int32)
+        for i, members in enumerate(cfg.intra_groups):
+            ig[i, list(members)] = 1
+    o = _Opts(int(kind), cfg.steps, cfg.lr, int(cfg.switch_step is not None),
+              int(cfg.switch_step) if cfg.switch_step is not None else 0, cfg.report_window, cfg.bytes_per_element,
+              _dptr(ah), _dptr(bh), _dptr(ig))
+    o._keep = (ah, bh, ig)  # the arrays must outlive the call
+    arrs = {n: np.zeros(cfg.steps) for n in ("task_loss", "aux_loss", "comm_us", "dropped_rate", "comm_measured_us")}
+    d0, d1, tv = np.zeros((P, N)), np.zeros((P, N)), np.zeros(P)
+    r = _Report(*[_dptr(arrs[n]) for n in ("task_loss", "aux_loss", "comm_us", "dropped_rate")], _dptr(d0), _dptr(d1),
+                _dptr(tv), (ctypes.c_double * 9)(), _dptr(arrs["comm_measured_us"]))
+    return o, arrs, d0, d1, tv, r
+
+
+def train_layer(layer, params: dict, x: torch.Tensor, y: torch.Tensor, cfg: "TrainConfig",
+                kind: LossKind = LossKind.balance, c_hat=None) -> TrainReport:
+    """train() on an existing TAMoELayer -- the expert-parallel training loop: every rank calls it with its own
+    process' x / y (device bf16), its gate replica and its local experts (params, updated in place) and the same
+    cfg / c_hat [P_global, N]; the report covers all processes and is identical on every rank
+    (tamoe_layer_train)."""
+    lc = layer.cfg
+    Pg = lc.P * lc.world_size
+    o, arrs, d0, d1, tv, r = _opts_report(cfg, kind, Pg)
+    ch = np.ascontiguousarray(c_hat, np.float64) if c_hat is not None else None
+    s = torch.cuda.current_stream(x.device)
+    w2 = params.get("w2")
+    _lib.check(_lib.lib.tamoe_layer_train(layer._h, ch.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+                                          if ch is not None else None, ctypes.byref(o), x.data_ptr(), y.data_ptr(),
+                                          params["wg"].data_ptr(), params["w1"].data_ptr(),
+                                          w2.data_ptr() if w2 is not None else None, ctypes.byref(r),
+                                          ctypes.c_void_p(s.cuda_stream)))
+    sm = list(r.summary)
+    return TrainReport(kind, arrs["task_loss"], arrs["aux_loss"], arrs["comm_us"], arrs["dropped_rate"], d0, d1,
+                       tv if c_hat is not None else np.zeros(0), *sm, weights=params,
+                       comm_measured_us=arrs["comm_measured_us"])

@@ -81,3 +81,16 @@ def test_p2p_sweep():
 def test_p2p_sweep_store_bootstrap():
     out = _run("p2p_worker.py", 2, store=True)
     assert "P2P_SWEEP_OK" in out and "bootstrap=store" in out, out[-2000:]
+
+
+@pytest.mark.parametrize("kind,cap", [(1, 3), (0, 2)])
+def test_ep_train_matches_reference(kind, cap):
+    """Expert-parallel train() (tamoe_layer_train) at world 2 vs the reference's train() at P = 2: loss
+    trajectories, dispatch, and per-step modelled vs measured exchange (§8(f) rows 2 and 4)."""
+    import oracle
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    n = torch.cuda.device_count()
+    world = 2
+    out = _run("ep_train_worker.py", world, [str(kind), str(cap)], store=n < world)
+    assert "EP_TRAIN_OK" in out, out[-2000:]
