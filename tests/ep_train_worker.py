@@ -68,6 +68,9 @@ def main():
     assert torch.equal(t, ref0), "ranks disagree on the report"
     if rank == 0:
         ref = R.train(x, y, gates, experts, kind=kind, cap_mode=cap, cf=1.25, c_hat=c_hat, lr=lr, steps=steps, k=k)
+        print("task", rep.task_loss, ref["task_loss"], "\naux", rep.aux_loss, ref["aux_loss"], "\ndropped",
+              rep.dropped_rate, ref["dropped_rate"], "\ndispatch0", rep.initial_dispatch, ref["initial_dispatch"],
+              "\ncomm", rep.comm_us, rep.comm_measured_us, flush=True)
         np.testing.assert_allclose(rep.task_loss, ref["task_loss"], rtol=3e-2)
         np.testing.assert_allclose(rep.aux_loss, ref["aux_loss"], rtol=5e-2, atol=1e-6)
         np.testing.assert_allclose(rep.dropped_rate, ref["dropped_rate"], atol=0.02)
@@ -76,7 +79,8 @@ def main():
         # alpha-beta model of this step's dispatch matrix (comm_cost.cpp:24-55) next to the measured exchange
         pay = ops.device_payload_tokens(rep.initial_dispatch)
         rounds = 1 if cap in (1, 3) else 0
-        assert rep.comm_us[0] == (beta * pay * d * 4 / 1e6).max() + rounds * 0.0
+        want = (beta * (pay * (d * 4 / 1e6))).max() + rounds * 0.0
+        assert abs(rep.comm_us[0] - want) <= 1e-9 * want, (rep.comm_us[0], want)
         assert np.all(rep.comm_measured_us > 0)
         print(f"EP_TRAIN_OK world={world} kind={kind} cap={cap} task {rep.task_loss[0]:.5f}->{rep.task_loss[-1]:.5f} "
               f"(ref {ref['task_loss'][0]:.5f}->{ref['task_loss'][-1]:.5f}) comm model {np.mean(rep.comm_us):.2f} us, "
