@@ -417,16 +417,23 @@ def main():
     with clk:
         # one untimed step enqueued ahead of ev0: its device barriers re-align the ranks' GPUs after any host skew
         layer.step(x, y, params)
-        torch.cuda.synchronize()
-        nvl0 = nvl.read() if nvl else None
         ev0.record(stream)
         for _ in range(args.steps):
             layer.step(x, y, params)
         ev1.record(stream)
         clk.sample_now()  # after ev1 is enqueued: an NVML call between launches stalls this rank's stream
         torch.cuda.synchronize()
-        nvl1 = nvl.read() if nvl else None
     barrier()
+    nvl0 = nvl1 = None
+    if nvl is not None:
+        # NVLink byte counters over a separate, untimed run of the same steps (an NVML read between the barrier and
+        # the timed launches would bill host skew to the ranks waiting in the step's device barriers)
+        torch.cuda.synchronize()
+        nvl0 = nvl.read()
+        for _ in range(args.steps):
+            layer.step(x, y, params)
+        torch.cuda.synchronize()
+        nvl1 = nvl.read()
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     clocks = clk.summary()
     if world > 1:  # every rank sampled its own GPU: union of reasons, per-rank medians
@@ -468,17 +475,20 @@ def main():
         tx = (nvl1[0] - nvl0[0]) / args.steps if ok else -1.0
         rx = (nvl1[1] - nvl0[1]) / args.steps if ok else -1.0
         txm, rxm = max_over_ranks(tx), max_over_ranks(rx)  # collective on every rank
-        if txm >= 0:
+        if txm > 0:
             algo = float(sum(nbytes))
             a2a["nvlink_counters"] = {
-                "source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX field values, all links, read around the timed "
-                          "region (payload bytes; max over ranks)",
+                "source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX field values, all links, read around an untimed "
+                          "repeat of the timed steps (payload bytes; max over ranks)",
                 "tx_bytes_per_step": txm, "rx_bytes_per_step": rxm,
                 "algorithmic_offrank_bytes_per_step": algo,
                 "tx_over_algorithmic": txm / algo if algo else None,
                 "tx_gbs_over_step": txm / (ms / 1e3) / 1e9}
         else:
-            a2a["nvlink_counters"] = {"unavailable": nvl.err if nvl else "no NVML"}
+            a2a["nvlink_counters"] = {"unavailable": (nvl.err if nvl and nvl.err else
+                                                      "NVLink throughput counters not exposed on this box (NVML "
+                                                      "field values stay 0, nvidia-smi nvlink -gt d: N/A); see "
+                                                      "profiles/ for the ncu nvltx/nvlrx byte counters")}
     losses = layer.losses.cpu().tolist()
     value = world * S / (ms / 1e3)
 

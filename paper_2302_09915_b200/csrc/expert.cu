@@ -380,7 +380,7 @@ static int lpt() {
   return v;
 }
 
-static void check_groups(int G) { require(G >= 1 && G <= kMaxGroups, "group count out of range [1, 1024]"); }
+static void check_groups(int G) { require(G >= 1 && G <= kMaxGroups, "group count out of range [1, 512]"); }
 
 
 void grouped_fwd(const __nv_bfloat16* tokens, const __nv_bfloat16* w, int G, int M, int K, int R,

@@ -25,7 +25,7 @@ constexpr int kEpiWarps = 8;
 constexpr int kProducerWarp = kEpiWarps;
 constexpr int kMmaWarp = kEpiWarps + 1;
 constexpr int kGemmThreads = (kEpiWarps + 2) * 32;
-constexpr int kMaxGroups = 1024;
+constexpr int kMaxGroups = 512;  // groups (experts x source segments) per grouped launch
 
 enum GemmMode : int {
   kModeSwap = 0,    // M = weight rows (fixed), N = tokens of group g (variable), K fixed

@@ -58,11 +58,21 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    ndev = torch.cuda.device_count()
+    # more ranks than GPUs (e.g. C5's 2 x 4 tree on a 4-GPU lease): the NCCL-free bootstrap over gloo, ranks
+    # sharing GPUs round-robin -- the pipeline runs end to end, the timings are not per-GPU numbers
+    shared = ndev < world
+    torch.cuda.set_device(local % ndev)
+    dev = torch.device("cuda", local % ndev)
+    if shared:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
+    cdev = torch.device("cpu") if shared else dev  # device of the torch.distributed collectives
 
     def bcast_id():
+        if shared:
+            return None  # TAMoELayer all-gathers the workspace handles over the default (gloo) group
         obj = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         return obj[0]
@@ -78,7 +88,10 @@ def main():
 
     # ---- 1. measured profile -> c_hat
     sizes = (1.0, 4.0, 16.0, 64.0, 128.0)  # >= L2 at the top: the self link is a real HBM copy
-    samples = ops.p2p_sweep(bcast_id(), world, rank, sizes, reps=args.reps, warmup=2)
+    if shared:
+        samples = ops.p2p_sweep_store(world, rank, sizes, reps=args.reps, warmup=2)
+    else:
+        samples = ops.p2p_sweep(bcast_id(), world, rank, sizes, reps=args.reps, warmup=2)
     post = args.cross_throttle if args.posthoc else 1.0
     thr = [(i, j, mb, us * (post if (i // group_size != j // group_size) else 1.0))
            for (i, j, mb, us) in samples]
@@ -88,13 +101,13 @@ def main():
     alpha, beta = ops.fill_partial_profile(alpha, beta, levels)
     for S in token_list:
         run_size(args, ops, torch, dist, dev, rank, world, levels, emulate, sizes, alpha, beta, bcast_id,
-                 N, k, S, d, f, LayerConfig, TAMoELayer, LOSS_BALANCE, LOSS_TOPO, ACT_GELU)
+                 N, k, S, d, f, LayerConfig, TAMoELayer, LOSS_BALANCE, LOSS_TOPO, ACT_GELU, cdev, shared)
     dist.barrier()
     dist.destroy_process_group()
 
 
 def run_size(args, ops, torch, dist, dev, rank, world, levels, emulate, sizes, alpha, beta, bcast_id,
-             N, k, S, d, f, LayerConfig, TAMoELayer, LOSS_BALANCE, LOSS_TOPO, ACT_GELU):
+             N, k, S, d, f, LayerConfig, TAMoELayer, LOSS_BALANCE, LOSS_TOPO, ACT_GELU, cdev, shared):
     c_topo, a_hat, b_hat = ops.solve_target_tree(levels, alpha, beta, N, k, S)
     c_even = ops.target_closed_form(np.ones((world, world)), N, k, S)
 
@@ -139,7 +152,7 @@ def run_size(args, ops, torch, dist, dev, rank, world, levels, emulate, sizes, a
             layer.step(x, y, params)
         e1.record()
         torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+        t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = t.item()
         layer.enable_timing(True)
@@ -151,7 +164,7 @@ def run_size(args, ops, torch, dist, dev, rank, world, levels, emulate, sizes, a
         nbytes = layer.a2a_bytes()
         counts = layer.read(ops.R_COUNTS, (1, N)).astype(np.float64)
         dropped = layer.read(ops.R_DROPPED, (1, N)).sum()
-        allc = torch.tensor(counts, device=dev)
+        allc = torch.tensor(counts, device=cdev)
         gathered = [torch.zeros_like(allc) for _ in range(world)]
         dist.all_gather(gathered, allc)
         cmat = torch.cat(gathered, 0).cpu().numpy()  # [P x N] kept tokens: the dispatch matrix that happened
@@ -175,7 +188,8 @@ def run_size(args, ops, torch, dist, dev, rank, world, levels, emulate, sizes, a
 
     if rank == 0:
         out = {"config": {"workload": "C5 emulation" if args.cross_throttle != 1.0 else "C3",
-                          "gpus": world, "tokens_per_gpu": S, "levels": levels, "cross_throttle": args.cross_throttle,
+                          "ranks": world, "gpus": min(world, torch.cuda.device_count()),
+                          "ranks_share_gpus": shared, "tokens_per_rank": S, "levels": levels, "cross_throttle": args.cross_throttle,
                           "throttle_mode": ("links throttled (every cross-group payload store issued "
                                             f"{int(round(args.cross_throttle))}x), profile measured on them")
                           if emulate else ("post-hoc sample scaling" if args.cross_throttle != 1.0 else "none"),

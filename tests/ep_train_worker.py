@@ -62,7 +62,8 @@ def main():
                      beta_hat=beta)
     rep = train_layer(layer, params, xt, yt, tc, kind=LossKind(kind), c_hat=c_hat)
     # the report is identical on every rank
-    t = torch.tensor(np.concatenate([rep.task_loss, rep.aux_loss, rep.initial_dispatch.ravel()]))
+    t = torch.tensor(np.concatenate([rep.task_loss, rep.aux_loss, rep.initial_dispatch.ravel()]),
+                     device="cpu" if shared else "cuda")
     ref0 = t.clone()
     dist.broadcast(ref0, 0)
     assert torch.equal(t, ref0), "ranks disagree on the report"
