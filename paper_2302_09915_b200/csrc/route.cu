@@ -362,99 +362,57 @@ __global__ void __launch_bounds__(kPermWarps * 32) route_permute_kernel(RouteDim
   // Under expert parallelism the rows are owner-major; every rank starts at its own owner segment and walks
   // the owners cyclically, so at any moment the P senders target P different receivers (no incast on rank 0).
   const int rot = (map.P > 1 && me * map.E < N && rows > 0) ? min(start[me * map.E], rows) % rows : 0;
-  // warps stride over the rows (the block's expert scan above is amortised over many rows), two rows at a time:
-  // both rows' metadata, then both rows' loads, then both rows' stores -- twice the bytes in flight per warp
-  const int nv = dx / 8;
-  struct RowJob {
-    uint4* dst;
-    const uint4* src;  // null: pad row (zeros)
-    long long drow;
-    int dst_rank, rep;
-  };
-  auto prep = [&](int rl, RowJob& jb) {
-    const int r = rl + rot < rows ? rl + rot : rl + rot - rows;
-    int lo = 0, hi = N - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (start[mid] <= r) lo = mid; else hi = mid - 1;
-    }
-    const int e = lo;
-    const int j = r - start[e];
-    jb.dst_rank = map.rank_of(e);
-    jb.drow = map.P == 1 ? r : static_cast<long long>(r) - start[e] + map.dst_off[e];
-    jb.dst = reinterpret_cast<uint4*>(xp.p[jb.dst_rank] + jb.drow * dx);
-    jb.rep = xp.rep[jb.dst_rank];
-    jb.src = nullptr;
-    if (j < cnt[e]) {
-      const int pick = b.clist[b.list_start[e] + j];
-      const long long tok = pick / d.k;
-      if (lane == 0) {
-        b.pos[pick] = r;
-        if (has_codes) codes.p[jb.dst_rank][jb.drow] = (me << kPushRowBits) | pick;
-      }
-      jb.src = reinterpret_cast<const uint4*>(x + tok * dx);
-    } else if (lane == 0 && has_codes) {
-      codes.p[jb.dst_rank][jb.drow] = (me << kPushRowBits) | trash_row;
-    }
-  };
-  auto finish_pad = [&](const RowJob& jb) {  // the pad rows' dO rows (owner side) are zeroed too
-    if (jb.src == nullptr && has_z) {
-      uint4* zd = reinterpret_cast<uint4*>(zrows.p[jb.dst_rank] + jb.drow * zdim);
-      const uint4 z = make_uint4(0, 0, 0, 0);
-      for (int v = lane; v < zdim / 8; v += 32) zd[v] = z;
-    }
-  };
-  constexpr int kU2 = 4;  // two-row path: 16-byte vectors per lane and row (rows up to 2 KiB: d <= 1024)
-  constexpr int kU = 8;   // one-row path for wider rows
-  const int stride = gridDim.x * kPermWarps;
-  int rl = blockIdx.x * kPermWarps + warp;
-  if (nv <= 32 * kU2) {
-    for (; rl < rows; rl += 2 * stride) {
-      RowJob jb[2];
-      const bool two = rl + stride < rows;
-      prep(rl, jb[0]);
-      if (two) prep(rl + stride, jb[1]);
-      uint4 t[2][kU2];
-#pragma unroll
-      for (int q = 0; q < 2; ++q)
-#pragma unroll
-        for (int u = 0; u < kU2; ++u) {
-          const int v = lane + 32 * u;
-          t[q][u] = make_uint4(0, 0, 0, 0);
-          if ((q == 0 || two) && v < nv && jb[q].src) t[q][u] = __ldg(jb[q].src + v);
-        }
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        if (q == 1 && !two) break;
-#pragma unroll
-        for (int u = 0; u < kU2; ++u) {
-          const int v = lane + 32 * u;
-          if (v < nv) {
-            jb[q].dst[v] = t[q][u];
-            if (jb[q].rep > 1) store_repeat(jb[q].dst + v, t[q][u], jb[q].rep);
-          }
-        }
-        finish_pad(jb[q]);
-      }
-    }
-    return;
+  // warps stride over the rows (the block's expert scan above is amortised over many rows)
+  for (int rl = blockIdx.x * kPermWarps + warp; rl < rows; rl += gridDim.x * kPermWarps) {
+  const int r = rl + rot < rows ? rl + rot : rl + rot - rows;
+  int lo = 0, hi = N - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (start[mid] <= r) lo = mid; else hi = mid - 1;
   }
-  for (; rl < rows; rl += stride) {  // wide rows: one row at a time, kU vectors per lane per pass
-    RowJob jb;
-    prep(rl, jb);
+  const int e = lo;
+  const int j = r - start[e];
+  const int dst_rank = map.rank_of(e);
+  const long long drow = map.P == 1 ? r : static_cast<long long>(r) - start[e] + map.dst_off[e];
+  uint4* dst = reinterpret_cast<uint4*>(xp.p[dst_rank] + drow * dx);
+  const int nv = dx / 8;
+  const int rep = xp.rep[dst_rank];
+  if (j < cnt[e]) {
+    const int pick = b.clist[b.list_start[e] + j];
+    const long long tok = pick / d.k;
+    if (lane == 0) {
+      b.pos[pick] = r;
+      if (has_codes) codes.p[dst_rank][drow] = (me << kPushRowBits) | pick;
+    }
+    const uint4* src = reinterpret_cast<const uint4*>(x + tok * dx);
+    // whole row in registers first (up to 8 x 16 B per lane), then the stores back to back
+    constexpr int kU = 8;
     for (int v0 = lane; v0 < nv; v0 += 32 * kU) {
       uint4 t[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u)
-        t[u] = (v0 + 32 * u < nv && jb.src) ? __ldg(jb.src + v0 + 32 * u) : make_uint4(0, 0, 0, 0);
+        if (v0 + 32 * u < nv) t[u] = __ldg(src + v0 + 32 * u);
 #pragma unroll
       for (int u = 0; u < kU; ++u)
-        if (v0 + 32 * u < nv) {
-          jb.dst[v0 + 32 * u] = t[u];
-          if (jb.rep > 1) store_repeat(jb.dst + v0 + 32 * u, t[u], jb.rep);
-        }
+        if (v0 + 32 * u < nv) dst[v0 + 32 * u] = t[u];
+      if (rep > 1) {
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+          if (v0 + 32 * u < nv) store_repeat(dst + v0 + 32 * u, t[u], rep);
+      }
     }
-    finish_pad(jb);
+  } else {
+    if (lane == 0 && has_codes) codes.p[dst_rank][drow] = (me << kPushRowBits) | trash_row;
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    for (int v = lane; v < nv; v += 32) {
+      dst[v] = z;
+      if (rep > 1) store_repeat(dst + v, z, rep);
+    }
+    if (has_z) {
+      uint4* zd = reinterpret_cast<uint4*>(zrows.p[dst_rank] + drow * zdim);
+      for (int v = lane; v < zdim / 8; v += 32) zd[v] = z;
+    }
+  }
   }
 }
 
