@@ -605,8 +605,11 @@ def main():
             "hbm_gbs": gbs, "hbm_frac": gbs / pk["hbm"],
             "note": "launch durations from CUDA events on the step stream around each GEMM (eager phase steps); "
                     "rows = nominal T*k (picks dropped by capacity not subtracted, pad rows not added)"}
-    prof_traffic = os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")
-    if os.path.exists(prof_traffic) and world == 1:
+    # the newest committed ncu --set full capture of the same step (scripts/profile_round.sh -> ncu_summary.py)
+    import glob
+    caps = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_gemm_traffic.json")))
+    prof_traffic = caps[-1] if caps else ""
+    if prof_traffic and world == 1:
         with open(prof_traffic) as f:
             roof["traffic"] = json.load(f).get("traffic_bytes_per_launch")
 
