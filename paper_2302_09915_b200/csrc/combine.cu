@@ -41,7 +41,7 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
 // slot in flight before computing, so the warp has (k + 1) * kU * 512 B of loads outstanding.
 // NPL > 0: the gate dz pass is fused in (experts per lane, N <= 32 * NPL).
 template <int KT, int NPL>
-__global__ void __launch_bounds__(kCombWarps * 32, KT == 1 ? 8 : 1) combine_loss_kernel(const __grid_constant__ CombineArgs a) {
+__global__ void __launch_bounds__(kCombWarps * 32) combine_loss_kernel(const __grid_constant__ CombineArgs a) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
   constexpr int KM = KT > 0 ? KT : kMaxTopK;

@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(kCapThreads) route_capacity_kernel(RouteDims d
 // One warp per destination row of the padded expert-sorted buffer.
 constexpr int kPermWarps = 8;
 
-__global__ void __launch_bounds__(kPermWarps * 32, 8) route_permute_kernel(RouteDims d, RouteBuffers b,
+__global__ void __launch_bounds__(kPermWarps * 32) route_permute_kernel(RouteDims d, RouteBuffers b,
                                                                         const __nv_bfloat16* __restrict__ x, int dx,
                                                                         const __grid_constant__ PeerBufs xp, int r_max,
                                                                         const __grid_constant__ PeerBufs zrows,
@@ -385,9 +385,8 @@ __global__ void __launch_bounds__(kPermWarps * 32, 8) route_permute_kernel(Route
       if (has_codes) codes.p[dst_rank][drow] = (me << kPushRowBits) | pick;
     }
     const uint4* src = reinterpret_cast<const uint4*>(x + tok * dx);
-    // whole row in registers first (4 x 16 B per lane: a 1,024-wide bf16 row in one pass), then the stores back
-    // to back; 4 (not 8) vectors keep the kernel at <= 32 registers, i.e. 8 resident blocks (64 warps) per SM
-    constexpr int kU = 4;
+    // whole row in registers first (up to 8 x 16 B per lane), then the stores back to back
+    constexpr int kU = 8;
     for (int v0 = lane; v0 < nv; v0 += 32 * kU) {
       uint4 t[kU];
 #pragma unroll
