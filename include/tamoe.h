@@ -118,7 +118,7 @@ int tamoe_exchange_cost(const double* alpha, const double* beta, const double* c
 /* ------------------------------------------------------------------ grouped expert GEMMs (device)
  * Building blocks of the expert FFN (trainer.cpp:284-289 / 310-316 generalised).
  * tokens are bf16 [R x K] row-major; group g owns rows [seg_start[g], seg_start[g]+seg_rows[g]),
- * seg_rows multiple of 16 (zero padded).  seg_start / seg_rows are device int32[G], 1 <= G <= 512.
+ * seg_rows multiple of 16 (zero padded).  seg_start / seg_rows are device int32[G], 1 <= G <= 256.
  * grouped_fwd: out = act(tokens W_g^T), pre_out (optional) = act'(tokens W_g^T) kept for the backward;
  * grouped_dgrad: out = (grad_tokens W_g) * pre_in (elementwise; pre_in = that act', optional). */
 int tamoe_grouped_fwd(const void* tokens, const void* w, int G, int M, int K, int R, const int* seg_start,

@@ -368,19 +368,10 @@ static SwapParams swap_params(__nv_bfloat16* out, __nv_bfloat16* pre_out, const 
   return e;
 }
 
-static int env_int(const char* name, int dflt) {
-  const char* v = std::getenv(name);
-  return v ? std::atoi(v) : dflt;
-}
 
-// Size-ordered, boustrophedon tile schedule of the swap GEMMs (TAMOE_LPT=1; off: measured 3-8 % slower than the
-// plain round robin at C2), read once
-static int lpt() {
-  static const int v = env_int("TAMOE_LPT", 0);
-  return v;
-}
 
-static void check_groups(int G) { require(G >= 1 && G <= kMaxGroups, "group count out of range [1, 512]"); }
+
+static void check_groups(int G) { require(G >= 1 && G <= kMaxGroups, "group count out of range [1, 256]"); }
 
 
 void grouped_fwd(const __nv_bfloat16* tokens, const __nv_bfloat16* w, int G, int M, int K, int R,
@@ -393,7 +384,7 @@ void grouped_fwd(const __nv_bfloat16* tokens, const __nv_bfloat16* w, int G, int
   const int Gw = w_mod > 0 ? w_mod : G;  // distinct weight matrices
   CUtensorMap ta = make_tmap_bf16(w, K, static_cast<uint64_t>(Gw) * M, K, kBM);
   CUtensorMap tb = make_tmap_bf16(tokens, K, R, K, swap_token_box(pair));
-  GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1, w_mod, 1, 0, 0, lpt()};
+  GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1, w_mod, 1, 0, 0};
   SwapParams ep = swap_params(out, pre_out, nullptr, M, R, act, kActNone);
   require(!(push && pre_out), "grouped_fwd: push needs a plain output");
   if (push) {
@@ -417,7 +408,7 @@ void grouped_dgrad(const __nv_bfloat16* grad_tokens, const __nv_bfloat16* w, int
   const int Gw = w_mod > 0 ? w_mod : G;
   CUtensorMap ta = make_tmap_bf16(w, M, static_cast<uint64_t>(Gw) * K, M, 64);
   CUtensorMap tb = make_tmap_bf16(grad_tokens, K, R, K, swap_token_box(pair));
-  GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1, w_mod, 1, 0, 0, lpt()};
+  GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1, w_mod, 1, 0, 0};
   SwapParams ep = swap_params(out, nullptr, pre_in, M, R, kActNone, pre_in ? act : kActNone);
   require(!(push && pre_in), "grouped_dgrad: push needs a plain output");
   if (push) {

@@ -25,7 +25,7 @@ constexpr int kEpiWarps = 8;
 constexpr int kProducerWarp = kEpiWarps;
 constexpr int kMmaWarp = kEpiWarps + 1;
 constexpr int kGemmThreads = (kEpiWarps + 2) * 32;
-constexpr int kMaxGroups = 512;  // groups (experts x source segments) per grouped launch
+constexpr int kMaxGroups = 256;  // groups (experts, or expert x source segments) per grouped launch
 
 enum GemmMode : int {
   kModeSwap = 0,    // M = weight rows (fixed), N = tokens of group g (variable), K fixed
@@ -48,15 +48,11 @@ struct GemmParams {
   int nsub;              // kModeWgrad: K of group g = sub-segments s*num_groups + g, s < nsub
   int pf_dist;           // unused (an L2 prefetch experiment, measured no gain)
   int pf_b;              // unused
-  int lpt;               // kModeSwap: groups in descending token-tile size, tiles dealt to the CTA pairs in
-                         // boustrophedon order (largest first, alternating direction per round) -- evens out
-                         // the last round of the persistent schedule
 };
 
-// i-th tile of persistent cluster c out of nc (>= the tile count: done).  Snake: rounds alternate direction.
-__device__ __forceinline__ int sched_tile(int i, int c, int nc, bool snake) {
-  return i * nc + ((snake && (i & 1)) ? nc - 1 - c : c);
-}
+// i-th tile of persistent cluster c out of nc (>= the tile count: done): round robin.  (A size-ordered,
+// boustrophedon schedule and a split of the last round were measured slower / no faster: DESIGN.md 3.1.)
+__device__ __forceinline__ int sched_tile(int i, int c, int nc) { return i * nc + c; }
 
 struct TileInfo {
   int g;       // group
@@ -110,8 +106,10 @@ struct GemmSmem {
   static constexpr int kBBytes = (BN / (kCG == 1 ? 1 : 2)) * kBK * 2;  // a CTA pair splits B's N between its CTAs
   static constexpr int kStageBytes = kABytes + kBBytes;
   // barriers: full[S], empty[S], tfull[2], tempty[2]; tmem addr; tile prefix; group starts / rows
-  static constexpr int kMiscBytes = (2 * 8 + 4) * 8 + 16 + (4 * kMaxGroups + 1) * 4;
-  static constexpr int kBudget = 227 * 1024 - ((kEpiBytes + 1023) / 1024) * 1024 - kMiscBytes - 2048;
+  // barriers + TMEM address + the tile prefix; the group table itself is read from global memory (L1-resident),
+  // so the pipeline gets every byte it can (one more stage for the FFN forward / wgrad / K = 4096 GEMMs)
+  static constexpr int kMiscBytes = (2 * 8 + 4) * 8 + 16 + (kMaxGroups + 1) * 4;
+  static constexpr int kBudget = 227 * 1024 - ((kEpiBytes + 1023) / 1024) * 1024 - kMiscBytes - 1024;
 #ifdef TAMOE_MAX_STAGES
   static constexpr int kMaxStages = TAMOE_MAX_STAGES;  // A/B experiments only
 #else
@@ -155,7 +153,7 @@ __device__ __forceinline__ int group_tiles(const GemmParams& p, int rows) {
 
 template <int kMode, int BN, int kCG = 1>
 __device__ __forceinline__ void decode_tile(const GemmParams& p, const int* prefix, const int* s_start,
-                                            const int* s_rows, const int* s_gid, int t, TileInfo& ti) {
+                                            const int* s_rows, int t, TileInfo& ti) {
   // find group: prefix[g] <= t < prefix[g+1]
   int lo = 0, hi = p.num_groups - 1;
   while (lo < hi) {
@@ -171,8 +169,7 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, const int* pref
     const int nb = swap_ntiles<BN>(rows);
     const int ns = swap_nsize<BN>(rows);
     const int mb = r / nb, nbk = r % nb;
-    const int gg = s_gid[g];  // the group's weight (groups may be visited in size order)
-    ti.wg = p.w_mod > 0 ? gg % p.w_mod : gg;
+    ti.wg = p.w_mod > 0 ? g % p.w_mod : g;
     ti.m0 = mb * kBM * kCG;
     ti.n0 = nbk * ns;
     ti.n = min(ns, rows - ti.n0);
@@ -259,9 +256,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   int* prefix = reinterpret_cast<int*>(tmem_slot + 4);
-  int* s_start = prefix + kMaxGroups + 1;
-  int* s_rows = s_start + kMaxGroups;
-  int* s_gid = s_rows + kMaxGroups;
+  // group table: global (seg_start / seg_rows of the grouped modes; the gate modes have one implicit group)
+  const int* s_start = p.seg_start;
+  const int* s_rows = p.seg_rows;
 
   const int warp = ptx::warp_id();
   const int lane = ptx::lane_id();
@@ -292,52 +289,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     else ptx::tmem_alloc<L::kTmemCols>(tmem_slot);
   }
   ptx::pdl_wait();
-  // group table -> smem (parallel loads), then a warp-parallel prefix of the tile counts
+  // warp-parallel prefix of the groups' tile counts (smem)
   const int G = p.num_groups;
-  const bool grouped = (kMode == kModeSwap || kMode == kModeWgrad);
-  const int nseg = (kMode == kModeWgrad) ? G * p.nsub : G;
-  for (int g = threadIdx.x; g < nseg; g += blockDim.x) {
-    s_start[g] = grouped ? p.seg_start[g] : 0;
-    s_rows[g] = grouped ? p.seg_rows[g] : 0;
-    s_gid[g] = g;
-  }
-  __syncthreads();
-  const bool snake = kMode == kModeSwap && p.lpt != 0;
-  if (snake) {
-    // stable order by token-tile size, descending: rank of every group, then the table permuted into it
-    constexpr int kPer = (kMaxGroups + kGemmThreads - 1) / kGemmThreads;
-    int rk[kPer], st[kPer], rw[kPer];
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-      const int g = threadIdx.x + j * kGemmThreads;
-      rk[j] = -1;
-      if (g < G) {
-        const int ns = swap_nsize<BN>(s_rows[g]);
-        int r = 0;
-        for (int h = 0; h < G; ++h) {
-          const int nh = swap_nsize<BN>(s_rows[h]);
-          r += (nh > ns) || (nh == ns && h < g);
-        }
-        rk[j] = r;
-        st[j] = s_start[g];
-        rw[j] = s_rows[g];
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kPer; ++j)
-      if (rk[j] >= 0) {
-        s_start[rk[j]] = st[j];
-        s_rows[rk[j]] = rw[j];
-        s_gid[rk[j]] = threadIdx.x + j * kGemmThreads;
-      }
-    __syncthreads();
-  }
+  constexpr bool grouped = (kMode == kModeSwap || kMode == kModeWgrad);
   if (warp == 0) {
     int carry = 0;
     for (int g0 = 0; g0 < G; g0 += 32) {
       const int g = g0 + lane;
-      const int c = g < G ? group_tiles<kMode, BN, kCG>(p, s_rows[g]) : 0;
+      const int c = g < G ? group_tiles<kMode, BN, kCG>(p, grouped ? s_rows[g] : 0) : 0;
       int x = c;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -374,10 +333,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       };
       for (int i = 0;; ++i) {
-        const int t = sched_tile(i, cluster_id, num_clusters, snake);
+        const int t = sched_tile(i, cluster_id, num_clusters);
         if (t >= total_tiles) break;
         TileInfo ti;
-        decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, s_gid, t, ti);
+        decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, t, ti);
         localize(ti);
         // K ranges: wgrad walks the group's (source) sub-segments; every other mode has one range
         const int nsub = (kMode == kModeWgrad) ? p.nsub : 1;
@@ -443,10 +402,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t phase = 0;
       int it = 0;
       for (;; ++it) {
-        const int t = sched_tile(it, cluster_id, num_clusters, snake);
+        const int t = sched_tile(it, cluster_id, num_clusters);
         if (t >= total_tiles) break;
         TileInfo ti;
-        decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, s_gid, t, ti);
+        decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, t, ti);
         const int buf = it & 1;
         const uint32_t use = static_cast<uint32_t>(it >> 1);
         ptx::mbar_wait(&tempty_bar[buf], (use & 1) ^ 1);
@@ -510,18 +469,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if constexpr (EpiAhead<Epi>::value) {
       static_assert(!EpiEarly<Epi>::value, "tile-ahead epilogues release TMEM after run()");
       TileInfo nx;
-      if (sched_tile(0, cluster_id, num_clusters, snake) < total_tiles) {
-        decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, s_gid, sched_tile(0, cluster_id, num_clusters, snake),
+      if (sched_tile(0, cluster_id, num_clusters) < total_tiles) {
+        decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, sched_tile(0, cluster_id, num_clusters),
                                     nx);
         nx.m0 += static_cast<int>(rank) * kBM;
         Epi::prefetch(ep, p, nx, q, h, lane, wsm, s_start);
       }
       for (;; ++it) {
-        if (sched_tile(it, cluster_id, num_clusters, snake) >= total_tiles) break;
+        if (sched_tile(it, cluster_id, num_clusters) >= total_tiles) break;
         const TileInfo ti = nx;
-        const int tn = sched_tile(it + 1, cluster_id, num_clusters, snake);
+        const int tn = sched_tile(it + 1, cluster_id, num_clusters);
         if (tn < total_tiles) {
-          decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, s_gid, tn, nx);
+          decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, tn, nx);
           nx.m0 += static_cast<int>(rank) * kBM;
           Epi::prefetch(ep, p, nx, q, h, lane, wsm + ((it + 1) & 1) * Epi::kBufBytes, s_start);
         } else {
@@ -542,10 +501,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     } else
     for (;; ++it) {
-      const int t = sched_tile(it, cluster_id, num_clusters, snake);
+      const int t = sched_tile(it, cluster_id, num_clusters);
       if (t >= total_tiles) break;
       TileInfo ti;
-      decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, s_gid, t, ti);
+      decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, t, ti);
       ti.m0 += static_cast<int>(rank) * kBM;  // this CTA's 128 accumulator rows
       const int buf = it & 1;
       const uint32_t use = static_cast<uint32_t>(it >> 1);
