@@ -14,6 +14,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.hpp"
 #include "expert.hpp"
@@ -320,6 +321,33 @@ struct EpiWgrad {
   }
 };
 
+// ---------------------------------------------------------------- chained swap GEMMs
+// Two swap GEMMs in one persistent launch (GemmParams::chain): tiles of the first use E0, tiles of the second E1 and
+// the second's tensor maps.  FFN forward: fwd1 (E0 = act + act' out) -> fwd2 (E1 = plain / pushed output); FFN
+// backward: dgrad2 (E0 = x act') -> dgrad1 (E1).
+template <class E0, class E1>
+struct EpiChain {
+  static constexpr bool kChained = true;
+  static constexpr bool kEarlyRelease = true;
+  static_assert(E0::kEarlyRelease && E1::kEarlyRelease, "chained epilogues release TMEM early");
+  static constexpr int kWarpBytes = E0::kWarpBytes > E1::kWarpBytes ? E0::kWarpBytes : E1::kWarpBytes;
+  struct Params {
+    typename E0::Params p0;
+    typename E1::Params p1;
+    CUtensorMap tmA2, tmB2;  // the second GEMM's operands
+  };
+  // the engine runs the two phases' tiles in two consecutive epilogue loops (a CTA's first-GEMM tiles all precede
+  // its second-GEMM tiles), so each loop inlines only its own epilogue body
+  using First = E0;
+  using Second = E1;
+  static __device__ __forceinline__ const typename E0::Params& params(const Params& e, std::integral_constant<int, 0>) {
+    return e.p0;
+  }
+  static __device__ __forceinline__ const typename E1::Params& params(const Params& e, std::integral_constant<int, 1>) {
+    return e.p1;
+  }
+};
+
 // cg: CTAs per cluster -- 1, 2 (a pair: cta_group::2, M = 256) or 4 (two pairs on adjacent 256-row weight blocks
 // sharing the token operand by TMA multicast)
 template <int kMode, int BN, bool A_MN, bool B_MN, class Epi>
@@ -433,6 +461,77 @@ void grouped_wgrad(const __nv_bfloat16* a_tokens, const __nv_bfloat16* b_tokens,
   GemmParams p{G, seg_start, seg_rows, M, N, 0, 1, 1, 1, 1, 0, nsub, 0, 0};
   EpiWgrad::Params ep{make_tmap_bf16_box(out, N, static_cast<uint64_t>(G) * M, N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)};
   launch_pair_or_single<kModeWgrad, 256, true, true, EpiWgrad>(M % 256 == 0 ? 2 : 1, ta, tb, p, ep, s);
+}
+
+static void chain_params(GemmParams& p, int M2, int K2, int* ready, int stride, int M1) {
+  p.chain = 1;
+  p.Mw2 = M2;
+  p.Kw2 = K2;
+  p.ready = ready;
+  p.ready_stride = stride;
+  // every epilogue warp of both CTAs of every first-GEMM m block signals once per (group, token tile)
+  p.ready_target = (M1 / 256) * kEpiWarps * 2;
+}
+
+int chain_ready_stride(int R) { return (R + 255) / 256 + 1; }
+
+void grouped_ffn_fwd_chain(const __nv_bfloat16* tokens, const __nv_bfloat16* w1, const __nv_bfloat16* w2, int G,
+                           int f, int d, int d_out, int R, const int* seg_start, const int* seg_rows,
+                           __nv_bfloat16* H, __nv_bfloat16* dact, __nv_bfloat16* out, int act, int* ready,
+                           cudaStream_t s, int w_mod, const SwapPush* push) {
+  check_groups(G);
+  require(f % 256 == 0 && d_out % 256 == 0 && d % 64 == 0 && f % 64 == 0, "chained FFN forward: f, d_out % 256");
+  const int Gw = w_mod > 0 ? w_mod : G;
+  CUtensorMap ta = make_tmap_bf16(w1, d, static_cast<uint64_t>(Gw) * f, d, kBM);
+  CUtensorMap tb = make_tmap_bf16(tokens, d, R, d, swap_token_box(2));
+  GemmParams p{G, seg_start, seg_rows, f, 0, d, 1, 1, 1, 1, w_mod, 1, 0, 0};
+  const int stride = chain_ready_stride(R);
+  chain_params(p, d_out, f, ready, stride, f);
+  TAMOE_CUDA(cudaMemsetAsync(ready, 0, sizeof(int) * static_cast<size_t>(G) * stride, s));
+  if (push) {
+    EpiChain<EpiSwap<1>, EpiSwap<3>>::Params ep{swap_params(H, dact, nullptr, f, R, act, kActNone),
+                                                swap_params(out, nullptr, nullptr, d_out, R, kActNone, kActNone),
+                                                make_tmap_bf16(w2, f, static_cast<uint64_t>(Gw) * d_out, f, kBM),
+                                                make_tmap_bf16(H, f, R, f, swap_token_box(2))};
+    ep.p1.push = *push;
+    launch_gemm<kModeSwap, 256, false, false, EpiChain<EpiSwap<1>, EpiSwap<3>>, 2>(ta, tb, p, ep, 0, s);
+  } else {
+    EpiChain<EpiSwap<1>, EpiSwap<0>>::Params ep{swap_params(H, dact, nullptr, f, R, act, kActNone),
+                                                swap_params(out, nullptr, nullptr, d_out, R, kActNone, kActNone),
+                                                make_tmap_bf16(w2, f, static_cast<uint64_t>(Gw) * d_out, f, kBM),
+                                                make_tmap_bf16(H, f, R, f, swap_token_box(2))};
+    launch_gemm<kModeSwap, 256, false, false, EpiChain<EpiSwap<1>, EpiSwap<0>>, 2>(ta, tb, p, ep, 0, s);
+  }
+}
+
+void grouped_ffn_dgrad_chain(const __nv_bfloat16* dO, const __nv_bfloat16* w2, const __nv_bfloat16* w1, int G, int f,
+                             int d, int d_out, int R, const int* seg_start, const int* seg_rows, __nv_bfloat16* dA,
+                             const __nv_bfloat16* dact, __nv_bfloat16* dx_out, int act, int* ready, cudaStream_t s,
+                             int w_mod, const SwapPush* push) {
+  // dA[R x f] = (dO[R x d_out] . W2_g) * act';  dx[R x d] = dA . W1_g   (W2_g stored d_out x f, W1_g f x d: MN-major A)
+  check_groups(G);
+  require(f % 256 == 0 && d % 256 == 0 && d_out % 64 == 0 && f % 64 == 0, "chained FFN dgrad: f, d % 256");
+  const int Gw = w_mod > 0 ? w_mod : G;
+  CUtensorMap ta = make_tmap_bf16(w2, f, static_cast<uint64_t>(Gw) * d_out, f, 64);
+  CUtensorMap tb = make_tmap_bf16(dO, d_out, R, d_out, swap_token_box(2));
+  GemmParams p{G, seg_start, seg_rows, f, 0, d_out, 1, 1, 1, 1, w_mod, 1, 0, 0};
+  const int stride = chain_ready_stride(R);
+  chain_params(p, d, f, ready, stride, f);
+  TAMOE_CUDA(cudaMemsetAsync(ready, 0, sizeof(int) * static_cast<size_t>(G) * stride, s));
+  if (push) {
+    EpiChain<EpiSwap<2>, EpiSwap<3>>::Params ep{swap_params(dA, nullptr, dact, f, R, kActNone, act),
+                                                swap_params(dx_out, nullptr, nullptr, d, R, kActNone, kActNone),
+                                                make_tmap_bf16(w1, d, static_cast<uint64_t>(Gw) * f, d, 64),
+                                                make_tmap_bf16(dA, f, R, f, swap_token_box(2))};
+    ep.p1.push = *push;
+    launch_gemm<kModeSwap, 256, true, false, EpiChain<EpiSwap<2>, EpiSwap<3>>, 2>(ta, tb, p, ep, 0, s);
+  } else {
+    EpiChain<EpiSwap<2>, EpiSwap<0>>::Params ep{swap_params(dA, nullptr, dact, f, R, kActNone, act),
+                                                swap_params(dx_out, nullptr, nullptr, d, R, kActNone, kActNone),
+                                                make_tmap_bf16(w1, d, static_cast<uint64_t>(Gw) * f, d, 64),
+                                                make_tmap_bf16(dA, f, R, f, swap_token_box(2))};
+    launch_gemm<kModeSwap, 256, true, false, EpiChain<EpiSwap<2>, EpiSwap<0>>, 2>(ta, tb, p, ep, 0, s);
+  }
 }
 
 }  // namespace tamoe

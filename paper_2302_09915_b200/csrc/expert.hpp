@@ -33,4 +33,18 @@ void grouped_dgrad(const __nv_bfloat16* grad_tokens, const __nv_bfloat16* w, int
 void grouped_wgrad(const __nv_bfloat16* a_tokens, const __nv_bfloat16* b_tokens, int G, int M, int N, int R,
                    const int* seg_start, const int* seg_rows, __nv_bfloat16* out, cudaStream_t s, int nsub = 1);
 
+// The FFN's two forward GEMMs (H = act(X W1^T) with act' kept, then O = H W2^T) in one persistent launch: CTAs that
+// finish the first GEMM start the second as soon as the H rows of a (group, token tile) are stored.  ready: device
+// int [G x chain_ready_stride(R)] scratch (zeroed by the call).  Needs f, d_out multiples of 256 (CTA pairs).
+int chain_ready_stride(int R);
+void grouped_ffn_fwd_chain(const __nv_bfloat16* tokens, const __nv_bfloat16* w1, const __nv_bfloat16* w2, int G,
+                           int f, int d, int d_out, int R, const int* seg_start, const int* seg_rows,
+                           __nv_bfloat16* H, __nv_bfloat16* dact, __nv_bfloat16* out, int act, int* ready,
+                           cudaStream_t s, int w_mod = 0, const SwapPush* push = nullptr);
+// The FFN's two input-gradient GEMMs (dA = (dO W2) * act', then dX = dA W1) in one persistent launch.
+void grouped_ffn_dgrad_chain(const __nv_bfloat16* dO, const __nv_bfloat16* w2, const __nv_bfloat16* w1, int G, int f,
+                             int d, int d_out, int R, const int* seg_start, const int* seg_rows, __nv_bfloat16* dA,
+                             const __nv_bfloat16* dact, __nv_bfloat16* dx_out, int act, int* ready, cudaStream_t s,
+                             int w_mod = 0, const SwapPush* push = nullptr);
+
 }  // namespace tamoe

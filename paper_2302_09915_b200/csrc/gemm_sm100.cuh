@@ -15,6 +15,8 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <type_traits>
+
 #include "ptx.cuh"
 
 namespace tamoe {
@@ -48,6 +50,15 @@ struct GemmParams {
   int nsub;              // kModeWgrad: K of group g = sub-segments s*num_groups + g, s < nsub
   int pf_dist;           // unused (an L2 prefetch experiment, measured no gain)
   int pf_b;              // unused
+  // kModeSwap chain: a second swap GEMM (Mw2 x Kw2, tensor maps / epilogue from EpiChain) whose token operand is
+  // the first one's output, in the same persistent launch.  Its tiles follow the first GEMM's in the schedule; a
+  // CTA reaching a second-GEMM tile waits until every first-GEMM tile of that (group, token tile) has stored its
+  // rows (ready[g * ready_stride + tile] == ready_target), so CTAs that finish the first GEMM early start the
+  // second one instead of idling at a kernel boundary.
+  int chain;
+  int Mw2, Kw2;
+  int* ready;
+  int ready_stride, ready_target;
 };
 
 // i-th tile of persistent cluster c out of nc (>= the tile count: done): round robin.  (A size-ordered,
@@ -55,6 +66,8 @@ struct GemmParams {
 __device__ __forceinline__ int sched_tile(int i, int c, int nc) { return i * nc + c; }
 
 struct TileInfo {
+  int phase;   // kModeSwap chain: 0 first GEMM, 1 second
+  int tj;      // kModeSwap: token tile index within the group
   int g;       // group
   int wg;      // weight index (kModeSwap)
   int m0, n0;  // offsets within the group's output
@@ -100,6 +113,17 @@ struct EpiSmem<Epi, decltype(void(Epi::kWarpBytes))> {
   static constexpr int value = Epi::kWarpBytes * kEpiWarps;
 };
 
+// Epilogues of a chained swap launch (EpiChain, expert.cu) declare `static constexpr bool kChained = true` and carry
+// the second GEMM's tensor maps (tmA2 / tmB2) in their Params.
+template <class Epi, class = void>
+struct EpiChained {
+  static constexpr bool value = false;
+};
+template <class Epi>
+struct EpiChained<Epi, decltype(void(Epi::kChained))> {
+  static constexpr bool value = Epi::kChained;
+};
+
 template <int BN, int kEpiBytes = 0, int kCG = 1>
 struct GemmSmem {
   static constexpr int kABytes = kBM * kBK * 2;
@@ -139,7 +163,7 @@ __device__ __forceinline__ int swap_nsize(int rows) {
 template <int kMode, int BN, int kCG = 1>
 __device__ __forceinline__ int group_tiles(const GemmParams& p, int rows) {
   if constexpr (kMode == kModeSwap) {
-    return (p.Mw / (kBM * kCG)) * swap_ntiles<BN>(rows);
+    return swap_ntiles<BN>(rows);  // token tiles; a tile = (m block, token tile), see decode_tile
   } else if constexpr (kMode == kModeWgrad) {
     return (p.Mw / (kBM * kCG)) * (p.Nw / BN);
   } else if constexpr (kMode == kModeGate) {
@@ -151,9 +175,53 @@ __device__ __forceinline__ int group_tiles(const GemmParams& p, int rows) {
   }
 }
 
+// Tiles of a swap launch: every group's (m block, token tile) pairs, m-block-major within the group; with a chain,
+// the second GEMM's tiles follow all of the first's.  prefix[] holds the groups' token-tile prefix.
+template <int BN, int kCG>
+__device__ __forceinline__ int swap_total_tiles(const GemmParams& p, const int* prefix) {
+  const int nt = prefix[p.num_groups];
+  return (p.Mw / (kBM * kCG)) * nt + (p.chain ? (p.Mw2 / (kBM * kCG)) * nt : 0);
+}
+
 template <int kMode, int BN, int kCG = 1>
 __device__ __forceinline__ void decode_tile(const GemmParams& p, const int* prefix, const int* s_start,
                                             const int* s_rows, int t, TileInfo& ti) {
+  ti.phase = 0;
+  ti.tj = 0;
+  if constexpr (kMode == kModeSwap) {
+    int MB = p.Mw / (kBM * kCG), Mw = p.Mw, Kw = p.Kw;
+    const int t1 = MB * prefix[p.num_groups];
+    if (p.chain && t >= t1) {
+      t -= t1;
+      ti.phase = 1;
+      MB = p.Mw2 / (kBM * kCG);
+      Mw = p.Mw2;
+      Kw = p.Kw2;
+    }
+    int lo = 0, hi = p.num_groups - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (MB * prefix[mid] <= t) lo = mid; else hi = mid - 1;
+    }
+    const int g = lo;
+    const int r = t - MB * prefix[g];
+    const int rows = s_rows[g];
+    const int nb = swap_ntiles<BN>(rows);
+    const int ns = swap_nsize<BN>(rows);
+    const int mb = r / nb, nbk = r % nb;
+    ti.g = g;
+    ti.ks = 0;
+    ti.tj = nbk;
+    ti.wg = p.w_mod > 0 ? g % p.w_mod : g;
+    ti.m0 = mb * kBM * kCG;
+    ti.n0 = nbk * ns;
+    ti.n = min(ns, rows - ti.n0);
+    ti.k_len = Kw;
+    // A (weights): K-major -> (k, g*Mw + m0) ; MN-major -> (m0, g*Kw + k) (the producer localises per CTA)
+    ti.ax = 0; ti.ay = g * Mw + ti.m0;
+    ti.bx = 0; ti.by = s_start[g] + ti.n0;
+    return;
+  }
   // find group: prefix[g] <= t < prefix[g+1]
   int lo = 0, hi = p.num_groups - 1;
   while (lo < hi) {
@@ -164,20 +232,7 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, const int* pref
   int r = t - prefix[g];
   ti.g = g;
   ti.ks = 0;
-  if constexpr (kMode == kModeSwap) {
-    const int rows = s_rows[g];
-    const int nb = swap_ntiles<BN>(rows);
-    const int ns = swap_nsize<BN>(rows);
-    const int mb = r / nb, nbk = r % nb;
-    ti.wg = p.w_mod > 0 ? g % p.w_mod : g;
-    ti.m0 = mb * kBM * kCG;
-    ti.n0 = nbk * ns;
-    ti.n = min(ns, rows - ti.n0);
-    ti.k_len = p.Kw;
-    // A (weights): K-major -> (k, g*Mw + m0) ; MN-major -> (m0, g*Kw + k)
-    ti.ax = 0; ti.ay = g * p.Mw + ti.m0;  // overwritten below for MN-major A by caller convention
-    ti.bx = 0; ti.by = s_start[g] + ti.n0;
-  } else if constexpr (kMode == kModeWgrad) {
+  if constexpr (kMode == kModeWgrad) {
     const int nb = p.Nw / BN;
     ti.m0 = (r / nb) * kBM * kCG;
     ti.n0 = (r % nb) * BN;
@@ -313,7 +368,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int total_tiles = prefix[G];
+  const int total_tiles = kMode == kModeSwap ? swap_total_tiles<BN, kCG>(p, prefix) : prefix[G];
 
   if (warp == kProducerWarp) {
     // ------------------------------------------------------------ TMA producer (both CTAs of a pair)
@@ -324,8 +379,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       auto localize = [&](TileInfo& ti) {
         const int my_m0 = ti.m0 + static_cast<int>(rank) * kBM;
         if constexpr (kMode == kModeSwap) {
-          if constexpr (A_MN) { ti.ax = my_m0; ti.ay = ti.wg * p.Kw; }
-          else { ti.ay = ti.wg * p.Mw + my_m0; }
+          const int Mw = ti.phase ? p.Mw2 : p.Mw, Kw = ti.phase ? p.Kw2 : p.Kw;
+          if constexpr (A_MN) { ti.ax = my_m0; ti.ay = ti.wg * Kw; }
+          else { ti.ay = ti.wg * Mw + my_m0; }
           ti.by += static_cast<int>(rank & 1u) * (ti.n / kCGm);  // this CTA's half of the token tile
         } else if constexpr (kMode == kModeWgrad) {
           ti.ax = my_m0;
@@ -338,6 +394,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         TileInfo ti;
         decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, t, ti);
         localize(ti);
+        const CUtensorMap* mA = &tmA;
+        const CUtensorMap* mB = &tmB;
+        if constexpr (EpiChained<Epi>::value) {
+          if (ti.phase) {
+            mA = &ep.tmA2;
+            mB = &ep.tmB2;
+            // the second GEMM's token operand is the first's output: every first-GEMM tile of this (group, token
+            // tile) must have stored its rows
+            ptx::wait_counter_geq(p.ready + ti.g * p.ready_stride + ti.tj, p.ready_target);
+          }
+        }
         // K ranges: wgrad walks the group's (source) sub-segments; every other mode has one range
         const int nsub = (kMode == kModeWgrad) ? p.nsub : 1;
         for (int sub = 0; sub < nsub; ++sub) {
@@ -357,37 +424,37 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             if constexpr (kCG > 1) {
               const uint32_t bar = ptx::mapa(&full_bar[stage], pair_base);
               if constexpr (A_MN) {
-                ptx::tma_load_2d_cg2(sa, &tmA, bar, ti.ax, ti.ay + kb * kBK);
-                ptx::tma_load_2d_cg2(sa + 8192, &tmA, bar, ti.ax + 64, ti.ay + kb * kBK);
+                ptx::tma_load_2d_cg2(sa, mA, bar, ti.ax, ti.ay + kb * kBK);
+                ptx::tma_load_2d_cg2(sa + 8192, mA, bar, ti.ax + 64, ti.ay + kb * kBK);
               } else {
-                ptx::tma_load_2d_cg2(sa, &tmA, bar, ti.ax + kb * kBK, ti.ay);
+                ptx::tma_load_2d_cg2(sa, mA, bar, ti.ax + kb * kBK, ti.ay);
               }
               if constexpr (kCG == 4) {
                 // this pair loads one half of the CTA-half token box; both pairs' CTAs of the same half get it
                 const int pp = static_cast<int>(rank >> 1);
                 const uint16_t mask = static_cast<uint16_t>((1u << (rank & 1u)) | (1u << ((rank & 1u) + 2)));
-                ptx::tma_load_2d_cg2_mc(sb + pp * (L::kBBytes / 2), &tmB, bar, ti.bx + kb * kBK,
+                ptx::tma_load_2d_cg2_mc(sb + pp * (L::kBBytes / 2), mB, bar, ti.bx + kb * kBK,
                                         ti.by + pp * (BN / 4), mask);
               } else if constexpr (B_MN) {
 #pragma unroll
                 for (int j = 0; j < BN / 128; ++j)
-                  ptx::tma_load_2d_cg2(sb + j * 8192, &tmB, bar, ti.bx + 64 * j, ti.by + kb * kBK);
+                  ptx::tma_load_2d_cg2(sb + j * 8192, mB, bar, ti.bx + 64 * j, ti.by + kb * kBK);
               } else {
-                ptx::tma_load_2d_cg2(sb, &tmB, bar, ti.bx + kb * kBK, ti.by);
+                ptx::tma_load_2d_cg2(sb, mB, bar, ti.bx + kb * kBK, ti.by);
               }
             } else {
               if constexpr (A_MN) {
-                ptx::tma_load_2d(sa, &tmA, &full_bar[stage], ti.ax, ti.ay + kb * kBK);
-                ptx::tma_load_2d(sa + 8192, &tmA, &full_bar[stage], ti.ax + 64, ti.ay + kb * kBK);
+                ptx::tma_load_2d(sa, mA, &full_bar[stage], ti.ax, ti.ay + kb * kBK);
+                ptx::tma_load_2d(sa + 8192, mA, &full_bar[stage], ti.ax + 64, ti.ay + kb * kBK);
               } else {
-                ptx::tma_load_2d(sa, &tmA, &full_bar[stage], ti.ax + kb * kBK, ti.ay);
+                ptx::tma_load_2d(sa, mA, &full_bar[stage], ti.ax + kb * kBK, ti.ay);
               }
               if constexpr (B_MN) {
 #pragma unroll
                 for (int j = 0; j < BN / 64; ++j)
-                  ptx::tma_load_2d(sb + j * 8192, &tmB, &full_bar[stage], ti.bx + 64 * j, ti.by + kb * kBK);
+                  ptx::tma_load_2d(sb + j * 8192, mB, &full_bar[stage], ti.bx + 64 * j, ti.by + kb * kBK);
               } else {
-                ptx::tma_load_2d(sb, &tmB, &full_bar[stage], ti.bx + kb * kBK, ti.by);
+                ptx::tma_load_2d(sb, mB, &full_bar[stage], ti.bx + kb * kBK, ti.by);
               }
             }
             if (++stage == L::kStages) { stage = 0; phase ^= 1; }
@@ -499,7 +566,52 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           else ptx::mbar_arrive(&tempty_bar[buf]);
         }
       }
-    } else
+    } else if constexpr (EpiChained<Epi>::value) {
+      // chained launch: the first GEMM's tiles (epilogue Epi::First), then the second's (Epi::Second) -- two loops,
+      // each inlining one epilogue body
+      auto phase_loop = [&](auto ph) {
+        constexpr int PH = decltype(ph)::value;
+        using E = typename std::conditional<PH == 0, typename Epi::First, typename Epi::Second>::type;
+        const auto& epp = Epi::params(ep, ph);
+        for (;; ++it) {
+          const int t = sched_tile(it, cluster_id, num_clusters);
+          if (t >= total_tiles) break;
+          TileInfo ti;
+          decode_tile<kMode, BN, kCG>(p, prefix, s_start, s_rows, t, ti);
+          if (ti.phase != PH) break;  // (first loop) this CTA's second-GEMM tiles start here
+          ti.m0 += static_cast<int>(rank) * kBM;
+          const int buf = it & 1;
+          const uint32_t use = static_cast<uint32_t>(it >> 1);
+          E::prefetch(epp, p, ti, q, h, lane, wsm, s_start);
+          ptx::mbar_wait(&tfull_bar[buf], use & 1);
+          ptx::tc_fence_after();
+          const uint32_t tmem_tile = tmem_base + buf * BN + (static_cast<uint32_t>(q * 32) << 16);
+          auto release = [&]() {
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if constexpr (kCG > 1) ptx::mbar_arrive_remote(ptx::mapa(&tempty_bar[buf], pair_base));
+              else ptx::mbar_arrive(&tempty_bar[buf]);
+            }
+          };
+          E::run(epp, p, ti, tmem_tile, q, h, lane, wsm, s_start, release);
+          if constexpr (PH == 0) {
+            // this warp's rows of a first-GEMM tile are in global memory: count them for the second GEMM's producers
+            if (lane == 0) {
+              ptx::bulk_wait<0>();
+              ptx::fence_proxy_async_global();
+              __threadfence();
+              atomicAdd(p.ready + ti.g * p.ready_stride + ti.tj, 1);
+            }
+            __syncwarp();
+          }
+        }
+      };
+      phase_loop(std::integral_constant<int, 0>{});
+      phase_loop(std::integral_constant<int, 1>{});
+      Epi::First::finish(ep.p0, lane);
+      Epi::Second::finish(ep.p1, lane);
+    } else {
     for (;; ++it) {
       const int t = sched_tile(it, cluster_id, num_clusters);
       if (t >= total_tiles) break;
@@ -528,6 +640,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
     Epi::finish(ep, lane);
+    }
   }
   if constexpr (kCG > 1) ptx::cluster_sync();
   else __syncthreads();

@@ -185,6 +185,7 @@ class Layer {
   __nv_bfloat16 *xp_ = nullptr, *O_ = nullptr, *dO_ = nullptr, *H_ = nullptr, *A_ = nullptr, *dA_ = nullptr,
                 *dxp_ = nullptr, *dz_ = nullptr;
   float *logits_ = nullptr, *dldg_ = nullptr, *dw_part_ = nullptr;
+  int* chain_ready_ = nullptr;  // chained FFN GEMMs' readiness counters (null: separate launches)
   double *penalties_ = nullptr, *loss_part_ = nullptr;
   int n_loss_part_ = 0;
   bool topo_ready_ = false;

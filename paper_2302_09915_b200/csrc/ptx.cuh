@@ -290,6 +290,26 @@ __device__ __forceinline__ float tanh_fast(float x) {
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// generic-proxy <-> async-proxy ordering of global memory (TMA stores / loads vs ordinary loads / atomics)
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+// Spin (one thread) until *p >= v with acquire semantics at gpu scope, then order the caller's subsequent
+// async-proxy (TMA) reads after it.  Traps after ~2 s instead of hanging the GPU.
+__device__ __forceinline__ void wait_counter_geq(const int* p, int v) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (true) {
+    int x;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(x) : "l"(p) : "memory");
+    if (x >= v) break;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 2000000000ull) __trap();
+  }
+  fence_proxy_async_global();
+}
+
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

@@ -208,3 +208,18 @@ def test_c4_one_gpu_shape_value_parity():
     out = run_parity(S=2048, d=4096, dout=4096, N=64, k=2, f=16384, cap=3, cf=1.25)
     print("C4 parity", out)
     _assert(out)
+
+
+def test_c2_parity_with_chained_ffn_gemms():
+    """The chained FFN GEMMs (fwd1 -> fwd2 and dgrad2 -> dgrad1 as single persistent launches with per-(expert,
+    token tile) readiness counters; TAMOE_CHAIN=1, off by default) give the same C2 values (fresh process: the
+    switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, TAMOE_CHAIN="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", os.path.abspath(__file__),
+                        "-k", "test_c2_full_shape_value_parity_and_200_replays"],
+                       capture_output=True, text=True, timeout=900, cwd=root, env=env)
+    assert r.returncode == 0 and "1 passed" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
