@@ -240,8 +240,9 @@ def test_layer_all_tokens_on_one_expert(cap, cf):
     check(layer, o, extra, P, S, N, k, f, True)
 
 
-@pytest.mark.parametrize("k,bad", [(1, float("inf")), (2, float("nan"))])
-def test_layer_non_finite_logit_raises(k, bad):
+@pytest.mark.parametrize("k,bad,N", [(1, float("inf"), 8), (2, float("nan"), 8), (1, float("nan"), 64),
+                                     (2, float("-inf"), 48)])
+def test_layer_non_finite_logit_raises(k, bad, N):
     """gate.cpp:16-17 throws ValidationError("non-finite gate logit").  The stream-ordered step reports it
     deferred: tamoe_layer_status (and the next step, once the bad step completed) returns status 2 through
     the C ABI and the Python mirror raises ValidationError.  The bad row is routed in range (no fault) and
@@ -249,7 +250,7 @@ def test_layer_non_finite_logit_raises(k, bad):
     import ctypes
     from paper_2302_09915_b200 import _lib, ops
     from paper_2302_09915_b200.layer import LayerConfig, TAMoELayer
-    P, S, d, dout, N, f = 1, 256, 256, 128, 8, 256
+    P, S, d, dout, f = 1, 256, 256, 128, 256
     cfg = LayerConfig(P=P, S=S, d=d, d_out=dout, N=N, k=k, f=f, act=1, cap_mode=2, aux_kind=0, need_dx=True)
     layer = TAMoELayer(cfg)
     params = layer.init_params(seed=2)
