@@ -97,6 +97,16 @@ if __name__ == "__main__":
             run(nm + " wgrad2", cnt, 1024, 4096, "wgrad")
             run(nm + " wgrad1", cnt, 4096, 1024, "wgrad")
         sys.exit(0)
+    if "--c4" in sys.argv:
+        c4 = [int(min(c, 640)) for c in rng.multinomial(32768, [1 / 64] * 64)]
+        print("C4 counts: min", min(c4), "max", max(c4), "sum", sum(c4), flush=True)
+        run("C4 fwd1", c4, 16384, 4096)
+        run("C4 fwd2", c4, 4096, 16384)
+        run("C4 dgrad2", c4, 16384, 4096, "dgrad")
+        run("C4 dgrad1", c4, 4096, 16384, "dgrad")
+        run("C4 wgrad2", c4, 4096, 16384, "wgrad")
+        run("C4 wgrad1", c4, 16384, 4096, "wgrad")
+        sys.exit(0)
     bal = list(rng.multinomial(16384, [1 / 64] * 64))
     run("dense 16384 rows", [16384], 4096, 1024)
     run("dense 16384 rows", [16384], 1024, 4096)
