@@ -8,13 +8,15 @@ ARCH    := -gencode arch=compute_100a,code=sm_100a
 NVIDIA_PKG ?= $(shell python -c "import nvidia;print(list(nvidia.__path__)[0])" 2>/dev/null)
 NCCL_INC ?= $(NVIDIA_PKG)/nccl/include
 NCCL_LIB ?= $(NVIDIA_PKG)/nccl/lib
-CUFLAGS := -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr -I$(NCCL_INC)
+EXTRA_CUFLAGS ?=  # A/B builds: make lib EXTRA_CUFLAGS=-DX BUILD=build/ab LIB=.gpujobs/libtamoe_ab.so
+CUFLAGS := -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr -I$(NCCL_INC) \
+           $(EXTRA_CUFLAGS)
 CXXFLAGS := -O3 -std=c++17 -fPIC -Wall -I/usr/local/cuda/include -I$(NCCL_INC)
 
 SRC     := paper_2302_09915_b200/csrc
-BUILD   := build/obj
+BUILD   ?= build/obj
 LIBDIR  := paper_2302_09915_b200/lib
-LIB     := $(LIBDIR)/libtamoe.so
+LIB     ?= $(LIBDIR)/libtamoe.so
 
 CU_SRCS  := $(wildcard $(SRC)/*.cu)
 CPP_SRCS := $(wildcard $(SRC)/*.cpp)
