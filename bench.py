@@ -590,8 +590,10 @@ def main():
     t_hbm = bytes_per_launch / (pk["hbm"] * 1e9)
     t_tc = flop_per_launch / (pk["bf16_sus"] * 1e12)
     hbm_bound = t_hbm > t_tc
-    roof = {"kernel": "expert grouped GEMMs (tcgen05; fwd1, fwd2, dgrad2, wgrad2, wgrad1, dgrad1 -- fwd1+fwd2 and "
-                      "dgrad2+dgrad1 as chained persistent launches)",
+    chained = any(n in phases for n in ("expert_fwd12", "expert_dgrad21"))
+    roof = {"kernel": "expert grouped GEMMs (tcgen05; fwd1, fwd2, dgrad2, wgrad2, wgrad1, dgrad1" +
+                      (" -- fwd1+fwd2 and dgrad2+dgrad1 as chained persistent launches, TAMOE_CHAIN=1)" if chained
+                       else ": six persistent launches per step)"),
             "bound": "hbm" if hbm_bound else "tensor",
             "achieved": gbs if hbm_bound else tflops,
             "peak": pk["hbm"] if hbm_bound else pk["bf16_sus"],

@@ -412,7 +412,7 @@ void grouped_fwd(const __nv_bfloat16* tokens, const __nv_bfloat16* w, int G, int
   const int Gw = w_mod > 0 ? w_mod : G;  // distinct weight matrices
   CUtensorMap ta = make_tmap_bf16(w, K, static_cast<uint64_t>(Gw) * M, K, kBM);
   CUtensorMap tb = make_tmap_bf16(tokens, K, R, K, swap_token_box(pair));
-  GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1, w_mod, 1, 0, 0};
+  GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1, w_mod, 1};
   SwapParams ep = swap_params(out, pre_out, nullptr, M, R, act, kActNone);
   require(!(push && pre_out), "grouped_fwd: push needs a plain output");
   if (push) {
@@ -436,7 +436,7 @@ void grouped_dgrad(const __nv_bfloat16* grad_tokens, const __nv_bfloat16* w, int
   const int Gw = w_mod > 0 ? w_mod : G;
   CUtensorMap ta = make_tmap_bf16(w, M, static_cast<uint64_t>(Gw) * K, M, 64);
   CUtensorMap tb = make_tmap_bf16(grad_tokens, K, R, K, swap_token_box(pair));
-  GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1, w_mod, 1, 0, 0};
+  GemmParams p{G, seg_start, seg_rows, M, 0, K, 1, 1, 1, 1, w_mod, 1};
   SwapParams ep = swap_params(out, nullptr, pre_in, M, R, kActNone, pre_in ? act : kActNone);
   require(!(push && pre_in), "grouped_dgrad: push needs a plain output");
   if (push) {
@@ -458,7 +458,7 @@ void grouped_wgrad(const __nv_bfloat16* a_tokens, const __nv_bfloat16* b_tokens,
   CUtensorMap ta = make_tmap_bf16(a_tokens, M, R, M, 64);
   CUtensorMap tb = make_tmap_bf16(b_tokens, N, R, N, 64);
   require(nsub >= 1 && G * nsub <= kMaxGroups, "grouped_wgrad: too many sub-segments");
-  GemmParams p{G, seg_start, seg_rows, M, N, 0, 1, 1, 1, 1, 0, nsub, 0, 0};
+  GemmParams p{G, seg_start, seg_rows, M, N, 0, 1, 1, 1, 1, 0, nsub};
   EpiWgrad::Params ep{make_tmap_bf16_box(out, N, static_cast<uint64_t>(G) * M, N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)};
   launch_pair_or_single<kModeWgrad, 256, true, true, EpiWgrad>(M % 256 == 0 ? 2 : 1, ta, tb, p, ep, s);
 }
@@ -484,7 +484,7 @@ void grouped_ffn_fwd_chain(const __nv_bfloat16* tokens, const __nv_bfloat16* w1,
   const int Gw = w_mod > 0 ? w_mod : G;
   CUtensorMap ta = make_tmap_bf16(w1, d, static_cast<uint64_t>(Gw) * f, d, kBM);
   CUtensorMap tb = make_tmap_bf16(tokens, d, R, d, swap_token_box(2));
-  GemmParams p{G, seg_start, seg_rows, f, 0, d, 1, 1, 1, 1, w_mod, 1, 0, 0};
+  GemmParams p{G, seg_start, seg_rows, f, 0, d, 1, 1, 1, 1, w_mod, 1};
   const int stride = chain_ready_stride(R);
   chain_params(p, d_out, f, ready, stride, f);
   TAMOE_CUDA(cudaMemsetAsync(ready, 0, sizeof(int) * static_cast<size_t>(G) * stride, s));
@@ -514,7 +514,7 @@ void grouped_ffn_dgrad_chain(const __nv_bfloat16* dO, const __nv_bfloat16* w2, c
   const int Gw = w_mod > 0 ? w_mod : G;
   CUtensorMap ta = make_tmap_bf16(w2, f, static_cast<uint64_t>(Gw) * d_out, f, 64);
   CUtensorMap tb = make_tmap_bf16(dO, d_out, R, d_out, swap_token_box(2));
-  GemmParams p{G, seg_start, seg_rows, f, 0, d_out, 1, 1, 1, 1, w_mod, 1, 0, 0};
+  GemmParams p{G, seg_start, seg_rows, f, 0, d_out, 1, 1, 1, 1, w_mod, 1};
   const int stride = chain_ready_stride(R);
   chain_params(p, d, f, ready, stride, f);
   TAMOE_CUDA(cudaMemsetAsync(ready, 0, sizeof(int) * static_cast<size_t>(G) * stride, s));

@@ -667,7 +667,7 @@ void gate_forward(const __nv_bfloat16* x, const __nv_bfloat16* wg, int n_pad, co
   const long long T = static_cast<long long>(d.P) * d.S;
   CUtensorMap ta = make_tmap_bf16(x, dm, T, dm, kBM);
   CUtensorMap tb = make_tmap_bf16(wg, dm, static_cast<uint64_t>(d.P) * n_pad, dm, BNsel);
-  GemmParams p{1, nullptr, nullptr, 0, n_pad, dm, 1, d.S, n_pad, d.P, 0, 1, 0, 0};
+  GemmParams p{1, nullptr, nullptr, 0, n_pad, dm, 1, d.S, n_pad, d.P, 0, 1};
   if (gate_is_fused(d.N, o.probs != nullptr)) {
     // one launch: logits GEMM + per-token routing in the epilogue
     static const int probe = [] {

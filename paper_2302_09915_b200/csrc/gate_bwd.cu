@@ -336,7 +336,7 @@ void gate_dw(const __nv_bfloat16* x, const __nv_bfloat16* dz, int P, int S, int 
   const long long T = static_cast<long long>(P) * S;
   CUtensorMap ta = make_tmap_bf16(x, d, T, d, 64);     // A = x^T (MN-major)
   CUtensorMap tb = make_tmap_bf16(dz, n64, T, n64, 64);  // B = dz   (MN-major)
-  GemmParams p{1, nullptr, nullptr, d, 64, 0, splits, S, 0, P, 0, 1, 0, 0};
+  GemmParams p{1, nullptr, nullptr, d, 64, 0, splits, S, 0, P, 0, 1};
   // one 64-column N block per launch keeps BN = 64 (n64 > 64 loops over column blocks)
   EpiGateDw::Params ep{part, d, n64, P, finalize ? 1 : 0, finalize ? *finalize : GateDzArgs{}};
   if (n64 == 64) {
@@ -364,7 +364,7 @@ void gate_dx(const __nv_bfloat16* dz, const __nv_bfloat16* wg, int P, int S, int
   const long long T = static_cast<long long>(P) * S;
   CUtensorMap ta = make_tmap_bf16(dz, n64, T, n64, 128);                         // A = dz (K-major)
   CUtensorMap tb = make_tmap_bf16(wg, d, static_cast<uint64_t>(P) * n_pad, d, 64);  // B = Wg (MN-major)
-  GemmParams p{1, nullptr, nullptr, 0, d, n_pad, 1, S, n_pad, P, 0, 1, 0, 0};
+  GemmParams p{1, nullptr, nullptr, 0, d, n_pad, 1, S, n_pad, P, 0, 1};
   // tile-ahead TMA path: top-1 / top-2, local expert-path rows, and 32-token warp groups that never straddle
   // two processes (the TMA store writes whole 32-row boxes; rows past T are clipped)
   static const bool ahead_on = [] {

@@ -48,8 +48,6 @@ struct GemmParams {
   int procs;             // logical processes (gate modes)
   int w_mod;             // kModeSwap: weight of group g is g % w_mod (0: g) -- (source, expert) segments
   int nsub;              // kModeWgrad: K of group g = sub-segments s*num_groups + g, s < nsub
-  int pf_dist;           // unused (an L2 prefetch experiment, measured no gain)
-  int pf_b;              // unused
   // kModeSwap chain: a second swap GEMM (Mw2 x Kw2, tensor maps / epilogue from EpiChain) whose token operand is
   // the first one's output, in the same persistent launch.  Its tiles follow the first GEMM's in the schedule; a
   // CTA reaching a second-GEMM tile waits until every first-GEMM tile of that (group, token tile) has stored its
