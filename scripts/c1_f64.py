@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """BASELINE config 1 (the reference's CPU layer: d=512, 8 experts, top-2, 4096 tokens, RE-1 [2,2] topology,
-topo loss + proportional capacity 1.25) in the reference's own precision on the device (tamoe_layer_step_f64)
-next to the reference's train() step (oracle/_ref, one host core).  Prints one JSON line.
+topo loss + proportional capacity 1.25) in the reference's own precision on the device (tamoe_layer_step_f64).
+Prints one JSON line.  The comparison with the reference's own train() (compiled from its sources) is test
+infrastructure and lives in tests/test_gpu_layer_f64.py::test_c1_trajectory_vs_reference_train.
 
   python scripts/c1_f64.py [--reps 20]
 """
@@ -22,7 +23,6 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
     args = ap.parse_args()
-    import oracle
     from paper_2302_09915_b200 import ops
     P, S, d, dout, N, k = 4, 1024, 512, 512, 8, 2
     rng = np.random.default_rng(0)
@@ -50,13 +50,6 @@ def main():
     line = {"config": "C1: d=512 d_out=512 N=8 top-2 P=4 x S=1024 fp64 linear experts, topo loss, proportional cf 1.25",
             "gpu_step_ms": gpu_ms, "gpu_tokens_per_s": P * S / (gpu_ms / 1e3),
             "task_loss": o["task_loss"], "aux_loss": o["aux_loss"]}
-    if oracle.ref_available():
-        R = oracle.ref()
-        r1 = R.train(x, y, gates, U, kind=1, cap_mode=3, cf=1.25, c_hat=c_hat, lr=0.0, steps=1, k=k)
-        line.update(ref_step_s=r1["seconds"], ref_tokens_per_s=P * S / r1["seconds"], ref_cores=1,
-                    ref_task_loss=float(r1["task_loss"][0]), ref_aux_loss=float(r1["aux_loss"][0]),
-                    task_loss_rel_diff=abs(o["task_loss"] - r1["task_loss"][0]) / abs(r1["task_loss"][0]),
-                    aux_loss_rel_diff=abs(o["aux_loss"] - r1["aux_loss"][0]) / abs(r1["aux_loss"][0]))
     print(json.dumps(line), flush=True)
 
 
