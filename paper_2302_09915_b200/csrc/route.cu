@@ -359,60 +359,72 @@ __global__ void __launch_bounds__(kPermWarps * 32) route_permute_kernel(RouteDim
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rows = min(total, r_max);
-  // Under expert parallelism the rows are owner-major; every rank starts at its own owner segment and walks
-  // the owners cyclically, so at any moment the P senders target P different receivers (no incast on rank 0).
-  const int rot = (map.P > 1 && me * map.E < N && rows > 0) ? min(start[me * map.E], rows) % rows : 0;
-  // warps stride over the rows (the block's expert scan above is amortised over many rows)
-  for (int rl = blockIdx.x * kPermWarps + warp; rl < rows; rl += gridDim.x * kPermWarps) {
-  const int r = rl + rot < rows ? rl + rot : rl + rot - rows;
-  int lo = 0, hi = N - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (start[mid] <= r) lo = mid; else hi = mid - 1;
-  }
-  const int e = lo;
-  const int j = r - start[e];
-  const int dst_rank = map.rank_of(e);
-  const long long drow = map.P == 1 ? r : static_cast<long long>(r) - start[e] + map.dst_off[e];
-  uint4* dst = reinterpret_cast<uint4*>(xp.p[dst_rank] + drow * dx);
-  const int nv = dx / 8;
-  const int rep = xp.rep[dst_rank];
-  if (j < cnt[e]) {
-    const int pick = b.clist[b.list_start[e] + j];
-    const long long tok = pick / d.k;
-    if (lane == 0) {
-      b.pos[pick] = r;
-      if (has_codes) codes.p[dst_rank][drow] = (me << kPushRowBits) | pick;
+  // Under expert parallelism the rows are owner-major.  With at least one block per owner, the blocks are dealt
+  // to the owners round robin (block b serves owner (me + b) % W), so this rank's stores to every peer and its local
+  // copies run concurrently from the start and, rank by rank, the peers are offset (no incast); otherwise every rank
+  // starts at its own owner segment and walks the owners cyclically.
+  auto move_row = [&](int r) {
+    int lo = 0, hi = N - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (start[mid] <= r) lo = mid; else hi = mid - 1;
     }
-    const uint4* src = reinterpret_cast<const uint4*>(x + tok * dx);
-    // whole row in registers first (up to 8 x 16 B per lane), then the stores back to back
-    constexpr int kU = 8;
-    for (int v0 = lane; v0 < nv; v0 += 32 * kU) {
-      uint4 t[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u)
-        if (v0 + 32 * u < nv) t[u] = __ldg(src + v0 + 32 * u);
-#pragma unroll
-      for (int u = 0; u < kU; ++u)
-        if (v0 + 32 * u < nv) dst[v0 + 32 * u] = t[u];
-      if (rep > 1) {
+    const int e = lo;
+    const int j = r - start[e];
+    const int dst_rank = map.rank_of(e);
+    const long long drow = map.P == 1 ? r : static_cast<long long>(r) - start[e] + map.dst_off[e];
+    uint4* dst = reinterpret_cast<uint4*>(xp.p[dst_rank] + drow * dx);
+    const int nv = dx / 8;
+    const int rep = xp.rep[dst_rank];
+    if (j < cnt[e]) {
+      const int pick = b.clist[b.list_start[e] + j];
+      const long long tok = pick / d.k;
+      if (lane == 0) {
+        b.pos[pick] = r;
+        if (has_codes) codes.p[dst_rank][drow] = (me << kPushRowBits) | pick;
+      }
+      const uint4* src = reinterpret_cast<const uint4*>(x + tok * dx);
+      // whole row in registers first (up to 8 x 16 B per lane), then the stores back to back
+      constexpr int kU = 8;
+      for (int v0 = lane; v0 < nv; v0 += 32 * kU) {
+        uint4 t[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u)
-          if (v0 + 32 * u < nv) store_repeat(dst + v0 + 32 * u, t[u], rep);
+          if (v0 + 32 * u < nv) t[u] = __ldg(src + v0 + 32 * u);
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+          if (v0 + 32 * u < nv) dst[v0 + 32 * u] = t[u];
+        if (rep > 1) {
+#pragma unroll
+          for (int u = 0; u < kU; ++u)
+            if (v0 + 32 * u < nv) store_repeat(dst + v0 + 32 * u, t[u], rep);
+        }
+      }
+    } else {
+      if (lane == 0 && has_codes) codes.p[dst_rank][drow] = (me << kPushRowBits) | trash_row;
+      const uint4 z = make_uint4(0, 0, 0, 0);
+      for (int v = lane; v < nv; v += 32) {
+        dst[v] = z;
+        if (rep > 1) store_repeat(dst + v, z, rep);
+      }
+      if (has_z) {
+        uint4* zd = reinterpret_cast<uint4*>(zrows.p[dst_rank] + drow * zdim);
+        for (int v = lane; v < zdim / 8; v += 32) zd[v] = z;
       }
     }
+  };
+  const int W = map.P;
+  if (W > 1 && static_cast<int>(gridDim.x) >= W && me * map.E < N) {
+    const int j = blockIdx.x % W;
+    const int o = (me + j) % W;
+    const int nb = (static_cast<int>(gridDim.x) - j + W - 1) / W;
+    const int lo = min(start[o * map.E], rows);
+    const int hi = o + 1 < W ? min(start[(o + 1) * map.E], rows) : rows;
+    for (int r = lo + static_cast<int>(blockIdx.x / W) * kPermWarps + warp; r < hi; r += nb * kPermWarps) move_row(r);
   } else {
-    if (lane == 0 && has_codes) codes.p[dst_rank][drow] = (me << kPushRowBits) | trash_row;
-    const uint4 z = make_uint4(0, 0, 0, 0);
-    for (int v = lane; v < nv; v += 32) {
-      dst[v] = z;
-      if (rep > 1) store_repeat(dst + v, z, rep);
-    }
-    if (has_z) {
-      uint4* zd = reinterpret_cast<uint4*>(zrows.p[dst_rank] + drow * zdim);
-      for (int v = lane; v < zdim / 8; v += 32) zd[v] = z;
-    }
-  }
+    const int rot = (W > 1 && me * map.E < N && rows > 0) ? min(start[me * map.E], rows) % rows : 0;
+    for (int rl = blockIdx.x * kPermWarps + warp; rl < rows; rl += gridDim.x * kPermWarps)
+      move_row(rl + rot < rows ? rl + rot : rl + rot - rows);
   }
 }
 
